@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""DABA hot-path benchmark (BASELINE.json metric: observations/sec per DABA iteration, % HBM roofline).
+
+One step = one DABA iteration (Algorithm 1) over the whole synthetic BAL Final-13682-shaped problem
+(BASELINE.json configs[3]: 13,682 cameras, 4,456,117 points, 28,987,644 observations, Huber loss), fp64.
+N = 1: one B200.  N > 1 (torchrun, one rank per GPU): the same problem partitioned across the ranks (strong
+scaling; NCCL halo exchange + one allreduce per iteration).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config final13682] [--impl reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "observations/sec per DABA iteration"
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_FMA_PEAK = 17.06e12  # measured DFMA/s, profiles/r01_day0_micro.log (148 SMs, full chip, independent chains)
+
+# Algorithmic bytes: what the kernel must move at least once per launch.
+#   camera pass (both anchors): per observation u (16 B) + point index (4 B); per point x^k and x^{k-1} (2 x 24 B)
+#   point pass: per observation u (16 B) + camera index (4 B); per point ptr (8 B) + read x^k, x^{k-1} (48 B) +
+#               write two candidates (48 B)
+BYTES = {
+    "k_cam_pass": lambda K, N, M: 20 * K + 48 * N + 2 * 128 * M,
+    "k_pt_pass": lambda K, N, M: 20 * K + 104 * N + 2 * 128 * M,
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="final13682")
+    ap.add_argument("--impl", default="daba", choices=["daba", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def sample_problem(p, max_obs):
+    """Induced sub-problem on the first cameras whose observations total <= max_obs (for the CPU oracle)."""
+    import numpy as np
+
+    import gen
+    counts = np.bincount(p.obs_cam, minlength=p.M)
+    m = int(np.searchsorted(np.cumsum(counts), max_obs))
+    m = max(1, min(m, p.M))
+    sel = p.obs_cam < m
+    pts_used = np.unique(p.obs_pt[sel])
+    remap = np.full(p.N, -1, np.int64)
+    remap[pts_used] = np.arange(pts_used.size)
+    return gen.Problem(p.name + f"[cams<{m}]", p.cams[:m].copy(), p.pts[pts_used].copy(),
+                       p.obs_cam[sel].astype(np.int32), remap[p.obs_pt[sel]].astype(np.int32), p.obs_uv[sel].copy(),
+                       p.gt_cams[:m].copy(), p.gt_pts[pts_used].copy(), p.loss, p.loss_scale)
+
+
+def run_oracle_sample(p, max_obs, iters):
+    import oracle
+    sp = sample_problem(p, max_obs)
+    o = oracle.Oracle(sp)
+    t0 = time.perf_counter()
+    o.iterate(iters)
+    dt = time.perf_counter() - t0
+    o.close()
+    return sp, dt
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import numpy as np
+
+    import gen
+
+    if a.impl == "reference":
+        # The reference arm is the CPU oracle, as it stands, on the box's host cores (rank 0 only).
+        if rank != 0:
+            return
+        p = gen.generate(a.config)
+        sp = sample_problem(p, 60_000)
+        import oracle
+        o = oracle.Oracle(sp)
+        o.iterate(max(a.warmup, 0))
+        t0 = time.perf_counter()
+        o.iterate(a.steps)
+        dt = time.perf_counter() - t0
+        v = a.steps * sp.K / dt
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "obs/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": a.config, "sample": sp.name, "sample_obs": int(sp.K)},
+            "cpu_baseline": {"value": v, "unit": "obs/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{sp.name}: {sp.K} observations, {a.steps} iterations"},
+            "e2e": {"value": v, "unit": "obs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_07026_b200 as daba
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    p = gen.generate(a.config)
+    comm_key = None
+    if world > 1:
+        obj = [daba.comm_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm_key = obj[0]
+    stream = torch.cuda.Stream(device=local)
+    kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, comm_key=comm_key, device=local)
+
+    # ---------------- device-resident timed region (production path: one CUDA graph per iteration)
+    s = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, **kw)
+    lpi = s.launches_per_iteration()
+    with torch.cuda.stream(stream):
+        s.iterate(a.warmup)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            time.sleep(0.3)
+            e0.record(stream)
+            s.iterate(a.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    F_end = s.objective()
+    info = s.shard_info()
+    s.close()
+
+    # ---------------- per-kernel times: the same steps with CUDA events around every launch (same stream)
+    sp_ = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, profile=1, **kw)
+    with torch.cuda.stream(stream):
+        sp_.iterate(a.warmup)
+        torch.cuda.synchronize()
+        sp_.reset_kernel_times()
+        if world > 1:
+            dist.barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        sp_.iterate(a.steps)
+        q1.record(stream)
+        torch.cuda.synchronize()
+    prof_ms = q0.elapsed_time(q1)
+    kt = sp_.kernel_times()
+    sp_.close()
+
+    # ---------------- e2e through the public API from pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        hc, hpnt, hoc, hop, huv = map(pin, (p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        se = daba.Solver(hc, hpnt, hoc, hop, huv, stream=stream.cuda_stream, **kw)
+        Ftr, _ = se.iterate(a.steps, F_trace=True)
+        cams_out, pts_out, _ = se.state()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        se.close()
+        if world > 1:
+            t = torch.tensor([te], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        h2d = (hc.nbytes + hpnt.nbytes + hoc.nbytes + hop.nbytes + huv.nbytes) / a.steps
+        d2h = (8 * a.steps + 1 * a.steps + cams_out.nbytes + pts_out.nbytes) / a.steps
+        e2e = {"value": a.steps * p.K / te, "unit": "obs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "includes": "daba_create (host shard plan + H2D) + iterations with "
+               "per-step F readback + daba_get_state"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- cpu baseline: the oracle on a bounded sample, rank 0, N = 1 only
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        spb, dt = run_oracle_sample(p, 2_000_000, 2)
+        cpu = {"value": 2 * spb.K / dt, "unit": "obs/s", "cores": 1, "kind": "oracle",
+               "sample": f"{spb.name}: {spb.K} of {p.K} observations, 2 iterations, single thread"}
+
+    value = a.steps * p.K / (ms * 1e-3)
+    hbm, hbm_src = peaks()
+    # dominant kernel and its roofline
+    dom = max(kt.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dl) = dom
+    per_launch_ms = dms / max(dl, 1)
+    kshare = {k: round(v[0] / prof_ms, 4) for k, v in kt.items()}
+    roof = None
+    if dname in BYTES:
+        byt = BYTES[dname](info["cam_side_obs"] if dname == "k_cam_pass" else info["pt_side_obs"],
+                           info["own_pts"] + info["halo_pts"], info["own_cams"])
+        ach = byt / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                "traffic": None, "kernel": dname, "bytes_per_launch": int(byt),
+                "kernel_ms_per_launch": round(per_launch_ms, 5), "peak_source": hbm_src}
+    out = {
+        "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": a.config, "cameras": p.M, "points": p.N, "observations": int(p.K),
+                   "loss": ["trivial", "huber", "cauchy"][p.loss], "parallelism": f"camera-partitioned x{world}",
+                   "l2": "inputs larger than L2 (observation streams 1.2 GB, point states 4 x 143 MB)",
+                   "F_end": F_end},
+        "roofline": roof,
+        "kernel_share": kshare,
+        "profiled_ms_per_step": prof_ms / a.steps,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": lpi * a.steps,
+        "clocks": clk.summary(),
+        "shard": info,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/* include/daba.h — C-ABI of the B200-native DABA hot path (libdaba.so).
+ *
+ * DABA = Decentralized and Accelerated Bundle Adjustment (Fan et al., arXiv 2305.07026).
+ * Citations "P:L<n>" refer to the paper's LaTeX line n.
+ *
+ * One call of daba_iterate(ctx, n, ...) runs n iterations of Algorithm 1
+ * under the readings listed in DESIGN.md: every observation is majorized by
+ * Proposition 1, cameras take one successful Levenberg-Marquardt step,
+ * points take the exact closed-form minimiser, Nesterov extrapolation (eqs.
+ * nesterov_x0 / nesterov_x) with the adaptive restart test
+ * E(x^{k+1}|x^k) > F-bar^{(k)} evaluated on one allreduced pair of
+ * scalars.  All arithmetic is fp64 on the GPU; nothing runs on the host between
+ * create and get_state.
+ *
+ * Conventions (all calls):
+ *   - return value: 0 (DABA_OK) or a negative DABA_E_* code; daba_last_error(ctx)
+ *     gives a human-readable reason for the last failure on that context;
+ *   - every pointer argument is a HOST pointer unless stated otherwise; arrays are
+ *     little-endian, row-major, caller-owned and copied during the call;
+ *   - calls on one context are not thread-safe; distinct contexts are independent.
+ *
+ * Camera layouts:
+ *   BAL (9 doubles):    angle-axis of R_w2c, t_w2c (3), f, k1, k2, with x_cam = R_w2c x + t_w2c.
+ *   native (15 doubles): R (3x3 row-major, camera -> world), t (camera centre), d = (f, f k1, f k2);
+ *                        the paper's variables: x_cam = R^T (l - t).
+ *   Conversion: R = Exp(aa)^T, t = -R t_w2c, d = (f, f k1, f k2).  k1, k2 are the paper's
+ *   UNDISTORTION coefficients on centred pixel coordinates (eq. reprojection1).
+ */
+#ifndef DABA_H
+#define DABA_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DABA_ABI_VERSION 1
+
+enum {
+  DABA_OK = 0,
+  DABA_E_INVALID_ARG = -1, /* null/negative sizes, index out of range, duplicate (i,j), scale<=0, xi<=0, eta not in (0,1] */
+  DABA_E_DEGENERATE = -2,  /* Assumption 2 fails at create: ||l_j - t_i|| <= eps for some observation */
+  DABA_E_CUDA = -3,        /* CUDA runtime error (message in daba_last_error) */
+  DABA_E_NCCL = -4,        /* NCCL error or unavailable library */
+  DABA_E_OOM = -5,         /* device or host allocation failed */
+  DABA_E_STATE = -6        /* call not valid in the context's state */
+};
+
+typedef enum { DABA_LOSS_TRIVIAL = 0, DABA_LOSS_HUBER = 1, DABA_LOSS_CAUCHY = 2 } daba_loss_kind;
+
+/* Robust loss rho(s) of eq. Fij, s = ||e||^2; all satisfy Assumption 1.
+ *   trivial: rho = s;  Huber(delta): s <= delta^2 ? s : 2 delta sqrt(s) - delta^2;
+ *   Cauchy(delta): delta^2 log(1 + s / delta^2).   scale = delta > 0, in ||e|| units. */
+typedef struct {
+  daba_loss_kind kind;
+  double scale;
+} daba_loss;
+
+enum { DABA_COMM_NCCL = 0, DABA_COMM_LOCAL = 1 };
+
+typedef struct {
+  double xi;          /* proximal weight xi > 0 of eq. Ealpha; default 1e-4 */
+  double eta;         /* restart averaging eta in (0,1] of eq. lFak; default 0.1 */
+  double lm_mu0;      /* initial Marquardt damping; default 1e-3 */
+  double lm_mu_up;    /* damping growth per failed trial; default 10 */
+  double eps;         /* Assumption 2 threshold on ||l - t||; default 1e-8 */
+  int lm_max_trials;  /* LM trials per camera per anchor, 1..8; default 5 */
+  int accelerate;     /* 1: DABA (Nesterov + restart); 0: DUBA ablation, plain MM; default 1 */
+  int comm;           /* DABA_COMM_NCCL (one process per GPU) or DABA_COMM_LOCAL (ranks = host threads of one
+                         process sharing a hub; used by tests to run several ranks on one GPU); default NCCL */
+  int use_graph;      /* 1: capture one iteration as a CUDA graph and replay it; default 1 */
+  int profile;        /* 1: record CUDA events around every kernel (see daba_kernel_times); default 0 */
+  void* stream;       /* cudaStream_t to launch on (NULL: a stream owned by the context) */
+} daba_options;
+
+/* Fill *o with the defaults above. */
+void daba_default_options(daba_options* o);
+
+typedef struct daba_ctx daba_ctx; /* opaque; owned by the library until daba_destroy */
+
+/* Create a solver context on `cuda_device` for rank `rank` of `nranks`.
+ *   cameras   M x 9 BAL initial cameras x^0;           points N x 3 initial points (world);
+ *   obs_cam, obs_pt: K observation indices (cameras < M, points < N, each (i,j) at most once);
+ *   obs_uv    K x 2 observed pixels u_ij, centred coordinates;
+ *   loss      robust loss;
+ *   cam_owner M ranks, or NULL: contiguous camera ranges balanced by observation count;
+ *   pt_owner  N ranks, or NULL: the rank owning most of the point's observations, ties -> lowest rank;
+ *   comm_id   128 bytes: an ncclUniqueId from daba_comm_id (DABA_COMM_NCCL) or any 128-byte key shared by the
+ *             ranks of one DABA_COMM_LOCAL group; may be NULL iff nranks == 1;
+ *   opt       options or NULL for defaults.
+ * Every rank passes the same global arrays; each keeps its shard (owned cameras/points and the observations
+ * touching them) plus the boundary (halo) states it reads.  Collective when nranks > 1: all ranks must call it.
+ * Sets x^{-1} = x^0, s^{(0)} = 1 and F-bar^{(-1)} = F(x^0) (eq. Fainit, global form).
+ * Errors: DABA_E_INVALID_ARG, DABA_E_DEGENERATE, DABA_E_CUDA, DABA_E_NCCL, DABA_E_OOM.  *out is NULL on error. */
+int daba_create(const double* cameras, int64_t M, const double* points, int64_t N, const int32_t* obs_cam,
+                const int32_t* obs_pt, const double* obs_uv, int64_t K, daba_loss loss, const int32_t* cam_owner,
+                const int32_t* pt_owner, int rank, int nranks, const void* comm_id, int cuda_device,
+                const daba_options* opt, daba_ctx** out);
+
+/* Write a fresh 128-byte NCCL unique id into id_out (rank 0 calls this and broadcasts it).  DABA_E_NCCL if the
+ * NCCL library cannot be loaded. */
+int daba_comm_id(void* id_out);
+
+/* Run n_iters iterations (collective when nranks > 1).  Optional per-iteration outputs (host, may be NULL):
+ *   F_trace[k]       = F(x^k), eq. Fobj, the same on every rank;
+ *   restart_trace[k] = 1 if the restart fired (x^{k+1} from eq. update_mm), else 0.
+ * The call is asynchronous w.r.t. the host only when both traces are NULL and no error occurs. */
+int daba_iterate(daba_ctx* ctx, int n_iters, double* F_trace, uint8_t* restart_trace);
+
+/* Extended per-iteration trace: n_iters x DABA_TRACE_COLS doubles (host). */
+enum { DABA_TR_F = 0, DABA_TR_FBAR, DABA_TR_EACC, DABA_TR_RESTART, DABA_TR_EMM, DABA_TR_STEP2, DABA_TR_GAMMA,
+       DABA_TR_NDEGEN, DABA_TR_NOACC_ACC, DABA_TR_NOACC_MM, DABA_TRACE_COLS };
+int daba_iterate_trace(daba_ctx* ctx, int n_iters, double* trace);
+
+/* F(x^k) at the current iterate (eq. Fobj), identical on every rank (collective when nranks > 1). */
+int daba_objective(daba_ctx* ctx, double* F_out);
+
+/* Current iterate x^k in BAL layout (cameras_out M x 9, points_out N x 3, either may be NULL).  Each rank writes
+ * only the entries it owns; owned_mask_out (M + N bytes, nullable) receives 1 for those entries. */
+int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points_out, uint8_t* owned_mask_out);
+
+/* Native-layout state.  which = 0: x^k, 1: x^{k-1}.  cameras_out M x 15, points_out N x 3 (owned entries). */
+int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_out, double* points_out,
+                          uint8_t* owned_mask_out);
+
+/* Overwrite x^k and x^{k-1} (native layout, GLOBAL arrays, every rank passes the same) together with the
+ * schedule state s^{(k)} and F-bar^{(k-1)}: an exact resume point of Algorithm 1.  Collective. */
+int daba_set_state_native(daba_ctx* ctx, const double* cams_k, const double* pts_k, const double* cams_km1,
+                          const double* pts_km1, double s, double Fbar);
+
+/* Schedule state: s^{(k)} and F-bar^{(k-1)} of the next iteration, and the iteration counter k. */
+int daba_get_schedule(daba_ctx* ctx, double* s, double* Fbar, int64_t* k);
+
+/* Accepted LM trial index per OWNED camera in the last iteration (-1: none accepted), for the accelerated and
+ * the MM anchor; arrays of M int32 (global ids, non-owned entries untouched). */
+int daba_last_decisions(daba_ctx* ctx, int32_t* trial_acc, int32_t* trial_mm);
+
+/* Sizes of this rank's shard. info[0..7] = owned cams, owned points, halo cams, halo points, camera-side obs,
+ * point-side obs, bytes sent per iteration, device bytes allocated. */
+int daba_shard_info(daba_ctx* ctx, int64_t info[8]);
+
+/* The cudaStream_t the context launches on (for events / synchronisation by the caller). */
+void* daba_stream(daba_ctx* ctx);
+
+/* Per-kernel device time summed since the last reset, requires opt.profile = 1.  names_out receives a
+ * '\n'-separated list of kernel names (buffer of `cap` bytes), ms_out/launches_out one entry per name (up to 32).
+ * Returns the number of entries (>= 0) or an error code. */
+int daba_kernel_times(daba_ctx* ctx, char* names_out, size_t cap, double* ms_out, int64_t* launches_out);
+int daba_reset_kernel_times(daba_ctx* ctx);
+
+/* Number of kernel launches one iteration performs on this rank. */
+int daba_launches_per_iteration(daba_ctx* ctx);
+
+const char* daba_last_error(const daba_ctx* ctx);
+void daba_destroy(daba_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

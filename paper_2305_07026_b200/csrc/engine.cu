@@ -1,0 +1,747 @@
+// engine.cu — per-rank DABA engine behind the C-ABI of include/daba.h.
+//
+// Host work happens only in daba_create / daba_set_state_native / daba_get_state: shard planning, layout
+// conversion, uploads.  daba_iterate enqueues device work only (optionally replaying a captured CUDA graph);
+// the restart decision, the role rotation and the schedule live on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/daba.h"
+#include "comm.h"
+#include "kernels.h"
+#include "shard.h"
+
+using namespace daba;
+
+struct daba_ctx {
+  std::string err;
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  daba_options opt{};
+  daba_loss loss{};
+  ShardPlan plan;
+  std::unique_ptr<Comm> comm;
+  std::vector<void*> allocs;
+  size_t dev_bytes = 0;
+  IterParams P{};
+  int64_t host_k = 0;
+  // halo exchange
+  std::vector<PeerSeg> segs;
+  std::vector<std::pair<int64_t, int64_t>> peer_cam_idx, peer_pt_idx;  // (offset, count) into the index arrays
+  int32_t *d_send_cam = nullptr, *d_send_pt = nullptr, *d_recv_cam = nullptr, *d_recv_pt = nullptr;
+  double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  int launches_per_iter = 0;
+  // profiling
+  std::vector<std::string> knames;
+  std::vector<double> kms;
+  std::vector<int64_t> klaunches;
+  struct Pending {
+    int name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+namespace {
+
+int fail(daba_ctx* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+
+#define CUDA_OR(ctx, x)                                                                          \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return fail(ctx, DABA_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+int dalloc(daba_ctx* c, T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+  if (e != cudaSuccess) return fail(c, e == cudaErrorMemoryAllocation ? DABA_E_OOM : DABA_E_CUDA,
+                                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  c->allocs.push_back(*p);
+  c->dev_bytes += n * sizeof(T);
+  return DABA_OK;
+}
+
+template <class T>
+int upload(daba_ctx* c, T** p, const std::vector<T>& h) {
+  int rc = dalloc(c, p, h.size());
+  if (rc) return rc;
+  if (!h.empty()) CUDA_OR(c, cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  return DABA_OK;
+}
+
+// BAL (angle-axis R_w2c, t_w2c, f, k1, k2) -> native (R camera->world, centre t, d = (f, f k1, f k2)).
+void bal_to_native(const double* b, double* c) {
+  const double wx = b[0], wy = b[1], wz = b[2];
+  const double th2 = wx * wx + wy * wy + wz * wz;
+  double A, B;
+  if (th2 < 1e-16) {
+    A = 1.0 - th2 / 6.0;
+    B = 0.5 - th2 / 24.0;
+  } else {
+    const double th = std::sqrt(th2);
+    A = std::sin(th) / th;
+    const double h = std::sin(0.5 * th);
+    B = 2.0 * h * h / th2;
+  }
+  // Q = R_w2c = I + A [w]x + B [w]x^2
+  const double Q[9] = {1.0 + B * (wx * wx - th2), -A * wz + B * wx * wy,     A * wy + B * wx * wz,
+                       A * wz + B * wx * wy,      1.0 + B * (wy * wy - th2), -A * wx + B * wy * wz,
+                       -A * wy + B * wx * wz,     A * wx + B * wy * wz,      1.0 + B * (wz * wz - th2)};
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) c[3 * r + k] = Q[3 * k + r];  // R = Q^T
+  for (int r = 0; r < 3; ++r) c[9 + r] = -(c[3 * r] * b[3] + c[3 * r + 1] * b[4] + c[3 * r + 2] * b[5]);  // t = -R t_w2c
+  c[12] = b[6];
+  c[13] = b[6] * b[7];
+  c[14] = b[6] * b[8];
+  c[15] = 0.0;
+}
+
+// native -> BAL via the quaternion of R_w2c = R^T (robust for every angle)
+void native_to_bal(const double* c, double* b) {
+  const double Q[9] = {c[0], c[3], c[6], c[1], c[4], c[7], c[2], c[5], c[8]};
+  double w, x, y, z;
+  const double tr = Q[0] + Q[4] + Q[8];
+  if (tr > Q[0] && tr > Q[4] && tr > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + tr);
+    w = 0.25 * s; x = (Q[7] - Q[5]) / s; y = (Q[2] - Q[6]) / s; z = (Q[3] - Q[1]) / s;
+  } else if (Q[0] > Q[4] && Q[0] > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + Q[0] - Q[4] - Q[8]);
+    w = (Q[7] - Q[5]) / s; x = 0.25 * s; y = (Q[1] + Q[3]) / s; z = (Q[2] + Q[6]) / s;
+  } else if (Q[4] > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + Q[4] - Q[0] - Q[8]);
+    w = (Q[2] - Q[6]) / s; x = (Q[1] + Q[3]) / s; y = 0.25 * s; z = (Q[5] + Q[7]) / s;
+  } else {
+    const double s = 2.0 * std::sqrt(1.0 + Q[8] - Q[0] - Q[4]);
+    w = (Q[3] - Q[1]) / s; x = (Q[2] + Q[6]) / s; y = (Q[5] + Q[7]) / s; z = 0.25 * s;
+  }
+  if (w < 0) { w = -w; x = -x; y = -y; z = -z; }
+  const double vn = std::sqrt(x * x + y * y + z * z);
+  const double ang = 2.0 * std::atan2(vn, w);
+  const double f = vn > 0 ? ang / vn : 0.0;
+  b[0] = x * f; b[1] = y * f; b[2] = z * f;
+  for (int k = 0; k < 3; ++k) b[3 + k] = -(Q[3 * k] * c[9] + Q[3 * k + 1] * c[10] + Q[3 * k + 2] * c[11]);
+  b[6] = c[12];
+  b[7] = c[13] / c[12];
+  b[8] = c[14] / c[12];
+}
+
+int name_index(daba_ctx* c, const char* name) {
+  for (size_t i = 0; i < c->knames.size(); ++i)
+    if (c->knames[i] == name) return (int)i;
+  c->knames.push_back(name);
+  c->kms.push_back(0.0);
+  c->klaunches.push_back(0);
+  return (int)c->knames.size() - 1;
+}
+
+cudaEvent_t take_event(daba_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Run one launcher, bracketed by events in profile mode.
+template <class F>
+int timed(daba_ctx* c, const char* name, F&& fn) {
+  if (!c->opt.profile) return fn();
+  const int id = name_index(c, name);
+  cudaEvent_t a = take_event(c), b = take_event(c);
+  cudaEventRecord(a, c->stream);
+  const int n = fn();
+  cudaEventRecord(b, c->stream);
+  c->pending.push_back({id, a, b});
+  c->klaunches[(size_t)id] += n;
+  return n;
+}
+
+void collect_times(daba_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0;
+    cudaEventSynchronize(p.b);
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->kms[(size_t)p.name] += ms;
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
+int exchange_halo(daba_ctx* c, int* launches) {
+  if (c->segs.empty()) return DABA_OK;
+  int n = 0;
+  for (size_t q = 0; q < c->segs.size(); ++q) {
+    const PeerSeg& s = c->segs[q];
+    const auto& sc = c->peer_cam_idx[2 * q];
+    const auto& sp = c->peer_pt_idx[2 * q];
+    n += timed(c, "k_pack", [&] {
+      return launch_pack(c->P, c->d_send_cam + sc.first, (int32_t)sc.second, c->d_send_pt + sp.first,
+                         (int32_t)sp.second, c->d_sendbuf + s.send_off, c->stream);
+    });
+  }
+  std::string e = c->comm->exchange(c->d_sendbuf, c->d_recvbuf, c->segs, c->stream);
+  if (!e.empty()) return fail(c, DABA_E_NCCL, e);
+  for (size_t q = 0; q < c->segs.size(); ++q) {
+    const PeerSeg& s = c->segs[q];
+    const auto& rc = c->peer_cam_idx[2 * q + 1];
+    const auto& rp = c->peer_pt_idx[2 * q + 1];
+    n += timed(c, "k_unpack", [&] {
+      return launch_unpack(c->P, c->d_recv_cam + rc.first, (int32_t)rc.second, c->d_recv_pt + rp.first,
+                           (int32_t)rp.second, c->d_recvbuf + s.recv_off, c->stream);
+    });
+  }
+  *launches += n;
+  return DABA_OK;
+}
+
+// Enqueue one iteration of Algorithm 1.
+int enqueue_iteration(daba_ctx* c, int* launches) {
+  const IterParams& P = c->P;
+  int n = 0;
+  n += timed(c, "k_extrapolate", [&] { return launch_extrapolate(P, c->stream); });
+  n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
+  n += timed(c, "k_pt_pass", [&] { return launch_pt_pass(P, c->stream); });
+  n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
+  n += timed(c, "k_cam_eval", [&] { return launch_cam_eval(P, c->stream); });
+  n += timed(c, "k_reduce_local", [&] { return launch_reduce_local(P, c->stream); });
+  if (c->nranks > 1) {
+    std::string e = c->comm->allreduce(P.local, P.global, kGlobalCols, c->stream);
+    if (!e.empty()) return fail(c, DABA_E_NCCL, e);
+  }
+  n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
+  *launches += n;
+  int rc = exchange_halo(c, launches);
+  if (rc) return rc;
+  CUDA_OR(c, cudaGetLastError());
+  return DABA_OK;
+}
+
+int compute_objective(daba_ctx* c, double* F, double* ndeg) {
+  launch_objective(c->P, c->stream);
+  if (c->nranks > 1) {
+    std::string e = c->comm->allreduce(c->P.local, c->P.global, kGlobalCols, c->stream);
+    if (!e.empty()) return fail(c, DABA_E_NCCL, e);
+  }
+  double g[kGlobalCols];
+  CUDA_OR(c, cudaMemcpyAsync(g, c->nranks > 1 ? c->P.global : c->P.local, sizeof g, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR(c, cudaStreamSynchronize(c->stream));
+  *F = g[0];
+  if (ndeg) *ndeg = g[7];
+  return DABA_OK;
+}
+
+// Upload global native states into the local role buffers `rk` (x^k) and `rkm1` (x^{k-1}).
+int upload_states(daba_ctx* c, const double* cams_k, const double* pts_k, const double* cams_km1,
+                  const double* pts_km1, int rk, int rkm1) {
+  const ShardPlan& S = c->plan;
+  std::vector<double> hc(S.cam_g.size() * kCamStride), hp(S.pt_g.size() * 4);
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* gc = pass ? cams_km1 : cams_k;
+    const double* gp = pass ? pts_km1 : pts_k;
+    for (size_t li = 0; li < S.cam_g.size(); ++li) {
+      std::memcpy(&hc[li * kCamStride], gc + 15 * (size_t)S.cam_g[li], 15 * sizeof(double));
+      hc[li * kCamStride + 15] = 0.0;
+    }
+    for (size_t lj = 0; lj < S.pt_g.size(); ++lj) {
+      for (int k = 0; k < 3; ++k) hp[lj * 4 + k] = gp[3 * (size_t)S.pt_g[lj] + k];
+      hp[lj * 4 + 3] = 0.0;
+    }
+    const int role = pass ? rkm1 : rk;
+    int h_roles[4];
+    CUDA_OR(c, cudaMemcpyAsync(h_roles, c->P.roles, sizeof h_roles, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR(c, cudaStreamSynchronize(c->stream));
+    if (!hc.empty())
+      CUDA_OR(c, cudaMemcpyAsync(c->P.cams[h_roles[role]], hc.data(), hc.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+    if (!hp.empty())
+      CUDA_OR(c, cudaMemcpyAsync(c->P.pts[h_roles[role]], hp.data(), hp.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+    CUDA_OR(c, cudaStreamSynchronize(c->stream));
+  }
+  return DABA_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" void daba_default_options(daba_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->xi = 1e-4;
+  o->eta = 0.1;
+  o->lm_mu0 = 1e-3;
+  o->lm_mu_up = 10.0;
+  o->eps = 1e-8;
+  o->lm_max_trials = 5;
+  o->accelerate = 1;
+  o->comm = DABA_COMM_NCCL;
+  o->use_graph = 1;
+  o->profile = 0;
+  o->stream = nullptr;
+}
+
+extern "C" int daba_comm_id(void* id_out) {
+  if (!id_out) return DABA_E_INVALID_ARG;
+  return nccl_unique_id(id_out).empty() ? DABA_OK : DABA_E_NCCL;
+}
+
+extern "C" int daba_create(const double* cameras, int64_t M, const double* points, int64_t N, const int32_t* obs_cam,
+                           const int32_t* obs_pt, const double* obs_uv, int64_t K, daba_loss loss,
+                           const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks,
+                           const void* comm_id, int cuda_device, const daba_options* opt, daba_ctx** out) {
+  if (!out) return DABA_E_INVALID_ARG;
+  *out = nullptr;
+  std::unique_ptr<daba_ctx> c(new (std::nothrow) daba_ctx());
+  if (!c) return DABA_E_OOM;
+  daba_ctx* C = c.get();
+  if (opt)
+    C->opt = *opt;
+  else
+    daba_default_options(&C->opt);
+  const daba_options& o = C->opt;
+  if (M < 0 || N < 0 || K < 0 || (M > 0 && !cameras) || (N > 0 && !points) || (K > 0 && (!obs_cam || !obs_pt || !obs_uv)))
+    return DABA_E_INVALID_ARG;
+  if (!(loss.scale > 0) || loss.kind < DABA_LOSS_TRIVIAL || loss.kind > DABA_LOSS_CAUCHY) return DABA_E_INVALID_ARG;
+  if (!(o.xi > 0) || !(o.eta > 0 && o.eta <= 1) || !(o.lm_mu0 > 0) || !(o.lm_mu_up >= 1) || !(o.eps >= 0) ||
+      o.lm_max_trials < 1 || o.lm_max_trials > 8)
+    return DABA_E_INVALID_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm_id)) return DABA_E_INVALID_ARG;
+  C->loss = loss;
+  C->rank = rank;
+  C->nranks = nranks;
+  C->device = cuda_device;
+  std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan);
+  if (!e.empty()) {
+    *out = nullptr;
+    return DABA_E_INVALID_ARG;
+  }
+  // native cameras and Assumption 2 at x^0
+  std::vector<double> nat((size_t)M * 15);
+  for (int64_t i = 0; i < M; ++i) {
+    double tmp[16];
+    bal_to_native(cameras + 9 * i, tmp);
+    std::memcpy(&nat[(size_t)i * 15], tmp, 15 * sizeof(double));
+  }
+  for (int64_t k = 0; k < K; ++k) {
+    const double* t = &nat[(size_t)obs_cam[k] * 15 + 9];
+    const double* l = points + 3 * (int64_t)obs_pt[k];
+    const double dx = l[0] - t[0], dy = l[1] - t[1], dz = l[2] - t[2];
+    if (!(dx * dx + dy * dy + dz * dz > o.eps * o.eps)) return DABA_E_DEGENERATE;
+  }
+  // device and stream
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return DABA_E_CUDA;
+  if (o.stream) {
+    C->stream = static_cast<cudaStream_t>(o.stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking) != cudaSuccess) return DABA_E_CUDA;
+    C->own_stream = true;
+  }
+  if (nranks > 1) {
+    std::string ce;
+    C->comm.reset(make_comm(o.comm, comm_id, rank, nranks, &ce));
+    if (!C->comm) {
+      fprintf(stderr, "daba_create: %s\n", ce.c_str());
+      daba_destroy(c.release());
+      return DABA_E_NCCL;
+    }
+  }
+  int rc = DABA_OK;
+  auto bail = [&](int code) {
+    daba_destroy(c.release());
+    return code;
+  };
+  const ShardPlan& S = C->plan;
+  IterParams& P = C->P;
+  P.n_cams = (int32_t)S.cam_g.size();
+  P.n_own_cams = S.n_own_cams;
+  P.n_pts = (int32_t)S.pt_g.size();
+  P.n_own_pts = S.n_own_pts;
+  P.loss = loss.kind;
+  P.delta = loss.scale;
+  P.delta2 = loss.scale * loss.scale;
+  P.idelta2 = 1.0 / P.delta2;
+  P.xi = o.xi;
+  P.eta = o.eta;
+  P.mu0 = o.lm_mu0;
+  P.mu_up = o.lm_mu_up;
+  P.eps2 = o.eps * o.eps;
+  P.max_trials = o.lm_max_trials;
+  P.accelerate = o.accelerate ? 1 : 0;
+  for (int r = 0; r < 4; ++r) {
+    if ((rc = dalloc(C, &P.cams[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
+    if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return bail(rc);
+  }
+  if ((rc = dalloc(C, &P.cbar, (size_t)P.n_cams * kCamStride))) return bail(rc);
+  {
+    std::vector<int32_t> roles = {0, 1, 2, 3};
+    if ((rc = upload(C, &P.roles, roles))) return bail(rc);
+  }
+  // camera side + chunks
+  {
+    const size_t kc = S.c_obs.size();
+    std::vector<double2> uv(kc);
+    for (size_t q = 0; q < kc; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
+    const double2* duv;
+    if ((rc = upload(C, const_cast<double2**>(&duv), uv))) return bail(rc);
+    P.c_uv = duv;
+    const int32_t* dpt;
+    if ((rc = upload(C, const_cast<int32_t**>(&dpt), S.c_pt))) return bail(rc);
+    P.c_pt = dpt;
+    std::vector<CamChunk> chunks;
+    std::vector<int32_t> cptr(1, 0);
+    for (int32_t i = 0; i < S.n_own_cams; ++i) {
+      for (int64_t o0 = S.cam_ptr[(size_t)i]; o0 < S.cam_ptr[(size_t)i + 1]; o0 += kCamChunkObs) {
+        CamChunk ch;
+        ch.cam = i;
+        ch.o0 = o0;
+        ch.n = (int32_t)std::min<int64_t>(kCamChunkObs, S.cam_ptr[(size_t)i + 1] - o0);
+        chunks.push_back(ch);
+      }
+      cptr.push_back((int32_t)chunks.size());
+    }
+    P.n_chunks = (int32_t)chunks.size();
+    const CamChunk* dch;
+    if ((rc = upload(C, const_cast<CamChunk**>(&dch), chunks))) return bail(rc);
+    P.chunks = dch;
+    const int32_t* dcp;
+    if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return bail(rc);
+    P.cam_chunk_ptr = dcp;
+  }
+  // point side
+  {
+    const size_t kp = S.p_obs.size();
+    std::vector<double2> uv(kp);
+    for (size_t q = 0; q < kp; ++q) uv[q] = make_double2(obs_uv[2 * S.p_obs[q]], obs_uv[2 * S.p_obs[q] + 1]);
+    const double2* duv;
+    if ((rc = upload(C, const_cast<double2**>(&duv), uv))) return bail(rc);
+    P.p_uv = duv;
+    const int32_t* dcam;
+    if ((rc = upload(C, const_cast<int32_t**>(&dcam), S.p_cam))) return bail(rc);
+    P.p_cam = dcam;
+    const int64_t* dptr;
+    if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
+    P.p_ptr = dptr;
+  }
+  // scratch
+  P.n_cam_eval_blocks = (P.n_own_cams + 127) / 128;
+  P.n_pt_blocks = (P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads;
+  P.trace_cap = 1024;
+  if ((rc = dalloc(C, &P.partial, (size_t)std::max(P.n_chunks, 1) * 2 * kPartialStride))) return bail(rc);
+  if ((rc = dalloc(C, &P.moments, (size_t)std::max(P.n_own_cams, 1) * 2 * kPartialStride))) return bail(rc);
+  if ((rc = dalloc(C, &P.dP_mm, (size_t)std::max(P.n_own_cams, 1)))) return bail(rc);
+  if ((rc = dalloc(C, &P.decisions, (size_t)std::max(P.n_own_cams, 1) * 2))) return bail(rc);
+  if ((rc = dalloc(C, &P.cam_part, (size_t)std::max(P.n_cam_eval_blocks, 1) * kCamEvalCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.pt_part, (size_t)std::max(P.n_pt_blocks, 1) * kPtCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.local, kGlobalCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.global, kGlobalCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.sched, 4))) return bail(rc);
+  if (nranks == 1) P.global = P.local;
+  cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
+  // halo plan
+  if (nranks > 1) {
+    std::vector<int32_t> sc, sp, rcam, rpt;
+    int64_t soff = 0, roff = 0;
+    for (const Peer& pe : S.peers) {
+      PeerSeg sg;
+      sg.rank = pe.rank;
+      sg.send_off = soff;
+      sg.send_cnt = 15 * (int64_t)pe.send_cams.size() + 3 * (int64_t)pe.send_pts.size();
+      sg.recv_off = roff;
+      sg.recv_cnt = 15 * (int64_t)pe.recv_cams.size() + 3 * (int64_t)pe.recv_pts.size();
+      soff += sg.send_cnt;
+      roff += sg.recv_cnt;
+      C->segs.push_back(sg);
+      C->peer_cam_idx.push_back({(int64_t)sc.size(), (int64_t)pe.send_cams.size()});
+      C->peer_cam_idx.push_back({(int64_t)rcam.size(), (int64_t)pe.recv_cams.size()});
+      C->peer_pt_idx.push_back({(int64_t)sp.size(), (int64_t)pe.send_pts.size()});
+      C->peer_pt_idx.push_back({(int64_t)rpt.size(), (int64_t)pe.recv_pts.size()});
+      sc.insert(sc.end(), pe.send_cams.begin(), pe.send_cams.end());
+      sp.insert(sp.end(), pe.send_pts.begin(), pe.send_pts.end());
+      rcam.insert(rcam.end(), pe.recv_cams.begin(), pe.recv_cams.end());
+      rpt.insert(rpt.end(), pe.recv_pts.begin(), pe.recv_pts.end());
+    }
+    if ((rc = upload(C, &C->d_send_cam, sc)) || (rc = upload(C, &C->d_send_pt, sp)) ||
+        (rc = upload(C, &C->d_recv_cam, rcam)) || (rc = upload(C, &C->d_recv_pt, rpt)))
+      return bail(rc);
+    if ((rc = dalloc(C, &C->d_sendbuf, (size_t)std::max<int64_t>(soff, 1))) ||
+        (rc = dalloc(C, &C->d_recvbuf, (size_t)std::max<int64_t>(roff, 1))))
+      return bail(rc);
+  }
+  // state: x^{-1} = x^0 (Alg. 1)
+  {
+    rc = upload_states(C, nat.data(), points, nat.data(), points, 1, 0);
+    if (rc) return bail(rc);
+  }
+  // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
+  double F0 = 0, nd = 0;
+  if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
+  {
+    const double sched[4] = {1.0, F0, 0.0, 0.0};
+    if (cudaMemcpyAsync(P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, C->stream) != cudaSuccess ||
+        cudaStreamSynchronize(C->stream) != cudaSuccess)
+      return bail(DABA_E_CUDA);
+  }
+  // launches per iteration (for bookkeeping)
+  C->launches_per_iter = 7 - (P.n_chunks == 0) - (P.n_pt_blocks == 0) - (P.n_own_cams == 0) * 2;
+  for (size_t q = 0; q < C->segs.size(); ++q)
+    C->launches_per_iter += (C->peer_cam_idx[2 * q].second + C->peer_pt_idx[2 * q].second > 0) +
+                            (C->peer_cam_idx[2 * q + 1].second + C->peer_pt_idx[2 * q + 1].second > 0);
+  *out = c.release();
+  return DABA_OK;
+}
+
+static int iterate_impl(daba_ctx* c, int n, double* trace_rows) {
+  if (!c) return DABA_E_INVALID_ARG;
+  if (n < 0) return fail(c, DABA_E_INVALID_ARG, "n_iters < 0");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, DABA_E_CUDA, "cudaSetDevice");
+  const bool graphable = c->opt.use_graph && !c->opt.profile && (c->nranks == 1 || c->comm->capturable());
+  int done = 0;
+  while (done < n) {
+    const int batch = std::min(n - done, c->P.trace_cap);
+    if (graphable) {
+      if (!c->graph) {
+        cudaGraph_t g;
+        CUDA_OR(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int launches = 0;
+        int rc = enqueue_iteration(c, &launches);
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(c, DABA_E_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&c->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return fail(c, DABA_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
+      }
+      for (int it = 0; it < batch; ++it) CUDA_OR(c, cudaGraphLaunch(c->graph, c->stream));
+    } else {
+      for (int it = 0; it < batch; ++it) {
+        int launches = 0;
+        int rc = enqueue_iteration(c, &launches);
+        if (rc) return rc;
+      }
+    }
+    if (trace_rows) {
+      std::vector<double> ring((size_t)c->P.trace_cap * kTraceCols);
+      CUDA_OR(c, cudaMemcpyAsync(ring.data(), c->P.trace, ring.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+      CUDA_OR(c, cudaStreamSynchronize(c->stream));
+      for (int it = 0; it < batch; ++it) {
+        const int64_t k = c->host_k + it;
+        std::memcpy(trace_rows + (size_t)(done + it) * kTraceCols, &ring[(size_t)(k % c->P.trace_cap) * kTraceCols],
+                    kTraceCols * sizeof(double));
+      }
+    }
+    c->host_k += batch;
+    done += batch;
+  }
+  if (c->opt.profile) collect_times(c);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return fail(c, DABA_E_CUDA, cudaGetErrorString(e));
+  return DABA_OK;
+}
+
+extern "C" int daba_iterate(daba_ctx* ctx, int n_iters, double* F_trace, uint8_t* restart_trace) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  if (!F_trace && !restart_trace) return iterate_impl(ctx, n_iters, nullptr);
+  std::vector<double> rows((size_t)std::max(n_iters, 0) * kTraceCols);
+  int rc = iterate_impl(ctx, n_iters, rows.data());
+  if (rc) return rc;
+  for (int k = 0; k < n_iters; ++k) {
+    if (F_trace) F_trace[k] = rows[(size_t)k * kTraceCols + DABA_TR_F];
+    if (restart_trace) restart_trace[k] = rows[(size_t)k * kTraceCols + DABA_TR_RESTART] != 0.0;
+  }
+  return DABA_OK;
+}
+
+extern "C" int daba_iterate_trace(daba_ctx* ctx, int n_iters, double* trace) {
+  if (!ctx || !trace) return DABA_E_INVALID_ARG;
+  return iterate_impl(ctx, n_iters, trace);
+}
+
+extern "C" int daba_objective(daba_ctx* ctx, double* F_out) {
+  if (!ctx || !F_out) return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  return compute_objective(ctx, F_out, nullptr);
+}
+
+static int get_native(daba_ctx* c, int which, std::vector<double>& hc, std::vector<double>& hp) {
+  int roles[4];
+  CUDA_OR(c, cudaMemcpyAsync(roles, c->P.roles, sizeof roles, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR(c, cudaStreamSynchronize(c->stream));
+  const int r = roles[which ? 0 : 1];
+  hc.resize((size_t)c->P.n_own_cams * kCamStride);
+  hp.resize((size_t)c->P.n_own_pts * 4);
+  if (!hc.empty())
+    CUDA_OR(c, cudaMemcpyAsync(hc.data(), c->P.cams[r], hc.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (!hp.empty())
+    CUDA_OR(c, cudaMemcpyAsync(hp.data(), c->P.pts[r], hp.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR(c, cudaStreamSynchronize(c->stream));
+  return DABA_OK;
+}
+
+extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_out, double* points_out,
+                                     uint8_t* owned_mask_out) {
+  if (!ctx || which < 0 || which > 1) return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  std::vector<double> hc, hp;
+  int rc = get_native(ctx, which, hc, hp);
+  if (rc) return rc;
+  const ShardPlan& S = ctx->plan;
+  if (owned_mask_out) std::memset(owned_mask_out, 0, (size_t)(S.M + S.N));
+  for (int32_t li = 0; li < S.n_own_cams; ++li) {
+    const int64_t g = S.cam_g[(size_t)li];
+    if (cameras_out) std::memcpy(cameras_out + 15 * g, &hc[(size_t)li * kCamStride], 15 * sizeof(double));
+    if (owned_mask_out) owned_mask_out[g] = 1;
+  }
+  for (int32_t lj = 0; lj < S.n_own_pts; ++lj) {
+    const int64_t g = S.pt_g[(size_t)lj];
+    if (points_out)
+      for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
+    if (owned_mask_out) owned_mask_out[S.M + g] = 1;
+  }
+  return DABA_OK;
+}
+
+extern "C" int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points_out, uint8_t* owned_mask_out) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  std::vector<double> hc, hp;
+  int rc = get_native(ctx, 0, hc, hp);
+  if (rc) return rc;
+  const ShardPlan& S = ctx->plan;
+  if (owned_mask_out) std::memset(owned_mask_out, 0, (size_t)(S.M + S.N));
+  for (int32_t li = 0; li < S.n_own_cams; ++li) {
+    const int64_t g = S.cam_g[(size_t)li];
+    if (cameras_out) native_to_bal(&hc[(size_t)li * kCamStride], cameras_out + 9 * g);
+    if (owned_mask_out) owned_mask_out[g] = 1;
+  }
+  for (int32_t lj = 0; lj < S.n_own_pts; ++lj) {
+    const int64_t g = S.pt_g[(size_t)lj];
+    if (points_out)
+      for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
+    if (owned_mask_out) owned_mask_out[S.M + g] = 1;
+  }
+  return DABA_OK;
+}
+
+extern "C" int daba_set_state_native(daba_ctx* ctx, const double* cams_k, const double* pts_k,
+                                     const double* cams_km1, const double* pts_km1, double s, double Fbar) {
+  if (!ctx || (ctx->plan.M > 0 && (!cams_k || !cams_km1)) || (ctx->plan.N > 0 && (!pts_k || !pts_km1)) || !(s >= 1))
+    return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc = upload_states(ctx, cams_k, pts_k, cams_km1, pts_km1, 1, 0);
+  if (rc) return rc;
+  double sched[3];
+  CUDA_OR(ctx, cudaMemcpyAsync(sched, ctx->P.sched, sizeof sched, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  sched[0] = s;
+  sched[1] = Fbar;
+  CUDA_OR(ctx, cudaMemcpyAsync(ctx->P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  return DABA_OK;
+}
+
+extern "C" int daba_get_schedule(daba_ctx* ctx, double* s, double* Fbar, int64_t* k) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  double sched[4];
+  CUDA_OR(ctx, cudaMemcpyAsync(sched, ctx->P.sched, sizeof sched, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  if (s) *s = sched[0];
+  if (Fbar) *Fbar = sched[1];
+  if (k) *k = (int64_t)sched[2];
+  return DABA_OK;
+}
+
+extern "C" int daba_last_decisions(daba_ctx* ctx, int32_t* trial_acc, int32_t* trial_mm) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  std::vector<int32_t> d((size_t)std::max(ctx->P.n_own_cams, 1) * 2);
+  CUDA_OR(ctx, cudaMemcpyAsync(d.data(), ctx->P.decisions, d.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int32_t li = 0; li < ctx->P.n_own_cams; ++li) {
+    const int64_t g = ctx->plan.cam_g[(size_t)li];
+    if (trial_acc) trial_acc[g] = d[(size_t)2 * li];
+    if (trial_mm) trial_mm[g] = d[(size_t)2 * li + 1];
+  }
+  return DABA_OK;
+}
+
+extern "C" int daba_shard_info(daba_ctx* ctx, int64_t info[8]) {
+  if (!ctx || !info) return DABA_E_INVALID_ARG;
+  const ShardPlan& S = ctx->plan;
+  info[0] = S.n_own_cams;
+  info[1] = S.n_own_pts;
+  info[2] = (int64_t)S.cam_g.size() - S.n_own_cams;
+  info[3] = (int64_t)S.pt_g.size() - S.n_own_pts;
+  info[4] = (int64_t)S.c_obs.size();
+  info[5] = (int64_t)S.p_obs.size();
+  info[6] = 8 * S.send_doubles;
+  info[7] = (int64_t)ctx->dev_bytes;
+  return DABA_OK;
+}
+
+extern "C" void* daba_stream(daba_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+extern "C" int daba_kernel_times(daba_ctx* ctx, char* names_out, size_t cap, double* ms_out, int64_t* launches_out) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  collect_times(ctx);
+  std::string all;
+  const int n = (int)std::min<size_t>(ctx->knames.size(), 32);
+  for (int i = 0; i < n; ++i) {
+    all += ctx->knames[(size_t)i];
+    all += '\n';
+    if (ms_out) ms_out[i] = ctx->kms[(size_t)i];
+    if (launches_out) launches_out[i] = ctx->klaunches[(size_t)i];
+  }
+  if (names_out && cap > 0) {
+    std::strncpy(names_out, all.c_str(), cap - 1);
+    names_out[cap - 1] = 0;
+  }
+  return n;
+}
+
+extern "C" int daba_reset_kernel_times(daba_ctx* ctx) {
+  if (!ctx) return DABA_E_INVALID_ARG;
+  collect_times(ctx);
+  std::fill(ctx->kms.begin(), ctx->kms.end(), 0.0);
+  std::fill(ctx->klaunches.begin(), ctx->klaunches.end(), 0);
+  return DABA_OK;
+}
+
+extern "C" int daba_launches_per_iteration(daba_ctx* ctx) { return ctx ? ctx->launches_per_iter : DABA_E_INVALID_ARG; }
+
+extern "C" const char* daba_last_error(const daba_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" void daba_destroy(daba_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  collect_times(ctx);
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  ctx->comm.reset();
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}

@@ -1,0 +1,778 @@
+// kernels.cu — fp64 CUDA kernels of one DABA iteration for sm_100a.
+//
+// Step map:
+//   a1+a2  k_extrapolate    schedule s, gamma (eq. nesterov_scalar) and x-bar cameras
+//                           (eqs. nesterov_R/t/d P:L312-323, ProjRot3D eq. proj_rot3d)
+//   a4+a5  k_cam_pass       per observation, both anchors: ray (eq. ray), lambda (eq. gamma
+//                           P:L222-224), error (eq. error), w and a (eqs. w, a P:L216-221);
+//                           block-reduced into 40 per-camera moments (the camera part of eq. P)
+//   a4+a5+a7 k_pt_pass      per point: both anchors' sums over its observations and the exact minimiser of
+//                           sum_i Q_ij + xi/2 ||l - l_hat||^2 (eq. Q, eq. Ealpha); the
+//                           point part of E(x_acc|x^k) (eq. Eak)
+//   a6     k_cam_solve      per camera and anchor: Gauss-Newton normal equations from the moments, one
+//                           successful Levenberg-Marquardt step by Jacobi-scaled 9x9 Cholesky
+//   a8     k_cam_eval       camera part of E(x_acc|x^k) and F(x^k) per camera
+//   a9     k_reduce_local   deterministic tree sums (-> allreduce when nranks > 1)
+//   a9+a10 k_select         F-bar (eq. lFak), restart test (Alg. 1), role rotation
+#include <cstdio>
+
+#include "kernels.h"
+#include "device_math.cuh"
+
+namespace daba {
+
+__device__ __forceinline__ double sched_gamma(double s, int accelerate, double* s_next_out) {
+  // eq. nesterov_scalar in Algorithm 1 line 407's order: s^{(k+1)} first, then gamma^{(k)}
+  const double s_next = (sqrt(4.0 * s * s + 1.0) + 1.0) / 2.0;
+  if (s_next_out) *s_next_out = s_next;
+  return accelerate ? (s - 1.0) / s_next : 0.0;
+}
+
+// Point record: 32 bytes (x, y, z, pad) — one sector per gather.
+__device__ __forceinline__ void ld_point(const double4* base, int64_t j, double& x, double& y, double& z) {
+  const double2* q = reinterpret_cast<const double2*>(base + j);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  x = a.x;
+  y = a.y;
+  z = b.x;
+}
+
+// ------------------------------------------------------------------ a1 + a2
+__global__ void k_extrapolate(IterParams p) {
+  const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) p.sched[3] = gamma;
+  if (i >= p.n_cams) return;
+  const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
+  const double* cp = p.cams[p.roles[0]] + (size_t)i * kCamStride;
+  double* cb = p.cbar + (size_t)i * kCamStride;
+  double M[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) M[k] = ck[k] + gamma * (ck[k] - cp[k]);  // eq. nesterov_R before ProjRot3D
+  double R[9];
+  proj_rot3d(M, R);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) cb[k] = R[k];
+#pragma unroll
+  for (int k = 9; k < 15; ++k) cb[k] = ck[k] + gamma * (ck[k] - cp[k]);  // eqs. nesterov_t, nesterov_d
+  cb[15] = 0.0;
+}
+
+// ------------------------------------------------------------------ a4 + a5: camera pass
+// Moment slots (anchor camera frame; e = camera-frame reprojection error, s = |u|^2):
+//  0 w ux^2   1 w ux uy  2 w uy^2   3-5 w ux s^m  6-8 w uy s^m  9-13 w s^m (m=0..4)
+//  14 w lam ux  15 w lam uy  16-18 w lam s^m  19 w lam^2
+//  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e
+//  38 w |e|^2   39 a   [40 degenerate pairs]
+template <int LOSS, bool ACC>
+__device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc, double gamma) {
+  const double* cam = (ACC ? p.cbar : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
+  const double R0 = cam[0], R1 = cam[1], R2 = cam[2], R3 = cam[3], R4 = cam[4], R5 = cam[5], R6 = cam[6],
+               R7 = cam[7], R8 = cam[8];
+  const double tx = cam[9], ty = cam[10], tz = cam[11];
+  const double d0 = cam[12], d1 = cam[13], d2 = cam[14];
+  const double4* __restrict__ Lk = p.pts[p.roles[1]];
+  const double4* __restrict__ Lp = p.pts[p.roles[0]];
+  const int64_t o_end = ch.o0 + ch.n;
+  double ndeg = 0;
+  for (int64_t o = ch.o0 + threadIdx.x; o < o_end; o += kCamPassThreads) {
+    const int32_t j = __ldg(p.c_pt + o);
+    const double2 u = __ldg(p.c_uv + o);
+    double lx, ly, lz;
+    ld_point(Lk, j, lx, ly, lz);
+    if (ACC) {  // eq. nesterov_l, on the fly
+      double px, py, pz_;
+      ld_point(Lp, j, px, py, pz_);
+      lx = fma(gamma, lx - px, lx);
+      ly = fma(gamma, ly - py, ly);
+      lz = fma(gamma, lz - pz_, lz);
+    }
+    const double s = fma(u.x, u.x, u.y * u.y);
+    const double s2 = s * s;
+    const double pz = fma(s, fma(s, d2, d1), d0);  // eq. ray
+    const double vx = lx - tx, vy = ly - ty, vz = lz - tz;
+    const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
+    if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
+      ndeg += 1.0;
+      continue;
+    }
+    // camera-frame point R^T (l - t)
+    const double cx = fma(R0, vx, fma(R3, vy, R6 * vz));
+    const double cy = fma(R1, vx, fma(R4, vy, R7 * vz));
+    const double cz = fma(R2, vx, fma(R5, vy, R8 * vz));
+    const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
+    const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
+    const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
+    double rho = 0;
+    const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
+    const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
+    acc[0] = fma(wx, u.x, acc[0]);
+    acc[1] = fma(wx, u.y, acc[1]);
+    acc[2] = fma(wy, u.y, acc[2]);
+    acc[3] += wx;
+    acc[4] = fma(wx, s, acc[4]);
+    acc[5] = fma(wx, s2, acc[5]);
+    acc[6] += wy;
+    acc[7] = fma(wy, s, acc[7]);
+    acc[8] = fma(wy, s2, acc[8]);
+    acc[9] += w;
+    acc[10] += ws;
+    acc[11] += ws2;
+    acc[12] = fma(ws2, s, acc[12]);
+    acc[13] = fma(ws2, s2, acc[13]);
+    const double wl = w * lam;
+    acc[14] = fma(wl, u.x, acc[14]);
+    acc[15] = fma(wl, u.y, acc[15]);
+    acc[16] += wl;
+    acc[17] = fma(wl, s, acc[17]);
+    acc[18] = fma(wl, s2, acc[18]);
+    acc[19] = fma(wl, lam, acc[19]);
+    const double wex = w * ex, wey = w * ey, wez = w * ez;
+    acc[20] = fma(wex, u.x, acc[20]);
+    acc[21] = fma(wey, u.x, acc[21]);
+    acc[22] = fma(wez, u.x, acc[22]);
+    acc[23] = fma(wex, u.y, acc[23]);
+    acc[24] = fma(wey, u.y, acc[24]);
+    acc[25] = fma(wez, u.y, acc[25]);
+    acc[26] += wex;
+    acc[27] += wey;
+    acc[28] += wez;
+    acc[29] = fma(wex, s, acc[29]);
+    acc[30] = fma(wey, s, acc[30]);
+    acc[31] = fma(wez, s, acc[31]);
+    acc[32] = fma(wex, s2, acc[32]);
+    acc[33] = fma(wey, s2, acc[33]);
+    acc[34] = fma(wez, s2, acc[34]);
+    acc[35] = fma(wl, ex, acc[35]);
+    acc[36] = fma(wl, ey, acc[36]);
+    acc[37] = fma(wl, ez, acc[37]);
+    if (!ACC) {
+      acc[38] = fma(w, sh, acc[38]);
+      acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
+    }
+  }
+  acc[40] = ndeg;
+}
+
+// Deterministic block reduction of kPartialStride doubles per thread (128 threads) via shared-memory transposes.
+__device__ __forceinline__ void block_reduce_moments(double* acc, double* out) {
+  __shared__ double red[4][32][kPartialStride];
+  __shared__ double wsum[4][kPartialStride];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kPartialStride; ++k) red[warp][lane][k] = acc[k];
+  __syncwarp();
+  for (int k = lane; k < kPartialStride; k += 32) {
+    double s0 = 0, s1 = 0;
+#pragma unroll 4
+    for (int r = 0; r < 32; r += 2) {
+      s0 += red[warp][r][k];
+      s1 += red[warp][r + 1][k];
+    }
+    wsum[warp][k] = s0 + s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < kPartialStride) {
+    const int k = threadIdx.x;
+    out[k] = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
+  }
+}
+
+template <int LOSS>
+__global__ void __launch_bounds__(kCamPassThreads) k_cam_pass(IterParams p) {
+  const int chunk = blockIdx.x >> 1;
+  const bool acc_anchor = (blockIdx.x & 1) == 0;
+  const CamChunk ch = p.chunks[chunk];
+  double acc[kPartialStride];
+#pragma unroll
+  for (int k = 0; k < kPartialStride; ++k) acc[k] = 0.0;
+  if (acc_anchor)
+    cam_pass_body<LOSS, true>(p, ch, acc, p.sched[3]);
+  else
+    cam_pass_body<LOSS, false>(p, ch, acc, 0.0);
+  block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride);
+}
+
+// ------------------------------------------------------------------ objective F(x^k) only
+template <int LOSS>
+__global__ void __launch_bounds__(kCamPassThreads) k_objective(IterParams p) {
+  const CamChunk ch = p.chunks[blockIdx.x];
+  const double* cam = p.cams[p.roles[1]] + (size_t)ch.cam * kCamStride;
+  const double4* __restrict__ Lk = p.pts[p.roles[1]];
+  double F = 0, nd = 0;
+  for (int64_t o = ch.o0 + threadIdx.x; o < ch.o0 + ch.n; o += kCamPassThreads) {
+    const int32_t j = p.c_pt[o];
+    const double2 u = p.c_uv[o];
+    const double4 l = Lk[j];
+    const double s = fma(u.x, u.x, u.y * u.y);
+    const double pz = fma(s, fma(s, cam[14], cam[13]), cam[12]);
+    const double vx = l.x - cam[9], vy = l.y - cam[10], vz = l.z - cam[11];
+    const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
+    if (!(nv > p.eps2)) {
+      nd += 1.0;
+      continue;
+    }
+    const double cx = fma(cam[0], vx, fma(cam[3], vy, cam[6] * vz));
+    const double cy = fma(cam[1], vx, fma(cam[4], vy, cam[7] * vz));
+    const double cz = fma(cam[2], vx, fma(cam[5], vy, cam[8] * vz));
+    const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);
+    const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);
+    double rho;
+    loss_eval<LOSS, true>(fma(ex, ex, fma(ey, ey, ez * ez)), p.delta, p.delta2, p.idelta2, &rho);
+    F += 0.5 * rho;  // eq. Fij
+  }
+  __shared__ double sF[kCamPassThreads], sN[kCamPassThreads];
+  sF[threadIdx.x] = F;
+  sN[threadIdx.x] = nd;
+  __syncthreads();
+  for (int st = kCamPassThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      sF[threadIdx.x] += sF[threadIdx.x + st];
+      sN[threadIdx.x] += sN[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.partial[(size_t)blockIdx.x * 2 * kPartialStride] = sF[0];
+    p.partial[(size_t)blockIdx.x * 2 * kPartialStride + 1] = sN[0];
+  }
+}
+
+__global__ void k_reduce_objective(IterParams p) {
+  __shared__ double sF[256], sN[256];
+  double F = 0, nd = 0;
+  for (int c = threadIdx.x; c < p.n_chunks; c += 256) {
+    F += p.partial[(size_t)c * 2 * kPartialStride];
+    nd += p.partial[(size_t)c * 2 * kPartialStride + 1];
+  }
+  sF[threadIdx.x] = F;
+  sN[threadIdx.x] = nd;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      sF[threadIdx.x] += sF[threadIdx.x + st];
+      sN[threadIdx.x] += sN[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kGlobalCols; ++k) p.local[k] = 0.0;
+    p.local[0] = sF[0];
+    p.local[7] = sN[0];
+  }
+}
+
+// ------------------------------------------------------------------ a4 + a5 + a7: point pass
+template <int LOSS>
+__device__ __forceinline__ void pt_terms(const double* cam, double lx, double ly, double lz, double2 u,
+                                         const IterParams& p, double& A, double& Cx, double& Cy, double& Cz) {
+  const double s = fma(u.x, u.x, u.y * u.y);
+  const double pz = fma(s, fma(s, cam[14], cam[13]), cam[12]);  // eq. ray
+  // world-frame ray R p
+  const double rx = fma(cam[0], u.x, fma(cam[1], u.y, cam[2] * pz));
+  const double ry = fma(cam[3], u.x, fma(cam[4], u.y, cam[5] * pz));
+  const double rz = fma(cam[6], u.x, fma(cam[7], u.y, cam[8] * pz));
+  const double vx = lx - cam[9], vy = ly - cam[10], vz = lz - cam[11];
+  const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
+  if (!(nv > p.eps2)) return;
+  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * __drcp_rn(nv);  // eq. gamma
+  const double ex = fma(-lam, vx, rx), ey = fma(-lam, vy, ry), ez = fma(-lam, vz, rz);  // R e (eq. error)
+  const double w = loss_eval<LOSS, false>(fma(ex, ex, fma(ey, ey, ez * ez)), p.delta, p.delta2, p.idelta2, nullptr);
+  const double wl = w * lam;
+  A = fma(wl, lam, A);
+  Cx = fma(wl, ex, Cx);
+  Cy = fma(wl, ey, Cy);
+  Cz = fma(wl, ez, Cz);
+}
+
+template <int LOSS>
+__global__ void __launch_bounds__(kPtPassThreads) k_pt_pass(IterParams p) {
+  const int j = blockIdx.x * kPtPassThreads + threadIdx.x;
+  double q[kPtCols] = {0, 0, 0, 0};
+  if (j < p.n_own_pts) {
+    const double gamma = p.sched[3];
+    const double4 lk = p.pts[p.roles[1]][j];
+    const double4 lp = p.pts[p.roles[0]][j];
+    const double bx = fma(gamma, lk.x - lp.x, lk.x), by = fma(gamma, lk.y - lp.y, lk.y),
+                 bz = fma(gamma, lk.z - lp.z, lk.z);  // eq. nesterov_l
+    double Ab = 0, Cbx = 0, Cby = 0, Cbz = 0, Ak = 0, Ckx = 0, Cky = 0, Ckz = 0;
+    const double* cams_k = p.cams[p.roles[1]];
+    for (int64_t o = p.p_ptr[j]; o < p.p_ptr[j + 1]; ++o) {
+      const int32_t i = p.p_cam[o];
+      const double2 u = p.p_uv[o];
+      pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, bx, by, bz, u, p, Ab, Cbx, Cby, Cbz);
+      pt_terms<LOSS>(cams_k + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, Ak, Ckx, Cky, Ckz);
+    }
+    // exact minimiser: (2 A + xi) dl = C  (eq. Q with the proximal term of eq. Ealpha)
+    const double ib = 1.0 / fma(2.0, Ab, p.xi), ik = 1.0 / fma(2.0, Ak, p.xi);
+    const double ax = fma(Cbx, ib, bx), ay = fma(Cby, ib, by), az = fma(Cbz, ib, bz);  // l_acc
+    const double mx = Ckx * ik, my = Cky * ik, mz = Ckz * ik;                          // l_mm - l^k
+    p.pts[p.roles[2]][j] = make_double4(ax, ay, az, 0.0);
+    p.pts[p.roles[3]][j] = make_double4(lk.x + mx, lk.y + my, lk.z + mz, 0.0);
+    // Q-part of E(x|x^k) - E(x^k|x^k): (A_k + xi/2) |dl|^2 - C_k . dl  (eq. Q expanded at the anchor)
+    const double dx = ax - lk.x, dy = ay - lk.y, dz = az - lk.z;
+    const double n_acc = fma(dx, dx, fma(dy, dy, dz * dz));
+    const double n_mm = fma(mx, mx, fma(my, my, mz * mz));
+    const double hk = fma(0.5, p.xi, Ak);
+    q[0] = fma(hk, n_acc, -fma(Ckx, dx, fma(Cky, dy, Ckz * dz)));
+    q[1] = fma(hk, n_mm, -fma(Ckx, mx, fma(Cky, my, Ckz * mz)));
+    q[2] = n_acc;
+    q[3] = n_mm;
+  }
+  __shared__ double sq[kPtCols][kPtPassThreads];
+#pragma unroll
+  for (int c = 0; c < kPtCols; ++c) sq[c][threadIdx.x] = q[c];
+  __syncthreads();
+  for (int st = kPtPassThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+#pragma unroll
+      for (int c = 0; c < kPtCols; ++c) sq[c][threadIdx.x] += sq[c][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < kPtCols) p.pt_part[(size_t)blockIdx.x * kPtCols + threadIdx.x] = sq[threadIdx.x][0];
+}
+
+// ------------------------------------------------------------------ a6: camera solve
+// Sums of App. A of SURVEY.md (all in the anchor camera frame), derived from the 40 moments.
+struct Sums {
+  double Spp[9], Spb[9], Sbb[9], Slp[3], Slb[3], Sll, Spe[9], Seb[9], Sle[3];
+};
+
+__device__ __forceinline__ void derive_sums(const double* m, const double* d, Sums& S) {
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) S.Sbb[3 * a + b] = m[9 + a + b];
+  double Sbbd[3];
+  for (int a = 0; a < 3; ++a) Sbbd[a] = S.Sbb[3 * a] * d[0] + S.Sbb[3 * a + 1] * d[1] + S.Sbb[3 * a + 2] * d[2];
+  S.Spp[0] = m[0];
+  S.Spp[1] = S.Spp[3] = m[1];
+  S.Spp[4] = m[2];
+  S.Spp[2] = S.Spp[6] = d[0] * m[3] + d[1] * m[4] + d[2] * m[5];
+  S.Spp[5] = S.Spp[7] = d[0] * m[6] + d[1] * m[7] + d[2] * m[8];
+  S.Spp[8] = d[0] * Sbbd[0] + d[1] * Sbbd[1] + d[2] * Sbbd[2];
+  for (int b = 0; b < 3; ++b) {
+    S.Spb[b] = m[3 + b];
+    S.Spb[3 + b] = m[6 + b];
+    S.Spb[6 + b] = Sbbd[b];
+  }
+  S.Slb[0] = m[16];
+  S.Slb[1] = m[17];
+  S.Slb[2] = m[18];
+  S.Slp[0] = m[14];
+  S.Slp[1] = m[15];
+  S.Slp[2] = d[0] * m[16] + d[1] * m[17] + d[2] * m[18];
+  S.Sll = m[19];
+  for (int a = 0; a < 3; ++a) {
+    S.Spe[a] = m[20 + a];      // sum w ux e_a
+    S.Spe[3 + a] = m[23 + a];  // sum w uy e_a
+    S.Spe[6 + a] = d[0] * m[26 + a] + d[1] * m[29 + a] + d[2] * m[32 + a];  // sum w pz e_a
+    for (int c = 0; c < 3; ++c) S.Seb[3 * a + c] = m[26 + 3 * c + a];       // sum w e_a b_c
+    S.Sle[a] = m[35 + a];
+  }
+}
+
+// Exact change of sum_j P_ij + xi/2 ||c - c_hat||^2 for a camera move (dR = R' - R_hat, dt, dd), from the sums
+// (identity of SURVEY.md App. A; derivation in DESIGN.md "Trial decrease from moments").
+__device__ double delta_P(const double* Rh, const Sums& S, const double* dR, const double* dt, const double* dd,
+                          double xi) {
+  double B[9];
+  mat3_tmul(Rh, dR, B);  // R_hat^T dR = R_hat^T (A - I) R_hat
+  const double c3[3] = {B[2], B[5], 1.0 + B[8]};
+  double tau[3];
+  for (int r = 0; r < 3; ++r) tau[r] = Rh[r] * dt[0] + Rh[3 + r] * dt[1] + Rh[6 + r] * dt[2];
+  double BS[9];
+  mat3_mul(B, S.Spp, BS);
+  double T1 = 0;
+  for (int k = 0; k < 9; ++k) T1 += BS[k] * B[k];
+  double Sbbdd[3], Spbdd[3], Sebdd[3];
+  for (int a = 0; a < 3; ++a) {
+    Sbbdd[a] = S.Sbb[3 * a] * dd[0] + S.Sbb[3 * a + 1] * dd[1] + S.Sbb[3 * a + 2] * dd[2];
+    Spbdd[a] = S.Spb[3 * a] * dd[0] + S.Spb[3 * a + 1] * dd[1] + S.Spb[3 * a + 2] * dd[2];
+    Sebdd[a] = S.Seb[3 * a] * dd[0] + S.Seb[3 * a + 1] * dd[1] + S.Seb[3 * a + 2] * dd[2];
+  }
+  const double ddSbbdd = dd[0] * Sbbdd[0] + dd[1] * Sbbdd[1] + dd[2] * Sbbdd[2];
+  const double c3n = c3[0] * c3[0] + c3[1] * c3[1] + c3[2] * c3[2];
+  const double taun = tau[0] * tau[0] + tau[1] * tau[1] + tau[2] * tau[2];
+  double BSpbdd[3], BSlp[3];
+  for (int r = 0; r < 3; ++r) {
+    BSpbdd[r] = B[3 * r] * Spbdd[0] + B[3 * r + 1] * Spbdd[1] + B[3 * r + 2] * Spbdd[2];
+    BSlp[r] = B[3 * r] * S.Slp[0] + B[3 * r + 1] * S.Slp[1] + B[3 * r + 2] * S.Slp[2];
+  }
+  const double T2 = ddSbbdd * c3n;
+  const double T3 = S.Sll * taun;
+  const double T4 = 2.0 * (c3[0] * BSpbdd[0] + c3[1] * BSpbdd[1] + c3[2] * BSpbdd[2]);
+  const double T5 = 2.0 * (tau[0] * BSlp[0] + tau[1] * BSlp[1] + tau[2] * BSlp[2]);
+  const double T6 = 2.0 * (tau[0] * c3[0] + tau[1] * c3[1] + tau[2] * c3[2]) *
+                    (S.Slb[0] * dd[0] + S.Slb[1] * dd[1] + S.Slb[2] * dd[2]);
+  double T7 = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) T7 += B[3 * a + b] * S.Spe[3 * b + a];
+  const double T8 = c3[0] * Sebdd[0] + c3[1] * Sebdd[1] + c3[2] * Sebdd[2];
+  const double T9 = S.Sle[0] * tau[0] + S.Sle[1] * tau[1] + S.Sle[2] * tau[2];
+  double prox = 0;
+  for (int k = 0; k < 9; ++k) prox += dR[k] * dR[k];
+  for (int k = 0; k < 3; ++k) prox += dt[k] * dt[k] + dd[k] * dd[k];
+  return ((T1 + T2 + T3) + (T4 + T5 + T6)) + (T7 + T8 + T9) + 0.5 * xi * prox;
+}
+
+// Gauss-Newton normal equations of sum_j P_ij + xi/2 ||c - c_hat||^2 on the tangent (dtheta, dt, dd),
+// left perturbation R = Exp(dtheta) R_hat.
+__device__ void normal_equations(const double* Rh, const Sums& S, double xi, double* H, double* g) {
+  for (int k = 0; k < 81; ++k) H[k] = 0.0;
+  // theta-theta: 2 R (tr(Spp) I - Spp) R^T
+  double Q[9];
+  const double tr = S.Spp[0] + S.Spp[4] + S.Spp[8];
+  for (int k = 0; k < 9; ++k) Q[k] = (k % 4 == 0 ? tr : 0.0) - S.Spp[k];
+  double RQ[9], RQRt[9];
+  mat3_mul(Rh, Q, RQ);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) RQRt[3 * r + c] = RQ[3 * r] * Rh[3 * c] + RQ[3 * r + 1] * Rh[3 * c + 1] + RQ[3 * r + 2] * Rh[3 * c + 2];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) H[9 * r + c] = 2.0 * RQRt[3 * r + c];
+  // theta-t: 2 [R Slp]x ; t-theta its transpose
+  double a[3];
+  for (int r = 0; r < 3; ++r) a[r] = Rh[3 * r] * S.Slp[0] + Rh[3 * r + 1] * S.Slp[1] + Rh[3 * r + 2] * S.Slp[2];
+  const double X[9] = {0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      H[9 * r + 3 + c] = 2.0 * X[3 * r + c];
+      H[9 * (3 + c) + r] = 2.0 * X[3 * r + c];
+    }
+  // theta-d: 2 R [sum w uy b^T ; -sum w ux b^T ; 0]
+  const double N[9] = {S.Spb[3], S.Spb[4], S.Spb[5], -S.Spb[0], -S.Spb[1], -S.Spb[2], 0, 0, 0};
+  double RN[9];
+  mat3_mul(Rh, N, RN);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      H[9 * r + 6 + c] = 2.0 * RN[3 * r + c];
+      H[9 * (6 + c) + r] = 2.0 * RN[3 * r + c];
+    }
+  // t-t: 2 Sll I;  t-d: 2 r3 Slb^T (r3 = R e3);  d-d: 2 Sbb
+  for (int r = 0; r < 3; ++r) {
+    H[9 * (3 + r) + 3 + r] = 2.0 * S.Sll;
+    for (int c = 0; c < 3; ++c) {
+      const double v = 2.0 * Rh[3 * r + 2] * S.Slb[c];
+      H[9 * (3 + r) + 6 + c] = v;
+      H[9 * (6 + c) + 3 + r] = v;
+      H[9 * (6 + r) + 6 + c] = 2.0 * S.Sbb[3 * r + c];
+    }
+  }
+  for (int k = 0; k < 9; ++k) H[9 * k + k] += xi * (k < 3 ? 2.0 : 1.0);
+  // gradient: (R sum w p x e, R Sle, sum w e_z b)
+  const double q[3] = {S.Spe[5] - S.Spe[7], S.Spe[6] - S.Spe[2], S.Spe[1] - S.Spe[3]};
+  for (int r = 0; r < 3; ++r) {
+    g[r] = Rh[3 * r] * q[0] + Rh[3 * r + 1] * q[1] + Rh[3 * r + 2] * q[2];
+    g[3 + r] = Rh[3 * r] * S.Sle[0] + Rh[3 * r + 1] * S.Sle[1] + Rh[3 * r + 2] * S.Sle[2];
+    g[6 + r] = S.Seb[6 + r];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * p.n_own_cams) return;
+  const int i = t >> 1, a = t & 1;  // a = 0: accelerated anchor x-bar^k, a = 1: x^k
+  // sum this camera's chunk partials in chunk order (deterministic)
+  double m[kPartialStride];
+  for (int k = 0; k < kPartialStride; ++k) m[k] = 0.0;
+  for (int c = p.cam_chunk_ptr[i]; c < p.cam_chunk_ptr[i + 1]; ++c) {
+    const double* src = p.partial + ((size_t)c * 2 + a) * kPartialStride;
+    for (int k = 0; k < kPartialStride; ++k) m[k] += src[k];
+  }
+  double* mdst = p.moments + ((size_t)i * 2 + a) * kPartialStride;
+  for (int k = 0; k < kPartialStride; ++k) mdst[k] = m[k];
+  const double* anchor = (a == 0 ? p.cbar : p.cams[p.roles[1]]) + (size_t)i * kCamStride;
+  double Rh[9], th[3], dh[3];
+  for (int k = 0; k < 9; ++k) Rh[k] = anchor[k];
+  for (int k = 0; k < 3; ++k) th[k] = anchor[9 + k];
+  for (int k = 0; k < 3; ++k) dh[k] = anchor[12 + k];
+  Sums S;
+  derive_sums(m, dh, S);
+  double H[81], g[9];
+  normal_equations(Rh, S, p.xi, H, g);
+  double sc[9];
+  for (int k = 0; k < 9; ++k) sc[k] = 1.0 / sqrt(H[9 * k + k]);
+  for (int r = 0; r < 9; ++r) {
+    g[r] *= sc[r];
+    for (int c = 0; c < 9; ++c) H[9 * r + c] *= sc[r] * sc[c];
+  }
+  double out[15];
+  for (int k = 0; k < 15; ++k) out[k] = anchor[k];
+  int accepted = -1;
+  double dP_acc = 0.0;
+  double mu = p.mu0;
+  for (int tau = 0; tau < p.max_trials; ++tau, mu *= p.mu_up) {
+    // Cholesky of (H + mu diag H) in the Jacobi-scaled variables (lower triangle in L)
+    double L[81];
+    bool ok = true;
+    for (int j = 0; j < 9 && ok; ++j) {
+      double s = H[9 * j + j] * (1.0 + mu);
+      for (int k = 0; k < j; ++k) s -= L[9 * j + k] * L[9 * j + k];
+      if (!(s > 0)) {
+        ok = false;
+        break;
+      }
+      const double ljj = sqrt(s);
+      L[9 * j + j] = ljj;
+      const double il = 1.0 / ljj;
+      for (int r = j + 1; r < 9; ++r) {
+        double v = H[9 * r + j];
+        for (int k = 0; k < j; ++k) v -= L[9 * r + k] * L[9 * j + k];
+        L[9 * r + j] = v * il;
+      }
+    }
+    if (!ok) continue;  // non-positive pivot: a failed trial (Q3)
+    double y[9], x[9];
+    for (int r = 0; r < 9; ++r) {
+      double v = -g[r];
+      for (int k = 0; k < r; ++k) v -= L[9 * r + k] * y[k];
+      y[r] = v / L[9 * r + r];
+    }
+    for (int r = 8; r >= 0; --r) {
+      double v = y[r];
+      for (int k = r + 1; k < 9; ++k) v -= L[9 * k + r] * x[k];
+      x[r] = v / L[9 * r + r];
+    }
+    double delta[9];
+    for (int k = 0; k < 9; ++k) delta[k] = x[k] * sc[k];
+    double EmI[9], dR[9];
+    expm_minus_identity(delta, EmI);
+    mat3_mul(EmI, Rh, dR);  // (Exp(dtheta) - I) R_hat
+    const double dP = delta_P(Rh, S, dR, delta + 3, delta + 6, p.xi);
+    if (dP < 0.0) {  // strict decrease: accept ("one successful inner LM step")
+      for (int k = 0; k < 9; ++k) out[k] = Rh[k] + dR[k];
+      for (int k = 0; k < 3; ++k) out[9 + k] = th[k] + delta[3 + k];
+      for (int k = 0; k < 3; ++k) out[12 + k] = dh[k] + delta[6 + k];
+      accepted = tau;
+      dP_acc = dP;
+      break;
+    }
+  }
+  double* dst = p.cams[p.roles[2 + a]] + (size_t)i * kCamStride;
+  for (int k = 0; k < 15; ++k) dst[k] = out[k];
+  dst[15] = 0.0;
+  p.decisions[2 * i + a] = accepted;
+  if (a == 1) p.dP_mm[i] = dP_acc;
+}
+
+// ------------------------------------------------------------------ a8: camera part of E(x_acc|x^k), F(x^k)
+__global__ void __launch_bounds__(128) k_cam_eval(IterParams p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double q[kCamEvalCols];
+  for (int k = 0; k < kCamEvalCols; ++k) q[k] = 0.0;
+  if (i < p.n_own_cams) {
+    const double* m = p.moments + ((size_t)i * 2 + 1) * kPartialStride;
+    const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
+    const double* ca = p.cams[p.roles[2]] + (size_t)i * kCamStride;
+    const double* cm = p.cams[p.roles[3]] + (size_t)i * kCamStride;
+    double Rh[9], dR[9], dt[3], dd[3], dh[3];
+    for (int k = 0; k < 9; ++k) {
+      Rh[k] = ck[k];
+      dR[k] = ca[k] - ck[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+      dt[k] = ca[9 + k] - ck[9 + k];
+      dd[k] = ca[12 + k] - ck[12 + k];
+      dh[k] = ck[12 + k];
+    }
+    Sums S;
+    derive_sums(m, dh, S);
+    q[0] = m[39] + 0.5 * m[38];  // F_i = sum (a + w |e|^2 / 2) = sum rho / 2
+    q[1] = delta_P(Rh, S, dR, dt, dd, p.xi);
+    q[2] = p.dP_mm[i];
+    double sa = 0, sm = 0;
+    for (int k = 0; k < 15; ++k) {
+      sa += (ca[k] - ck[k]) * (ca[k] - ck[k]);
+      sm += (cm[k] - ck[k]) * (cm[k] - ck[k]);
+    }
+    q[3] = sa;
+    q[4] = sm;
+    q[5] = m[40];
+    q[6] = p.decisions[2 * i] < 0 ? 1.0 : 0.0;
+    q[7] = p.decisions[2 * i + 1] < 0 ? 1.0 : 0.0;
+  }
+  __shared__ double sq[kCamEvalCols][128];
+  for (int c = 0; c < kCamEvalCols; ++c) sq[c][threadIdx.x] = q[c];
+  __syncthreads();
+  for (int st = 64; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int c = 0; c < kCamEvalCols; ++c) sq[c][threadIdx.x] += sq[c][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < kCamEvalCols) p.cam_part[(size_t)blockIdx.x * kCamEvalCols + threadIdx.x] = sq[threadIdx.x][0];
+}
+
+// ------------------------------------------------------------------ a9: rank-local sums
+__global__ void __launch_bounds__(256) k_reduce_local(IterParams p) {
+  __shared__ double s[kGlobalCols][256];
+  double v[kGlobalCols];
+  for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
+  for (int b = threadIdx.x; b < p.n_cam_eval_blocks; b += 256) {
+    const double* q = p.cam_part + (size_t)b * kCamEvalCols;
+    v[0] += q[0];
+    v[1] += q[1];
+    v[3] += q[2];
+    v[5] += q[3];
+    v[6] += q[4];
+    v[7] += q[5];
+    v[8] += q[6];
+    v[9] += q[7];
+  }
+  for (int b = threadIdx.x; b < p.n_pt_blocks; b += 256) {
+    const double* q = p.pt_part + (size_t)b * kPtCols;
+    v[2] += q[0];
+    v[4] += q[1];
+    v[5] += q[2];
+    v[6] += q[3];
+  }
+  for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < kGlobalCols) p.local[threadIdx.x] = s[threadIdx.x][0];
+}
+
+// ------------------------------------------------------------------ a9 + a10: restart test and selection
+__global__ void k_select(IterParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* G = p.global;
+  double s_next;
+  const double gamma = sched_gamma(p.sched[0], p.accelerate, &s_next);
+  const double F = G[0];
+  const double Fbar = (1.0 - p.eta) * p.sched[1] + p.eta * F;  // eq. lFak (global form)
+  const double Eacc = F + (G[1] + G[2]);                        // eq. Eak: E(x_acc | x^k)
+  const double Emm = F + (G[3] + G[4]);
+  const bool restart = p.accelerate ? (Eacc > Fbar) : true;     // Alg. 1, strict ">"
+  const int64_t k = (int64_t)p.sched[2];
+  double* tr = p.trace + (size_t)(k % p.trace_cap) * kTraceCols;
+  tr[0] = F;
+  tr[1] = Fbar;
+  tr[2] = Eacc;
+  tr[3] = (p.accelerate && restart) ? 1.0 : 0.0;
+  tr[4] = Emm;
+  tr[5] = restart ? G[6] : G[5];
+  tr[6] = gamma;
+  tr[7] = G[7];
+  tr[8] = G[8];
+  tr[9] = G[9];
+  const int r0 = p.roles[0], r1 = p.roles[1], r2 = p.roles[2], r3 = p.roles[3];
+  p.roles[0] = r1;                 // x^{k}   -> x^{k-1}
+  p.roles[1] = restart ? r3 : r2;  // x^{k+1} = x_mm (restart, Alg. 1) or x_acc (L414)
+  p.roles[2] = r0;
+  p.roles[3] = restart ? r2 : r3;
+  p.sched[0] = s_next;
+  p.sched[1] = Fbar;
+  p.sched[2] = (double)(k + 1);
+}
+
+// ------------------------------------------------------------------ halo pack / unpack (x^k)
+__global__ void k_pack(IterParams p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                       double* buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_cam) {
+    const double* c = p.cams[p.roles[1]] + (size_t)cam_idx[t] * kCamStride;
+    for (int k = 0; k < 15; ++k) buf[(size_t)t * 15 + k] = c[k];
+  } else if (t < n_cam + n_pt) {
+    const int q = t - n_cam;
+    const double4 l = p.pts[p.roles[1]][pt_idx[q]];
+    double* b = buf + (size_t)n_cam * 15 + (size_t)q * 3;
+    b[0] = l.x;
+    b[1] = l.y;
+    b[2] = l.z;
+  }
+}
+
+__global__ void k_unpack(IterParams p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                         const double* buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_cam) {
+    double* c = p.cams[p.roles[1]] + (size_t)cam_idx[t] * kCamStride;
+    for (int k = 0; k < 15; ++k) c[k] = buf[(size_t)t * 15 + k];
+    c[15] = 0.0;
+  } else if (t < n_cam + n_pt) {
+    const int q = t - n_cam;
+    const double* b = buf + (size_t)n_cam * 15 + (size_t)q * 3;
+    p.pts[p.roles[1]][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static inline int blocks(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+int launch_extrapolate(const IterParams& p, cudaStream_t st) {
+  k_extrapolate<<<blocks(p.n_cams > 0 ? p.n_cams : 1, 128), 128, 0, st>>>(p);
+  return 1;
+}
+
+int launch_cam_pass(const IterParams& p, cudaStream_t st) {
+  if (p.n_chunks == 0) return 0;
+  switch (p.loss) {
+    case kHuber: k_cam_pass<kHuber><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+    case kCauchy: k_cam_pass<kCauchy><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+    default: k_cam_pass<kTrivial><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_pt_pass(const IterParams& p, cudaStream_t st) {
+  if (p.n_pt_blocks == 0) return 0;
+  switch (p.loss) {
+    case kHuber: k_pt_pass<kHuber><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
+    case kCauchy: k_pt_pass<kCauchy><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
+    default: k_pt_pass<kTrivial><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_cam_solve(const IterParams& p, cudaStream_t st) {
+  if (p.n_own_cams == 0) return 0;
+  k_cam_solve<<<blocks(2 * (int64_t)p.n_own_cams, 128), 128, 0, st>>>(p);
+  return 1;
+}
+
+int launch_cam_eval(const IterParams& p, cudaStream_t st) {
+  if (p.n_cam_eval_blocks == 0) return 0;
+  k_cam_eval<<<p.n_cam_eval_blocks, 128, 0, st>>>(p);
+  return 1;
+}
+
+int launch_reduce_local(const IterParams& p, cudaStream_t st) {
+  k_reduce_local<<<1, 256, 0, st>>>(p);
+  return 1;
+}
+
+int launch_select(const IterParams& p, cudaStream_t st) {
+  k_select<<<1, 32, 0, st>>>(p);
+  return 1;
+}
+
+int launch_objective(const IterParams& p, cudaStream_t st) {
+  int n = 0;
+  if (p.n_chunks > 0) {
+    switch (p.loss) {
+      case kHuber: k_objective<kHuber><<<p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+      case kCauchy: k_objective<kCauchy><<<p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+      default: k_objective<kTrivial><<<p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+    }
+    ++n;
+  }
+  k_reduce_objective<<<1, 256, 0, st>>>(p);
+  return n + 1;
+}
+
+int launch_pack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                double* buf, cudaStream_t st) {
+  if (n_cam + n_pt == 0) return 0;
+  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, n_cam, pt_idx, n_pt, buf);
+  return 1;
+}
+
+int launch_unpack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                  const double* buf, cudaStream_t st) {
+  if (n_cam + n_pt == 0) return 0;
+  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, n_cam, pt_idx, n_pt, buf);
+  return 1;
+}
+
+}  // namespace daba

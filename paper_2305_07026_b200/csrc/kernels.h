@@ -1,0 +1,85 @@
+// kernels.h — launch interface of the DABA iteration kernels (host side).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace daba {
+
+// Camera record in HBM: 16 doubles (128 B, one cache line): R[0..8] row-major camera->world, t[9..11] centre,
+// d[12..14] = (f, f k1, f k2), [15] unused.
+constexpr int kCamStride = 16;
+constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camera moments"
+constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
+constexpr int kCamPassThreads = 128;
+constexpr int kCamChunkObs = 128 * 16;  // observations per camera-pass chunk (one CTA)
+constexpr int kPtPassThreads = 128;
+constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
+constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
+constexpr int kGlobalCols = 10;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
+constexpr int kTraceCols = 10;    // = DABA_TRACE_COLS
+
+struct CamChunk {
+  int32_t cam;    // local camera index (owned)
+  int32_t n;      // observations in the chunk
+  int64_t o0;     // first camera-side observation
+};
+
+// Device state of one iteration.  Role buffers: roles[0] = x^{k-1}, roles[1] = x^k, roles[2] = acc candidate,
+// roles[3] = mm candidate; the select kernel rotates them on the device.
+struct IterParams {
+  // sizes
+  int32_t n_cams;        // local cameras (owned first, then halo)
+  int32_t n_own_cams;
+  int32_t n_pts;         // local points (owned first, then halo)
+  int32_t n_own_pts;
+  int32_t n_chunks;      // camera-pass chunks
+  int32_t loss;
+  double delta, delta2, idelta2;
+  double xi, eta, mu0, mu_up, eps2;
+  int32_t max_trials, accelerate;
+  // state
+  double* cams[4];       // n_cams x 16
+  double4* pts[4];       // n_pts
+  double* cbar;          // extrapolated cameras x-bar^k, n_cams x 16
+  int32_t* roles;        // [4]
+  double* sched;         // [0] s^{(k)}, [1] F-bar^{(k-1)}, [2] iteration counter k (as double), [3] gamma^{(k)}
+  // camera-side observations (sorted by camera, then point)
+  const CamChunk* chunks;
+  const int32_t* cam_chunk_ptr;  // n_own_cams + 1
+  const double2* c_uv;
+  const int32_t* c_pt;
+  // point-side observations (sorted by point, then camera)
+  const int64_t* p_ptr;          // n_own_pts + 1
+  const double2* p_uv;
+  const int32_t* p_cam;
+  // scratch
+  double* partial;        // n_chunks * 2 * kPartialStride
+  double* moments;        // n_own_cams * 2 * kNumMoments (summed per camera)
+  double* dP_mm;          // n_own_cams
+  int32_t* decisions;     // n_own_cams * 2
+  double* cam_part;       // camera-eval blocks x kCamEvalCols
+  double* pt_part;        // point-pass blocks x kPtCols
+  int32_t n_cam_eval_blocks, n_pt_blocks;
+  double* local;          // kGlobalCols (this rank's sums)
+  double* global;         // kGlobalCols (allreduced)
+  double* trace;          // trace ring, trace_cap x kTraceCols
+  int32_t trace_cap;
+};
+
+// Launchers (all asynchronous on `st`).  They return the number of kernels launched.
+int launch_extrapolate(const IterParams& p, cudaStream_t st);
+int launch_cam_pass(const IterParams& p, cudaStream_t st);
+int launch_pt_pass(const IterParams& p, cudaStream_t st);
+int launch_cam_solve(const IterParams& p, cudaStream_t st);
+int launch_cam_eval(const IterParams& p, cudaStream_t st);
+int launch_reduce_local(const IterParams& p, cudaStream_t st);
+int launch_select(const IterParams& p, cudaStream_t st);
+// F(x^k) only (create-time F-bar^{(-1)} and daba_objective): writes local[0] (and local[7] = degenerate count)
+int launch_objective(const IterParams& p, cudaStream_t st);
+// halo exchange helpers: gather owned boundary entries of x^k into a send buffer / scatter received entries
+int launch_pack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                double* buf, cudaStream_t st);
+int launch_unpack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
+                  const double* buf, cudaStream_t st);
+
+}  // namespace daba

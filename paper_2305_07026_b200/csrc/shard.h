@@ -1,0 +1,48 @@
+// shard.h — host-side partition of a DABA problem across ranks (no CUDA).
+//
+// Partitioning follows P:L532 ("evenly distributing measurements to each device"): cameras in contiguous id
+// ranges balanced by observation count; a point goes to the rank owning most of its observations (ties -> lowest
+// rank).  Under reading D1 every observation is majorized, so the partition decides only what crosses the
+// interconnect: rank r keeps
+//   camera side: observations whose camera it owns (camera moments, F partial);
+//   point side : observations whose point it owns (point sums);
+//   halo       : non-owned points read by its camera side, non-owned cameras read by its point side,
+// and exchanges x^k of boundary variables with its neighbours each iteration (Alg. 1).
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace daba {
+
+struct Peer {
+  int rank;
+  std::vector<int32_t> send_cams, send_pts;  // LOCAL indices of owned entries to send (sorted by global id)
+  std::vector<int32_t> recv_cams, recv_pts;  // LOCAL indices of halo slots to fill (sorted by global id)
+};
+
+struct ShardPlan {
+  int rank = 0, nranks = 1;
+  int64_t M = 0, N = 0, K = 0;
+  std::vector<int32_t> cam_owner, pt_owner;     // global ownership maps
+  std::vector<int32_t> cam_g, pt_g;             // local -> global ids: owned (ascending) then halo (ascending)
+  int32_t n_own_cams = 0, n_own_pts = 0;
+  // camera side (sorted by camera, then point): local camera, local point, global observation id
+  std::vector<int32_t> c_cam, c_pt;
+  std::vector<int64_t> c_obs;
+  std::vector<int64_t> cam_ptr;                 // n_own_cams + 1 offsets into the camera side
+  // point side (sorted by point, then camera)
+  std::vector<int32_t> p_cam, p_pt;
+  std::vector<int64_t> p_obs;
+  std::vector<int64_t> pt_ptr;                  // n_own_pts + 1
+  std::vector<Peer> peers;
+  int64_t send_doubles = 0, recv_doubles = 0;   // per iteration
+};
+
+// Build rank `rank`'s shard.  cam_owner/pt_owner may be null (defaults above).  Returns "" or an error message
+// (index out of range, duplicate (i,j), owner out of range).
+std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, const int32_t* obs_pt,
+                       const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks, ShardPlan* out);
+
+}  // namespace daba

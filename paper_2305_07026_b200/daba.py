@@ -1,0 +1,223 @@
+"""ctypes binding of libdaba.so (include/daba.h).  Argument marshalling only: every step of the
+iteration runs in the CUDA kernels behind the C-ABI; there is no CPU fallback — if the library
+is missing this module raises on import of the library."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdaba.so")
+_lib = None
+
+LOSS_TRIVIAL, LOSS_HUBER, LOSS_CAUCHY = 0, 1, 2
+COMM_NCCL, COMM_LOCAL = 0, 1
+(TR_F, TR_FBAR, TR_EACC, TR_RESTART, TR_EMM, TR_STEP2, TR_GAMMA, TR_NDEGEN, TR_NOACC_ACC, TR_NOACC_MM,
+ TRACE_COLS) = range(11)
+ERRORS = {0: "DABA_OK", -1: "DABA_E_INVALID_ARG", -2: "DABA_E_DEGENERATE", -3: "DABA_E_CUDA", -4: "DABA_E_NCCL",
+          -5: "DABA_E_OOM", -6: "DABA_E_STATE"}
+
+
+class DabaError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Loss(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("scale", ctypes.c_double)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("xi", ctypes.c_double), ("eta", ctypes.c_double), ("lm_mu0", ctypes.c_double),
+                ("lm_mu_up", ctypes.c_double), ("eps", ctypes.c_double), ("lm_max_trials", ctypes.c_int),
+                ("accelerate", ctypes.c_int), ("comm", ctypes.c_int), ("use_graph", ctypes.c_int),
+                ("profile", ctypes.c_int), ("stream", ctypes.c_void_p)]
+
+
+EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate", "daba_iterate_trace",
+           "daba_objective", "daba_get_state", "daba_get_state_native", "daba_set_state_native",
+           "daba_get_schedule", "daba_last_decisions", "daba_shard_info", "daba_stream", "daba_kernel_times",
+           "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy"]
+
+
+def lib():
+    """Load libdaba.so (built by __graft_entry__.build() / paper_2305_07026_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        V, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.daba_default_options.argtypes = [ctypes.POINTER(Options)]
+        L.daba_default_options.restype = None
+        L.daba_comm_id.argtypes = [V]
+        L.daba_create.argtypes = [V, I64, V, I64, V, V, V, I64, Loss, V, V, I32, I32, V, I32,
+                                  ctypes.POINTER(Options), ctypes.POINTER(V)]
+        L.daba_iterate.argtypes = [V, I32, V, V]
+        L.daba_iterate_trace.argtypes = [V, I32, V]
+        L.daba_objective.argtypes = [V, ctypes.POINTER(ctypes.c_double)]
+        L.daba_get_state.argtypes = [V, V, V, V]
+        L.daba_get_state_native.argtypes = [V, I32, V, V, V]
+        L.daba_set_state_native.argtypes = [V, V, V, V, V, ctypes.c_double, ctypes.c_double]
+        L.daba_get_schedule.argtypes = [V, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(I64)]
+        L.daba_last_decisions.argtypes = [V, V, V]
+        L.daba_shard_info.argtypes = [V, V]
+        L.daba_stream.argtypes = [V]
+        L.daba_stream.restype = V
+        L.daba_kernel_times.argtypes = [V, ctypes.c_char_p, ctypes.c_size_t, V, V]
+        L.daba_reset_kernel_times.argtypes = [V]
+        L.daba_launches_per_iteration.argtypes = [V]
+        L.daba_last_error.argtypes = [V]
+        L.daba_last_error.restype = ctypes.c_char_p
+        L.daba_destroy.argtypes = [V]
+        L.daba_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def default_options(**kw) -> Options:
+    o = Options()
+    lib().daba_default_options(ctypes.byref(o))
+    for k, v in kw.items():
+        if k == "stream":
+            v = ctypes.c_void_p(v) if v is not None else None
+        setattr(o, k, v)
+    return o
+
+
+def comm_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().daba_comm_id(buf)
+    if rc:
+        raise DabaError(rc, "ncclGetUniqueId")
+    return buf.raw
+
+
+def _c(x, dtype):
+    return np.ascontiguousarray(x, dtype=dtype)
+
+
+class Solver:
+    """One rank's DABA context.  Arrays follow include/daba.h (BAL cameras M x 9, points N x 3, observations
+    sorted or not, pixels K x 2 centred)."""
+
+    def __init__(self, cameras, points, obs_cam, obs_pt, obs_uv, loss=LOSS_TRIVIAL, loss_scale=1.0,
+                 cam_owner=None, pt_owner=None, rank=0, nranks=1, comm_key: bytes | None = None, device=0,
+                 **opts):
+        L = lib()
+        self._arrs = [_c(cameras, np.float64).reshape(-1, 9), _c(points, np.float64).reshape(-1, 3),
+                      _c(obs_cam, np.int32), _c(obs_pt, np.int32), _c(obs_uv, np.float64).reshape(-1, 2)]
+        cams, pts, oc, op, uv = self._arrs
+        self.M, self.N, self.K = cams.shape[0], pts.shape[0], oc.shape[0]
+        co = _c(cam_owner, np.int32) if cam_owner is not None else None
+        po = _c(pt_owner, np.int32) if pt_owner is not None else None
+        self.opt = default_options(**opts)
+        key = ctypes.create_string_buffer(comm_key, 128) if comm_key is not None else None
+        h = ctypes.c_void_p()
+        rc = L.daba_create(cams.ctypes.data, self.M, pts.ctypes.data, self.N, oc.ctypes.data, op.ctypes.data,
+                           uv.ctypes.data, self.K, Loss(loss, loss_scale),
+                           co.ctypes.data if co is not None else None, po.ctypes.data if po is not None else None,
+                           rank, nranks, key, device, ctypes.byref(self.opt), ctypes.byref(h))
+        if rc:
+            raise DabaError(rc, "daba_create")
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+
+    def _check(self, rc, what):
+        if rc < 0:
+            raise DabaError(rc, f"{what}: {lib().daba_last_error(self.h).decode()}")
+        return rc
+
+    def iterate(self, n: int, F_trace: bool = False):
+        """Run n iterations; returns (F(x^k) trace, restart flags) when F_trace, else None."""
+        if not F_trace:
+            self._check(lib().daba_iterate(self.h, n, None, None), "daba_iterate")
+            return None
+        F = np.zeros(n)
+        r = np.zeros(n, np.uint8)
+        self._check(lib().daba_iterate(self.h, n, F.ctypes.data, r.ctypes.data), "daba_iterate")
+        return F, r
+
+    def iterate_trace(self, n: int) -> np.ndarray:
+        tr = np.zeros((n, TRACE_COLS))
+        self._check(lib().daba_iterate_trace(self.h, n, tr.ctypes.data), "daba_iterate_trace")
+        return tr
+
+    def objective(self) -> float:
+        F = ctypes.c_double()
+        self._check(lib().daba_objective(self.h, ctypes.byref(F)), "daba_objective")
+        return F.value
+
+    def state(self):
+        cams, pts = np.full((self.M, 9), np.nan), np.full((self.N, 3), np.nan)
+        mask = np.zeros(self.M + self.N, np.uint8)
+        self._check(lib().daba_get_state(self.h, cams.ctypes.data, pts.ctypes.data, mask.ctypes.data), "get_state")
+        return cams, pts, mask
+
+    def state_native(self, which: int = 0):
+        cams, pts = np.full((self.M, 15), np.nan), np.full((self.N, 3), np.nan)
+        mask = np.zeros(self.M + self.N, np.uint8)
+        self._check(lib().daba_get_state_native(self.h, which, cams.ctypes.data, pts.ctypes.data, mask.ctypes.data),
+                    "get_state_native")
+        return cams, pts, mask
+
+    def set_state_native(self, cams_k, pts_k, cams_km1, pts_km1, s, Fbar):
+        a = [_c(x, np.float64) for x in (cams_k, pts_k, cams_km1, pts_km1)]
+        self._check(lib().daba_set_state_native(self.h, a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data,
+                                                a[3].ctypes.data, s, Fbar), "set_state_native")
+
+    def schedule(self):
+        s, Fb, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        self._check(lib().daba_get_schedule(self.h, ctypes.byref(s), ctypes.byref(Fb), ctypes.byref(k)), "schedule")
+        return s.value, Fb.value, k.value
+
+    def decisions(self):
+        a, m = np.full(self.M, -2, np.int32), np.full(self.M, -2, np.int32)
+        self._check(lib().daba_last_decisions(self.h, a.ctypes.data, m.ctypes.data), "decisions")
+        return a, m
+
+    def shard_info(self) -> dict:
+        info = np.zeros(8, np.int64)
+        self._check(lib().daba_shard_info(self.h, info.ctypes.data), "shard_info")
+        keys = ["own_cams", "own_pts", "halo_cams", "halo_pts", "cam_side_obs", "pt_side_obs", "send_bytes_per_iter",
+                "device_bytes"]
+        return dict(zip(keys, (int(v) for v in info)))
+
+    @property
+    def stream(self) -> int:
+        return lib().daba_stream(self.h) or 0
+
+    def kernel_times(self) -> dict:
+        names = ctypes.create_string_buffer(4096)
+        ms = np.zeros(32)
+        cnt = np.zeros(32, np.int64)
+        n = self._check(lib().daba_kernel_times(self.h, names, 4096, ms.ctypes.data, cnt.ctypes.data), "kernel_times")
+        keys = names.value.decode().split("\n")[:n]
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}
+
+    def reset_kernel_times(self):
+        self._check(lib().daba_reset_kernel_times(self.h), "reset_kernel_times")
+
+    def launches_per_iteration(self) -> int:
+        return self._check(lib().daba_launches_per_iteration(self.h), "launches_per_iteration")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().daba_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

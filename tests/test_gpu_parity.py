@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): F(x^k) within 1e-10 relative every iteration; camera / point states
+within 1e-8 relative after 50 iterations.  Decisions (LM accept index per camera, restart flag) must match.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+D = pytest.importorskip("paper_2305_07026_b200")
+
+F_TOL = 1e-10
+X_TOL = 1e-8
+
+
+def solver(p, **kw):
+    return D.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, loss=p.loss, loss_scale=p.loss_scale, **kw)
+
+
+def oracle_for(p, **kw):
+    return oracle.Oracle(p, **kw)
+
+
+def state_errors(cg, lg, co, lo):
+    """max relative errors: rotation (Frobenius), centre, intrinsics, points (SURVEY §8(c) parity protocol)."""
+    eR = np.linalg.norm((cg[:, :9] - co[:, :9]), axis=1).max(initial=0)
+    et = (np.linalg.norm(cg[:, 9:12] - co[:, 9:12], axis=1) / np.maximum(1, np.linalg.norm(co[:, 9:12], axis=1))).max(initial=0)
+    ed = (np.linalg.norm(cg[:, 12:] - co[:, 12:], axis=1) / np.linalg.norm(co[:, 12:], axis=1)).max(initial=0)
+    el = (np.linalg.norm(lg - lo, axis=1) / np.maximum(1, np.linalg.norm(lo, axis=1))).max(initial=0)
+    return eR, et, ed, el
+
+
+CASES = ["tiny_seq", "small_huber", "small_cauchy", "small_seq_huber", "ladybug49"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_objective_at_x0(name):
+    p = gen.generate(name)
+    with solver(p) as s:
+        o = oracle_for(p)
+        assert s.objective() == pytest.approx(o.objective(), rel=F_TOL)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_one_iteration(name):
+    p = gen.generate(name)
+    o = oracle_for(p)
+    tro = o.iterate(1)
+    with solver(p) as s:
+        trg = s.iterate_trace(1)
+        assert trg[0, D.daba.TR_F] == pytest.approx(tro[0, oracle.TR_F], rel=F_TOL)
+        assert trg[0, D.daba.TR_RESTART] == tro[0, oracle.TR_RESTART]
+        cg, lg, _ = s.state_native(0)
+        co, lo = o.state(0)
+        errs = state_errors(cg, lg, co, lo)
+        assert max(errs) < 1e-11, errs
+        ga, gm = s.decisions()
+        oa, om = o.decisions()
+        np.testing.assert_array_equal(ga, oa)
+        np.testing.assert_array_equal(gm, om)
+        # x^{k-1} is the old x^k
+        cp, lp, _ = s.state_native(1)
+        cp0, lp0 = o.state(1)
+        assert max(state_errors(cp, lp, cp0, lp0)) < 1e-14
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("eta", [0.1, 1.0])
+def test_fifty_iterations(name, eta):
+    p = gen.generate(name)
+    o = oracle_for(p, eta=eta)
+    tro = o.iterate(50)
+    with solver(p, eta=eta) as s:
+        trg = s.iterate_trace(50)
+        rel = np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])
+        assert rel.max() <= F_TOL, (rel.max(), int(rel.argmax()))
+        np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
+        cg, lg, _ = s.state_native(0)
+        co, lo = o.state(0)
+        errs = state_errors(cg, lg, co, lo)
+        assert max(errs) <= X_TOL, errs
+        # the same invariants the oracle satisfies (App. C.3.1)
+        F, Fb, st = trg[:, 0], trg[:, 1], trg[:, 5]
+        tol = 1e-12 * F[0]
+        assert np.all(np.diff(Fb) <= tol)
+        assert np.all(F[1:] + 0.5 * 1e-4 * st[:-1] <= Fb[:-1] + tol)
+        assert np.all(trg[:, 4] <= F + tol)
+
+
+def test_bal_state_roundtrip_matches_oracle_conversion():
+    p = gen.generate("small_huber")
+    o = oracle_for(p)
+    o.iterate(3)
+    with solver(p) as s:
+        s.iterate(3)
+        cams, pts, mask = s.state()
+        assert mask.all()
+        co, lo = o.state(0)
+        # compare through the oracle's conversion of the GPU's BAL output back to native
+        back = oracle.bal_to_native(cams)
+        assert max(state_errors(back, pts, co, lo)) < 1e-10
+
+
+def test_unaccelerated_mode():
+    p = gen.generate("small_huber")
+    o = oracle_for(p, accelerate=0)
+    tro = o.iterate(10)
+    with solver(p, accelerate=0) as s:
+        trg = s.iterate_trace(10)
+        assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
+        assert np.all(trg[:, D.daba.TR_GAMMA] == 0)
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
+
+
+def test_graph_and_eager_paths_agree():
+    p = gen.generate("small_cauchy")
+    with solver(p, use_graph=1) as a, solver(p, use_graph=0) as b, solver(p, profile=1) as c:
+        ta, tb, tc = a.iterate_trace(7), b.iterate_trace(7), c.iterate_trace(7)
+        np.testing.assert_array_equal(ta, tb)
+        np.testing.assert_array_equal(ta, tc)
+        kt = c.kernel_times()
+        assert "k_cam_pass" in kt and kt["k_cam_pass"][1] == 7
+
+
+def test_resume_from_set_state():
+    p = gen.generate("small_seq_huber")
+    with solver(p) as a, solver(p) as b:
+        a.iterate(5)
+        ck, lk, _ = a.state_native(0)
+        cp, lp, _ = a.state_native(1)
+        s, Fb, k = a.schedule()
+        b.set_state_native(ck, lk, cp, lp, s, Fb)
+        ta, tb = a.iterate_trace(4), b.iterate_trace(4)
+        np.testing.assert_array_equal(ta[:, :5], tb[:, :5])
+
+
+# ---------------------------------------------------------------- edge cases
+def test_isolated_cameras_and_points():
+    # a camera and points without observations: the anchor-extrapolated / MM candidates of an empty subproblem
+    p = gen.generate("small_huber")
+    M, N = p.M, p.N
+    cams = np.vstack([p.cams, p.cams[:1] + 0.01])
+    pts = np.vstack([p.pts, p.pts[:5] + 0.5])
+    q = gen.Problem("iso", cams, pts, p.obs_cam, p.obs_pt, p.obs_uv, p.gt_cams, p.gt_pts, p.loss)
+    o = oracle_for(q)
+    tro = o.iterate(6)
+    with solver(q) as s:
+        trg = s.iterate_trace(6)
+        assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= 1e-10
+
+
+def test_empty_observation_set():
+    p = gen.generate("tiny_seq")
+    with D.Solver(p.cams, p.pts, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2))) as s:
+        tr = s.iterate_trace(3)
+        assert np.all(tr[:, 0] == 0)
+        cg, lg, _ = s.state_native(0)
+        assert np.isfinite(cg).all() and np.isfinite(lg).all()
+
+
+def test_invalid_arguments():
+    p = gen.generate("tiny_seq")
+    with pytest.raises(D.DabaError) as e:
+        D.Solver(p.cams, p.pts, p.obs_cam, np.where(np.arange(p.K) == 3, p.N, p.obs_pt), p.obs_uv)
+    assert e.value.code == -1
+    dup_c = np.concatenate([p.obs_cam, p.obs_cam[:1]])
+    dup_p = np.concatenate([p.obs_pt, p.obs_pt[:1]])
+    dup_u = np.vstack([p.obs_uv, p.obs_uv[:1]])
+    with pytest.raises(D.DabaError) as e:
+        D.Solver(p.cams, p.pts, dup_c, dup_p, dup_u)
+    assert e.value.code == -1
+    with pytest.raises(D.DabaError) as e:
+        D.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, eta=1.5)
+    assert e.value.code == -1
+    with pytest.raises(D.DabaError) as e:
+        D.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, loss=1, loss_scale=0.0)
+    assert e.value.code == -1
+
+
+def test_degenerate_pair_rejected_at_create():
+    # Assumption 2: a point at a camera centre
+    p = gen.generate("tiny_seq")
+    pts = p.pts.copy()
+    c0 = oracle.bal_to_native(p.cams[p.obs_cam[0]])[0]
+    pts[p.obs_pt[0]] = c0[9:12]
+    with pytest.raises(D.DabaError) as e:
+        D.Solver(p.cams, pts, p.obs_cam, p.obs_pt, p.obs_uv)
+    assert e.value.code == -2
+
+
+def test_unsorted_observations_same_result():
+    p = gen.generate("small_huber")
+    perm = np.random.default_rng(0).permutation(p.K)
+    q = gen.Problem("shuf", p.cams, p.pts, p.obs_cam[perm], p.obs_pt[perm], p.obs_uv[perm], p.gt_cams, p.gt_pts,
+                    p.loss)
+    with solver(p) as a, solver(q) as b:
+        np.testing.assert_array_equal(a.iterate_trace(5), b.iterate_trace(5))
+
+
+# ---------------------------------------------------------------- several ranks on one GPU (LOCAL comm)
+def run_ranks(p, nranks, n_iter, **kw):
+    key = np.random.default_rng(nranks).bytes(128)
+    out = [None] * nranks
+    err = []
+
+    def work(r):
+        try:
+            s = solver(p, rank=r, nranks=nranks, comm_key=key, comm=D.COMM_LOCAL, **kw)
+            tr = s.iterate_trace(n_iter)
+            c, l, mask = s.state_native(0)
+            out[r] = (tr, c, l, mask, s.shard_info())
+            s.close()
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    if err:
+        raise err[0]
+    M, N = p.M, p.N
+    cams, pts = np.full((M, 15), np.nan), np.full((N, 3), np.nan)
+    for tr, c, l, mask, info in out:
+        cams[mask[:M] == 1] = c[mask[:M] == 1]
+        pts[mask[M:] == 1] = l[mask[M:] == 1]
+    return out[0][0], cams, pts, [o[4] for o in out]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_rank_count_invariance(nranks):
+    # Reading D1: every observation is majorized, so the iterates do not depend on the partition; only the
+    # grouping of the global sums changes (F to rounding).
+    p = gen.generate("small_seq_huber")
+    with solver(p) as s:
+        t1 = s.iterate_trace(20)
+        c1, l1, _ = s.state_native(0)
+    tn, cn, ln, infos = run_ranks(p, nranks, 20)
+    assert not np.isnan(cn).any() and not np.isnan(ln).any()
+    assert np.abs(tn[:, 0] - t1[:, 0]).max() <= 1e-13 * t1[0, 0]
+    np.testing.assert_array_equal(tn[:, D.daba.TR_RESTART], t1[:, D.daba.TR_RESTART])
+    assert max(state_errors(cn, ln, c1, l1)) <= 1e-12
+    assert sum(i["own_cams"] for i in infos) == p.M and sum(i["own_pts"] for i in infos) == p.N
+    assert sum(i["cam_side_obs"] for i in infos) == p.K and sum(i["pt_side_obs"] for i in infos) == p.K
+    assert all(i["halo_pts"] > 0 for i in infos)
+
+
+# ---------------------------------------------------------------- full-size sampled parity
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["trafalgar", "final13682"])
+def test_full_size_sampled(name):
+    """At the benchmark's full size: F(x^k) over all observations, and the next iterate of sampled cameras and
+    points computed one by one by the oracle from the GPU's (x^k, x^{k-1}, s)."""
+    p = gen.generate(name)
+    rng = np.random.default_rng(5)
+    with solver(p) as s:
+        s.iterate(3)
+        ck, lk, _ = s.state_native(0)
+        cp, lp, _ = s.state_native(1)
+        sk, Fb, k = s.schedule()
+        tr = s.iterate_trace(1)
+        c1, l1, _ = s.state_native(0)
+    o = oracle_for(p)
+    o.set_state(0, ck, lk)
+    o.set_state(1, cp, lp)
+    o.set_schedule(sk, Fb)
+    assert tr[0, 0] == pytest.approx(o.objective(), rel=F_TOL)
+    cam_ids = rng.choice(p.M, 24, replace=False)
+    pt_ids = rng.choice(p.N, 200, replace=False)
+    ca, cm, pa, pm = o.candidates(cam_ids, pt_ids)
+    restart = tr[0, D.daba.TR_RESTART] == 1
+    cexp, pexp = (cm, pm) if restart else (ca, pa)
+    errs = state_errors(c1[cam_ids], l1[pt_ids], cexp, pexp)
+    assert max(errs) < 1e-11, errs
