@@ -428,7 +428,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return bail(rc);
     P.cam_chunk_ptr = dcp;
   }
-  // point side
+  // point side + point chunks (camera tables for the shared-memory staged point pass)
   {
     const size_t kp = S.p_obs.size();
     std::vector<double2> uv(kp);
@@ -442,10 +442,77 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     const int64_t* dptr;
     if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
     P.p_ptr = dptr;
+    std::vector<PtChunk> pch;
+    std::vector<int32_t> pcams;
+    std::vector<uint16_t> sp(kp, 0);
+    std::vector<int32_t> slot_of((size_t)std::max<size_t>(S.cam_g.size(), 1), -1);
+    std::vector<int32_t> stamp((size_t)std::max<size_t>(S.cam_g.size(), 1), -1);
+    int32_t max_cams = 1;
+    int32_t j = 0;
+    while (j < S.n_own_pts) {
+      PtChunk ch{};
+      ch.o0 = S.pt_ptr[(size_t)j];
+      ch.p0 = j;
+      ch.c0 = (int32_t)pcams.size();
+      const int32_t id = (int32_t)pch.size();
+      // greedy: add points while the chunk stays within its limits
+      while (j < S.n_own_pts && ch.npts < kPtPassThreads) {
+        const int64_t b = S.pt_ptr[(size_t)j], e = S.pt_ptr[(size_t)j + 1];
+        int32_t fresh = 0;
+        for (int64_t o = b; o < e; ++o) {
+          const int32_t c = S.p_cam[(size_t)o];
+          if (stamp[(size_t)c] != id) {
+            stamp[(size_t)c] = id;
+            slot_of[(size_t)c] = -2;  // tentatively new
+            ++fresh;
+          }
+        }
+        const bool fits = ch.nobs + (e - b) <= kPtChunkObs && ch.ncam + fresh <= kPtMaxCams;
+        if (!fits) {
+          // roll back the tentative marks of this point
+          for (int64_t o = b; o < e; ++o) {
+            const int32_t c = S.p_cam[(size_t)o];
+            if (slot_of[(size_t)c] == -2) stamp[(size_t)c] = -1;
+          }
+          break;
+        }
+        for (int64_t o = b; o < e; ++o) {
+          const int32_t c = S.p_cam[(size_t)o];
+          if (slot_of[(size_t)c] == -2) {
+            slot_of[(size_t)c] = ch.ncam++;
+            pcams.push_back(c);
+          }
+          sp[(size_t)o] = (uint16_t)(slot_of[(size_t)c] | (ch.npts << 8));
+        }
+        ch.nobs += (int32_t)(e - b);
+        ++ch.npts;
+        ++j;
+      }
+      if (ch.npts == 0) {  // a single point larger than a chunk
+        ch.large = 1;
+        ch.npts = 1;
+        ch.nobs = (int32_t)(S.pt_ptr[(size_t)j + 1] - S.pt_ptr[(size_t)j]);
+        ch.ncam = 0;
+        for (int64_t o = S.pt_ptr[(size_t)j]; o < S.pt_ptr[(size_t)j + 1]; ++o) stamp[(size_t)S.p_cam[(size_t)o]] = -1;
+        ++j;
+      }
+      max_cams = std::max(max_cams, ch.ncam);
+      pch.push_back(ch);
+    }
+    P.pt_table_cams = max_cams;
+    P.n_pt_blocks = (int32_t)pch.size();
+    const PtChunk* dpch;
+    if ((rc = upload(C, const_cast<PtChunk**>(&dpch), pch))) return bail(rc);
+    P.pchunks = dpch;
+    const int32_t* dpc;
+    if ((rc = upload(C, const_cast<int32_t**>(&dpc), pcams))) return bail(rc);
+    P.pchunk_cams = dpc;
+    const uint16_t* dsp;
+    if ((rc = upload(C, const_cast<uint16_t**>(&dsp), sp))) return bail(rc);
+    P.p_sp = dsp;
   }
   // scratch
   P.n_cam_eval_blocks = (P.n_own_cams + 127) / 128;
-  P.n_pt_blocks = (P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads;
   P.trace_cap = 1024;
   if ((rc = dalloc(C, &P.partial, (size_t)std::max(P.n_chunks, 1) * 2 * kPartialStride))) return bail(rc);
   if ((rc = dalloc(C, &P.moments, (size_t)std::max(P.n_own_cams, 1) * 2 * kPartialStride))) return bail(rc);

@@ -64,99 +64,151 @@ __global__ void k_extrapolate(IterParams p) {
 //  14 w lam ux  15 w lam uy  16-18 w lam s^m  19 w lam^2
 //  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e
 //  38 w |e|^2   39 a   [40 degenerate pairs]
+struct CamRegs {
+  double R0, R1, R2, R3, R4, R5, R6, R7, R8, tx, ty, tz, d0, d1, d2;
+};
+
+// One observation's contribution to the camera moments at one anchor.
 template <int LOSS, bool ACC>
-__device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc, double gamma) {
+__device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, double2 u, double lx, double ly,
+                                        double lz, double* acc) {
+  const double s = fma(u.x, u.x, u.y * u.y);
+  const double s2 = s * s;
+  const double pz = fma(s, fma(s, c.d2, c.d1), c.d0);  // eq. ray
+  const double vx = lx - c.tx, vy = ly - c.ty, vz = lz - c.tz;
+  const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
+  if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
+    acc[40] += 1.0;
+    return;
+  }
+  // camera-frame point R^T (l - t)
+  const double cx = fma(c.R0, vx, fma(c.R3, vy, c.R6 * vz));
+  const double cy = fma(c.R1, vx, fma(c.R4, vy, c.R7 * vz));
+  const double cz = fma(c.R2, vx, fma(c.R5, vy, c.R8 * vz));
+  const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
+  const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
+  const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
+  double rho = 0;
+  const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
+  const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
+  acc[0] = fma(wx, u.x, acc[0]);
+  acc[1] = fma(wx, u.y, acc[1]);
+  acc[2] = fma(wy, u.y, acc[2]);
+  acc[3] += wx;
+  acc[4] = fma(wx, s, acc[4]);
+  acc[5] = fma(wx, s2, acc[5]);
+  acc[6] += wy;
+  acc[7] = fma(wy, s, acc[7]);
+  acc[8] = fma(wy, s2, acc[8]);
+  acc[9] += w;
+  acc[10] += ws;
+  acc[11] += ws2;
+  acc[12] = fma(ws2, s, acc[12]);
+  acc[13] = fma(ws2, s2, acc[13]);
+  const double wl = w * lam;
+  acc[14] = fma(wl, u.x, acc[14]);
+  acc[15] = fma(wl, u.y, acc[15]);
+  acc[16] += wl;
+  acc[17] = fma(wl, s, acc[17]);
+  acc[18] = fma(wl, s2, acc[18]);
+  acc[19] = fma(wl, lam, acc[19]);
+  const double wex = w * ex, wey = w * ey, wez = w * ez;
+  acc[20] = fma(wex, u.x, acc[20]);
+  acc[21] = fma(wey, u.x, acc[21]);
+  acc[22] = fma(wez, u.x, acc[22]);
+  acc[23] = fma(wex, u.y, acc[23]);
+  acc[24] = fma(wey, u.y, acc[24]);
+  acc[25] = fma(wez, u.y, acc[25]);
+  acc[26] += wex;
+  acc[27] += wey;
+  acc[28] += wez;
+  acc[29] = fma(wex, s, acc[29]);
+  acc[30] = fma(wey, s, acc[30]);
+  acc[31] = fma(wez, s, acc[31]);
+  acc[32] = fma(wex, s2, acc[32]);
+  acc[33] = fma(wey, s2, acc[33]);
+  acc[34] = fma(wez, s2, acc[34]);
+  acc[35] = fma(wl, ex, acc[35]);
+  acc[36] = fma(wl, ey, acc[36]);
+  acc[37] = fma(wl, ez, acc[37]);
+  if (!ACC) {
+    acc[38] = fma(w, sh, acc[38]);
+    acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Per-thread prefetch ring of the camera pass: every thread streams its own observations
+// (o0 + tid + k * kCamPassThreads), so no block synchronisation is needed between the async copies and the math.
+// Units of 16 B, SoA over threads (conflict-free): 0 u, 1 l^k.xy, 2 l^k.z, 3 l^{k-1}.xy, 4 l^{k-1}.z
+constexpr int kRing = 4;
+constexpr int kUnits = 5;
+constexpr int kMaxObsPerThread = kCamChunkObs / kCamPassThreads;
+
+template <int LOSS, bool ACC>
+__device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc, double gamma,
+                                              double2* ring) {
   const double* cam = (ACC ? p.cbar : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
-  const double R0 = cam[0], R1 = cam[1], R2 = cam[2], R3 = cam[3], R4 = cam[4], R5 = cam[5], R6 = cam[6],
-               R7 = cam[7], R8 = cam[8];
-  const double tx = cam[9], ty = cam[10], tz = cam[11];
-  const double d0 = cam[12], d1 = cam[13], d2 = cam[14];
+  CamRegs c;
+  c.R0 = cam[0]; c.R1 = cam[1]; c.R2 = cam[2]; c.R3 = cam[3]; c.R4 = cam[4]; c.R5 = cam[5];
+  c.R6 = cam[6]; c.R7 = cam[7]; c.R8 = cam[8];
+  c.tx = cam[9]; c.ty = cam[10]; c.tz = cam[11];
+  c.d0 = cam[12]; c.d1 = cam[13]; c.d2 = cam[14];
   const double4* __restrict__ Lk = p.pts[p.roles[1]];
   const double4* __restrict__ Lp = p.pts[p.roles[0]];
-  const int64_t o_end = ch.o0 + ch.n;
-  double ndeg = 0;
-  for (int64_t o = ch.o0 + threadIdx.x; o < o_end; o += kCamPassThreads) {
-    const int32_t j = __ldg(p.c_pt + o);
-    const double2 u = __ldg(p.c_uv + o);
-    double lx, ly, lz;
-    ld_point(Lk, j, lx, ly, lz);
-    if (ACC) {  // eq. nesterov_l, on the fly
-      double px, py, pz_;
-      ld_point(Lp, j, px, py, pz_);
-      lx = fma(gamma, lx - px, lx);
-      ly = fma(gamma, ly - py, ly);
-      lz = fma(gamma, lz - pz_, lz);
+  const int tid = threadIdx.x;
+  const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
+  int32_t idx[kMaxObsPerThread];
+#pragma unroll
+  for (int k = 0; k < kMaxObsPerThread; ++k)
+    idx[k] = k < n ? __ldg(p.c_pt + ch.o0 + tid + (int64_t)k * kCamPassThreads) : 0;
+  auto slot = [&](int k, int unit) { return ring + ((k % kRing) * kUnits + unit) * kCamPassThreads + tid; };
+  auto issue = [&](int k) {
+    if (k < n) {
+      cp_async16(slot(k, 0), p.c_uv + ch.o0 + tid + (int64_t)k * kCamPassThreads);
+      const double2* lk = reinterpret_cast<const double2*>(Lk + idx[k]);
+      cp_async16(slot(k, 1), lk);
+      cp_async16(slot(k, 2), lk + 1);
+      if (ACC) {
+        const double2* lp = reinterpret_cast<const double2*>(Lp + idx[k]);
+        cp_async16(slot(k, 3), lp);
+        cp_async16(slot(k, 4), lp + 1);
+      }
     }
-    const double s = fma(u.x, u.x, u.y * u.y);
-    const double s2 = s * s;
-    const double pz = fma(s, fma(s, d2, d1), d0);  // eq. ray
-    const double vx = lx - tx, vy = ly - ty, vz = lz - tz;
-    const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
-    if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
-      ndeg += 1.0;
-      continue;
-    }
-    // camera-frame point R^T (l - t)
-    const double cx = fma(R0, vx, fma(R3, vy, R6 * vz));
-    const double cy = fma(R1, vx, fma(R4, vy, R7 * vz));
-    const double cz = fma(R2, vx, fma(R5, vy, R8 * vz));
-    const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
-    const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
-    const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
-    double rho = 0;
-    const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
-    const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
-    acc[0] = fma(wx, u.x, acc[0]);
-    acc[1] = fma(wx, u.y, acc[1]);
-    acc[2] = fma(wy, u.y, acc[2]);
-    acc[3] += wx;
-    acc[4] = fma(wx, s, acc[4]);
-    acc[5] = fma(wx, s2, acc[5]);
-    acc[6] += wy;
-    acc[7] = fma(wy, s, acc[7]);
-    acc[8] = fma(wy, s2, acc[8]);
-    acc[9] += w;
-    acc[10] += ws;
-    acc[11] += ws2;
-    acc[12] = fma(ws2, s, acc[12]);
-    acc[13] = fma(ws2, s2, acc[13]);
-    const double wl = w * lam;
-    acc[14] = fma(wl, u.x, acc[14]);
-    acc[15] = fma(wl, u.y, acc[15]);
-    acc[16] += wl;
-    acc[17] = fma(wl, s, acc[17]);
-    acc[18] = fma(wl, s2, acc[18]);
-    acc[19] = fma(wl, lam, acc[19]);
-    const double wex = w * ex, wey = w * ey, wez = w * ez;
-    acc[20] = fma(wex, u.x, acc[20]);
-    acc[21] = fma(wey, u.x, acc[21]);
-    acc[22] = fma(wez, u.x, acc[22]);
-    acc[23] = fma(wex, u.y, acc[23]);
-    acc[24] = fma(wey, u.y, acc[24]);
-    acc[25] = fma(wez, u.y, acc[25]);
-    acc[26] += wex;
-    acc[27] += wey;
-    acc[28] += wez;
-    acc[29] = fma(wex, s, acc[29]);
-    acc[30] = fma(wey, s, acc[30]);
-    acc[31] = fma(wez, s, acc[31]);
-    acc[32] = fma(wex, s2, acc[32]);
-    acc[33] = fma(wey, s2, acc[33]);
-    acc[34] = fma(wez, s2, acc[34]);
-    acc[35] = fma(wl, ex, acc[35]);
-    acc[36] = fma(wl, ey, acc[36]);
-    acc[37] = fma(wl, ez, acc[37]);
-    if (!ACC) {
-      acc[38] = fma(w, sh, acc[38]);
-      acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < kRing - 1; ++k) issue(k);
+#pragma unroll
+  for (int k = 0; k < kMaxObsPerThread; ++k) {
+    issue(k + kRing - 1);
+    cp_async_wait<kRing - 1>();
+    if (k < n) {
+      const double2 u = *slot(k, 0);
+      const double2 a = *slot(k, 1), b = *slot(k, 2);
+      double lx = a.x, ly = a.y, lz = b.x;
+      if (ACC) {  // eq. nesterov_l, on the fly
+        const double2 pa = *slot(k, 3), pb = *slot(k, 4);
+        lx = fma(gamma, lx - pa.x, lx);
+        ly = fma(gamma, ly - pa.y, ly);
+        lz = fma(gamma, lz - pb.x, lz);
+      }
+      cam_obs<LOSS, ACC>(p, c, u, lx, ly, lz, acc);
     }
   }
-  acc[40] = ndeg;
+  cp_async_wait<0>();
 }
 
 // Deterministic block reduction of kPartialStride doubles per thread (128 threads) via shared-memory transposes.
-__device__ __forceinline__ void block_reduce_moments(double* acc, double* out) {
-  __shared__ double red[4][32][kPartialStride];
+__device__ __forceinline__ void block_reduce_moments(double* acc, double* out, double* smem) {
+  double(*red)[32][kPartialStride] = reinterpret_cast<double(*)[32][kPartialStride]>(smem);
   __shared__ double wsum[4][kPartialStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -178,19 +230,26 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out) {
   }
 }
 
+constexpr int kCamSmemDoubles = (kRing * kUnits * 2 * kCamPassThreads > 4 * 32 * kPartialStride)
+                                    ? kRing * kUnits * 2 * kCamPassThreads
+                                    : 4 * 32 * kPartialStride;
+
 template <int LOSS>
-__global__ void __launch_bounds__(kCamPassThreads) k_cam_pass(IterParams p) {
+__global__ void __launch_bounds__(kCamPassThreads, 3) k_cam_pass(IterParams p) {
+  __shared__ __align__(16) double smem[kCamSmemDoubles];
   const int chunk = blockIdx.x >> 1;
   const bool acc_anchor = (blockIdx.x & 1) == 0;
   const CamChunk ch = p.chunks[chunk];
   double acc[kPartialStride];
 #pragma unroll
   for (int k = 0; k < kPartialStride; ++k) acc[k] = 0.0;
+  double2* ring = reinterpret_cast<double2*>(smem);
   if (acc_anchor)
-    cam_pass_body<LOSS, true>(p, ch, acc, p.sched[3]);
+    cam_pass_body<LOSS, true>(p, ch, acc, p.sched[3], ring);
   else
-    cam_pass_body<LOSS, false>(p, ch, acc, 0.0);
-  block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride);
+    cam_pass_body<LOSS, false>(p, ch, acc, 0.0, ring);
+  __syncthreads();  // the ring is reused as the reduction buffer
+  block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride, smem);
 }
 
 // ------------------------------------------------------------------ objective F(x^k) only
@@ -285,51 +344,151 @@ __device__ __forceinline__ void pt_terms(const double* cam, double lx, double ly
   Cz = fma(wl, ez, Cz);
 }
 
-template <int LOSS>
-__global__ void __launch_bounds__(kPtPassThreads) k_pt_pass(IterParams p) {
-  const int j = blockIdx.x * kPtPassThreads + threadIdx.x;
-  double q[kPtCols] = {0, 0, 0, 0};
-  if (j < p.n_own_pts) {
-    const double gamma = p.sched[3];
-    const double4 lk = p.pts[p.roles[1]][j];
-    const double4 lp = p.pts[p.roles[0]][j];
-    const double bx = fma(gamma, lk.x - lp.x, lk.x), by = fma(gamma, lk.y - lp.y, lk.y),
-                 bz = fma(gamma, lk.z - lp.z, lk.z);  // eq. nesterov_l
-    double Ab = 0, Cbx = 0, Cby = 0, Cbz = 0, Ak = 0, Ckx = 0, Cky = 0, Ckz = 0;
-    const double* cams_k = p.cams[p.roles[1]];
-    for (int64_t o = p.p_ptr[j]; o < p.p_ptr[j + 1]; ++o) {
-      const int32_t i = p.p_cam[o];
-      const double2 u = p.p_uv[o];
-      pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, bx, by, bz, u, p, Ab, Cbx, Cby, Cbz);
-      pt_terms<LOSS>(cams_k + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, Ak, Ckx, Cky, Ckz);
-    }
-    // exact minimiser: (2 A + xi) dl = C  (eq. Q with the proximal term of eq. Ealpha)
-    const double ib = 1.0 / fma(2.0, Ab, p.xi), ik = 1.0 / fma(2.0, Ak, p.xi);
-    const double ax = fma(Cbx, ib, bx), ay = fma(Cby, ib, by), az = fma(Cbz, ib, bz);  // l_acc
-    const double mx = Ckx * ik, my = Cky * ik, mz = Ckz * ik;                          // l_mm - l^k
-    p.pts[p.roles[2]][j] = make_double4(ax, ay, az, 0.0);
-    p.pts[p.roles[3]][j] = make_double4(lk.x + mx, lk.y + my, lk.z + mz, 0.0);
-    // Q-part of E(x|x^k) - E(x^k|x^k): (A_k + xi/2) |dl|^2 - C_k . dl  (eq. Q expanded at the anchor)
-    const double dx = ax - lk.x, dy = ay - lk.y, dz = az - lk.z;
-    const double n_acc = fma(dx, dx, fma(dy, dy, dz * dz));
-    const double n_mm = fma(mx, mx, fma(my, my, mz * mz));
-    const double hk = fma(0.5, p.xi, Ak);
-    q[0] = fma(hk, n_acc, -fma(Ckx, dx, fma(Cky, dy, Ckz * dz)));
-    q[1] = fma(hk, n_mm, -fma(Ckx, mx, fma(Cky, my, Ckz * mz)));
-    q[2] = n_acc;
-    q[3] = n_mm;
-  }
-  __shared__ double sq[kPtCols][kPtPassThreads];
+// Solve both anchors' point subproblems from their sums and write the candidates; returns the Q-part of
+// E(x_acc|x^k) - E(x^k|x^k), of E(x_mm|x^k) - E(x^k|x^k), and the squared moves (q[0..3]).
+__device__ __forceinline__ void pt_finish(const IterParams& p, int j, const double* lb, const double* lk,
+                                          const double* a, double* q) {
+  // exact minimiser: (2 A + xi) dl = C  (eq. Q with the proximal term of eq. Ealpha)
+  const double ib = 1.0 / fma(2.0, a[0], p.xi), ik = 1.0 / fma(2.0, a[4], p.xi);
+  const double ax = fma(a[1], ib, lb[0]), ay = fma(a[2], ib, lb[1]), az = fma(a[3], ib, lb[2]);  // l_acc
+  const double mx = a[5] * ik, my = a[6] * ik, mz = a[7] * ik;                                  // l_mm - l^k
+  p.pts[p.roles[2]][j] = make_double4(ax, ay, az, 0.0);
+  p.pts[p.roles[3]][j] = make_double4(lk[0] + mx, lk[1] + my, lk[2] + mz, 0.0);
+  // Q-part of E(x|x^k) - E(x^k|x^k): (A_k + xi/2) |dl|^2 - C_k . dl  (eq. Q expanded at the anchor)
+  const double dx = ax - lk[0], dy = ay - lk[1], dz = az - lk[2];
+  const double n_acc = fma(dx, dx, fma(dy, dy, dz * dz));
+  const double n_mm = fma(mx, mx, fma(my, my, mz * mz));
+  const double hk = fma(0.5, p.xi, a[4]);
+  q[0] = fma(hk, n_acc, -fma(a[5], dx, fma(a[6], dy, a[7] * dz)));
+  q[1] = fma(hk, n_mm, -fma(a[5], mx, fma(a[6], my, a[7] * mz)));
+  q[2] = n_acc;
+  q[3] = n_mm;
+}
+
+__device__ __forceinline__ void pt_block_store(double* q, double* red, double* out) {
+  // deterministic block tree over kPtPassThreads threads, kPtCols columns (red: kPtCols x kPtPassThreads)
 #pragma unroll
-  for (int c = 0; c < kPtCols; ++c) sq[c][threadIdx.x] = q[c];
+  for (int c = 0; c < kPtCols; ++c) red[c * kPtPassThreads + threadIdx.x] = q[c];
   __syncthreads();
   for (int st = kPtPassThreads / 2; st > 0; st >>= 1) {
     if (threadIdx.x < st)
 #pragma unroll
-      for (int c = 0; c < kPtCols; ++c) sq[c][threadIdx.x] += sq[c][threadIdx.x + st];
+      for (int c = 0; c < kPtCols; ++c) red[c * kPtPassThreads + threadIdx.x] += red[c * kPtPassThreads + threadIdx.x + st];
     __syncthreads();
   }
-  if (threadIdx.x < kPtCols) p.pt_part[(size_t)blockIdx.x * kPtCols + threadIdx.x] = sq[threadIdx.x][0];
+  if (threadIdx.x < kPtCols) out[threadIdx.x] = red[threadIdx.x * kPtPassThreads];
+}
+
+// A single point with more observations / distinct cameras than a chunk holds: one CTA, cameras from global.
+template <int LOSS>
+__device__ void pt_pass_large(const IterParams& p, const PtChunk& ch, double* red) {
+  const int j = ch.p0;
+  const double gamma = p.sched[3];
+  const double4 lk4 = p.pts[p.roles[1]][j], lp4 = p.pts[p.roles[0]][j];
+  const double lk[3] = {lk4.x, lk4.y, lk4.z};
+  const double lb[3] = {fma(gamma, lk4.x - lp4.x, lk4.x), fma(gamma, lk4.y - lp4.y, lk4.y),
+                        fma(gamma, lk4.z - lp4.z, lk4.z)};
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const double* cams_k = p.cams[p.roles[1]];
+  for (int o = threadIdx.x; o < ch.nobs; o += kPtPassThreads) {
+    const int32_t i = p.p_cam[ch.o0 + o];
+    const double2 u = p.p_uv[ch.o0 + o];
+    pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, lb[0], lb[1], lb[2], u, p, a[0], a[1], a[2], a[3]);
+    pt_terms<LOSS>(cams_k + (size_t)i * kCamStride, lk[0], lk[1], lk[2], u, p, a[4], a[5], a[6], a[7]);
+  }
+  // block sum of the 8 sums (two rounds of the kPtCols-wide tree)
+  double tot[8];
+  for (int h = 0; h < 2; ++h) {
+    double q[kPtCols] = {a[4 * h], a[4 * h + 1], a[4 * h + 2], a[4 * h + 3]};
+    double r[kPtCols];
+    pt_block_store(q, red, r);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int c = 0; c < 4; ++c) tot[4 * h + c] = red[c * kPtPassThreads];
+    __syncthreads();
+  }
+  double q[kPtCols] = {0, 0, 0, 0};
+  if (threadIdx.x == 0) pt_finish(p, j, lb, lk, tot, q);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < kPtCols; ++c) p.pt_part[(size_t)blockIdx.x * kPtCols + c] = q[c];
+}
+
+// Point pass over one chunk (a7 fused with a4/a5 on the point side): the chunk's cameras (both anchors) are
+// staged in shared memory once; each round, one observation per thread computes its contributions
+// (w lam^2, w lam R e) at both anchors into a shared stage; then each point's owner thread adds its
+// observations' entries in ascending order.  No atomics; sums are deterministic.
+template <int LOSS>
+__global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_pass(IterParams p) {
+  extern __shared__ double smem[];
+  const PtChunk ch = p.pchunks[blockIdx.x];
+  const int T = p.pt_table_cams;
+  double* scam = smem;                             // [2][T][kPtCamStride]
+  double* spt = scam + 2 * T * kPtCamStride;       // [kPtPassThreads][8]: x-bar, x^k
+  double* stage = spt + 8 * kPtPassThreads;        // [8][kPtPassThreads]
+  if (ch.large) {
+    pt_pass_large<LOSS>(p, ch, stage);
+    return;
+  }
+  const double gamma = p.sched[3];
+  const double* cb = p.cbar;
+  const double* ck = p.cams[p.roles[1]];
+  for (int idx = threadIdx.x; idx < ch.ncam * 32; idx += kPtPassThreads) {
+    const int slot = idx >> 5, a = (idx >> 4) & 1, k = idx & 15;
+    if (k < 15) {
+      const int32_t cam = p.pchunk_cams[ch.c0 + slot];
+      scam[(a * T + slot) * kPtCamStride + k] = (a ? ck : cb)[(size_t)cam * kCamStride + k];
+    }
+  }
+  const int q = threadIdx.x;
+  const bool own = q < ch.npts;
+  double lb[3] = {0, 0, 0}, lk[3] = {0, 0, 0};
+  int64_t pb = 0, pe = 0;
+  if (own) {
+    const int j = ch.p0 + q;
+    const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
+    lk[0] = k4.x;
+    lk[1] = k4.y;
+    lk[2] = k4.z;
+    lb[0] = fma(gamma, k4.x - p4.x, k4.x);  // eq. nesterov_l
+    lb[1] = fma(gamma, k4.y - p4.y, k4.y);
+    lb[2] = fma(gamma, k4.z - p4.z, k4.z);
+    double* P = spt + 8 * q;
+    P[0] = lb[0];
+    P[1] = lb[1];
+    P[2] = lb[2];
+    P[3] = lk[0];
+    P[4] = lk[1];
+    P[5] = lk[2];
+    pb = p.p_ptr[j] - ch.o0;
+    pe = p.p_ptr[j + 1] - ch.o0;
+  }
+  __syncthreads();
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r0 = 0; r0 < ch.nobs; r0 += kPtPassThreads) {
+    const int o = r0 + threadIdx.x;
+    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (o < ch.nobs) {
+      const uint32_t sp = p.p_sp[ch.o0 + o];
+      const int slot = sp & 255, lp = sp >> 8;
+      const double2 u = p.p_uv[ch.o0 + o];
+      const double* P = spt + 8 * lp;
+      pt_terms<LOSS>(scam + slot * kPtCamStride, P[0], P[1], P[2], u, p, c[0], c[1], c[2], c[3]);
+      pt_terms<LOSS>(scam + (T + slot) * kPtCamStride, P[3], P[4], P[5], u, p, c[4], c[5], c[6], c[7]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) stage[k * kPtPassThreads + threadIdx.x] = c[k];
+    __syncthreads();
+    if (own) {
+      const int64_t a0 = pb > r0 ? pb : r0, a1 = pe < r0 + kPtPassThreads ? pe : r0 + kPtPassThreads;
+      for (int64_t pos = a0; pos < a1; ++pos)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += stage[k * kPtPassThreads + (pos - r0)];
+    }
+    __syncthreads();
+  }
+  double qv[kPtCols] = {0, 0, 0, 0};
+  if (own) pt_finish(p, ch.p0 + q, lb, lk, acc, qv);
+  pt_block_store(qv, stage, p.pt_part + (size_t)blockIdx.x * kPtCols);
 }
 
 // ------------------------------------------------------------------ a6: camera solve
@@ -715,12 +874,27 @@ int launch_cam_pass(const IterParams& p, cudaStream_t st) {
   return 1;
 }
 
+size_t pt_pass_smem(const IterParams& p) {
+  return sizeof(double) * ((size_t)2 * p.pt_table_cams * kPtCamStride + 16 * kPtPassThreads);
+}
+
+template <int LOSS>
+static void pt_launch(const IterParams& p, cudaStream_t st) {
+  const size_t sm = pt_pass_smem(p);
+  static size_t configured = 0;
+  if (sm > configured) {
+    cudaFuncSetAttribute(k_pt_pass<LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = sm;
+  }
+  k_pt_pass<LOSS><<<p.n_pt_blocks, kPtPassThreads, sm, st>>>(p);
+}
+
 int launch_pt_pass(const IterParams& p, cudaStream_t st) {
   if (p.n_pt_blocks == 0) return 0;
   switch (p.loss) {
-    case kHuber: k_pt_pass<kHuber><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
-    case kCauchy: k_pt_pass<kCauchy><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
-    default: k_pt_pass<kTrivial><<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p); break;
+    case kHuber: pt_launch<kHuber>(p, st); break;
+    case kCauchy: pt_launch<kCauchy>(p, st); break;
+    default: pt_launch<kTrivial>(p, st); break;
   }
   return 1;
 }

@@ -12,11 +12,22 @@ constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camer
 constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
 constexpr int kCamPassThreads = 128;
 constexpr int kCamChunkObs = 128 * 16;  // observations per camera-pass chunk (one CTA)
-constexpr int kPtPassThreads = 128;
+constexpr int kPtPassThreads = 256;     // point pass: threads per CTA = max points per chunk
+constexpr int kPtMaxCams = 256;         // camera-table slots per point chunk (uint8 slot ids)
+constexpr int kPtChunkObs = 4096;       // observations per point chunk (larger single points: "large" chunks)
+constexpr int kPtCamStride = 17;        // doubles per camera in the shared-memory table (bank spread)
 constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
 constexpr int kGlobalCols = 10;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kTraceCols = 10;    // = DABA_TRACE_COLS
+
+// A point chunk: consecutive owned points [p0, p0 + npts) whose observations [o0, o0 + nobs) (point side) read at
+// most kPtMaxCams distinct cameras, listed at chunk_cams[c0 .. c0 + ncam).  large = 1: a single point with more
+// observations / cameras than a chunk holds (its cameras are read from global memory).
+struct PtChunk {
+  int64_t o0;
+  int32_t nobs, p0, npts, c0, ncam, large;
+};
 
 struct CamChunk {
   int32_t cam;    // local camera index (owned)
@@ -51,7 +62,11 @@ struct IterParams {
   // point-side observations (sorted by point, then camera)
   const int64_t* p_ptr;          // n_own_pts + 1
   const double2* p_uv;
-  const int32_t* p_cam;
+  const int32_t* p_cam;          // local camera of each point-side observation
+  const uint16_t* p_sp;          // (camera slot in the chunk table) | (point index in the chunk) << 8
+  const PtChunk* pchunks;
+  const int32_t* pchunk_cams;
+  int32_t pt_table_cams;         // max ncam over chunks (shared-memory table size)
   // scratch
   double* partial;        // n_chunks * 2 * kPartialStride
   double* moments;        // n_own_cams * 2 * kNumMoments (summed per camera)
