@@ -151,6 +151,22 @@ int daba_reset_kernel_times(daba_ctx* ctx);
 /* Number of kernel launches one iteration performs on this rank. */
 int daba_launches_per_iteration(daba_ctx* ctx);
 
+/* ---- host-only shard planning (no CUDA calls; usable on machines without a GPU) ----
+ * The partition daba_create uses, exposed for tests and tooling.  Returns NULL on invalid input. */
+typedef struct daba_plan daba_plan;
+daba_plan* daba_plan_create(int64_t M, int64_t N, const int32_t* obs_cam, const int32_t* obs_pt, int64_t K,
+                            const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks);
+/* counts[0..9] = owned cams, owned points, halo cams, halo points, camera-side obs, point-side obs, doubles sent
+ * per iteration, doubles received per iteration, number of peers, (reserved 0) */
+int daba_plan_counts(const daba_plan* p, int64_t counts[10]);
+/* which: 0 local->global cameras (owned then halo), 1 local->global points, 2 camera owners (M), 3 point owners (N),
+ *        4 peer ranks (counts[8]) */
+int daba_plan_array(const daba_plan* p, int which, int32_t* out);
+/* Per peer (index into the peer list): kind 0 send cameras, 1 send points, 2 recv cameras, 3 recv points, as
+ * GLOBAL ids in exchange order.  Returns the length (call with out = NULL to size). */
+int64_t daba_plan_peer_list(const daba_plan* p, int peer, int kind, int32_t* out);
+void daba_plan_destroy(daba_plan* p);
+
 const char* daba_last_error(const daba_ctx* ctx);
 void daba_destroy(daba_ctx* ctx);
 

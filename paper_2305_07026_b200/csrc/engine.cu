@@ -393,8 +393,10 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return bail(rc);
   }
   if ((rc = dalloc(C, &P.cbar, (size_t)P.n_cams * kCamStride))) return bail(rc);
+  for (int r = 0; r < 2; ++r)
+    if ((rc = dalloc(C, &P.lbar[r], (size_t)P.n_pts))) return bail(rc);
   {
-    std::vector<int32_t> roles = {0, 1, 2, 3};
+    std::vector<int32_t> roles = {0, 1, 2, 3, 0};
     if ((rc = upload(C, &P.roles, roles))) return bail(rc);
   }
   // camera side + chunks
@@ -428,88 +430,42 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return bail(rc);
     P.cam_chunk_ptr = dcp;
   }
-  // point side + point chunks (camera tables for the shared-memory staged point pass)
+  // point side: records written by the camera pass at its observation index; boundary observations (camera
+  // owned elsewhere) are recomputed into records n_cam_side + b
   {
-    const size_t kp = S.p_obs.size();
-    std::vector<double2> uv(kp);
-    for (size_t q = 0; q < kp; ++q) uv[q] = make_double2(obs_uv[2 * S.p_obs[q]], obs_uv[2 * S.p_obs[q] + 1]);
-    const double2* duv;
-    if ((rc = upload(C, const_cast<double2**>(&duv), uv))) return bail(rc);
-    P.p_uv = duv;
-    const int32_t* dcam;
-    if ((rc = upload(C, const_cast<int32_t**>(&dcam), S.p_cam))) return bail(rc);
-    P.p_cam = dcam;
+    const size_t kp = S.p_obs.size(), kc = S.c_obs.size();
     const int64_t* dptr;
     if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
     P.p_ptr = dptr;
-    std::vector<PtChunk> pch;
-    std::vector<int32_t> pcams;
-    std::vector<uint16_t> sp(kp, 0);
-    std::vector<int32_t> slot_of((size_t)std::max<size_t>(S.cam_g.size(), 1), -1);
-    std::vector<int32_t> stamp((size_t)std::max<size_t>(S.cam_g.size(), 1), -1);
-    int32_t max_cams = 1;
-    int32_t j = 0;
-    while (j < S.n_own_pts) {
-      PtChunk ch{};
-      ch.o0 = S.pt_ptr[(size_t)j];
-      ch.p0 = j;
-      ch.c0 = (int32_t)pcams.size();
-      const int32_t id = (int32_t)pch.size();
-      // greedy: add points while the chunk stays within its limits
-      while (j < S.n_own_pts && ch.npts < kPtPassThreads) {
-        const int64_t b = S.pt_ptr[(size_t)j], e = S.pt_ptr[(size_t)j + 1];
-        int32_t fresh = 0;
-        for (int64_t o = b; o < e; ++o) {
-          const int32_t c = S.p_cam[(size_t)o];
-          if (stamp[(size_t)c] != id) {
-            stamp[(size_t)c] = id;
-            slot_of[(size_t)c] = -2;  // tentatively new
-            ++fresh;
-          }
-        }
-        const bool fits = ch.nobs + (e - b) <= kPtChunkObs && ch.ncam + fresh <= kPtMaxCams;
-        if (!fits) {
-          // roll back the tentative marks of this point
-          for (int64_t o = b; o < e; ++o) {
-            const int32_t c = S.p_cam[(size_t)o];
-            if (slot_of[(size_t)c] == -2) stamp[(size_t)c] = -1;
-          }
-          break;
-        }
-        for (int64_t o = b; o < e; ++o) {
-          const int32_t c = S.p_cam[(size_t)o];
-          if (slot_of[(size_t)c] == -2) {
-            slot_of[(size_t)c] = ch.ncam++;
-            pcams.push_back(c);
-          }
-          sp[(size_t)o] = (uint16_t)(slot_of[(size_t)c] | (ch.npts << 8));
-        }
-        ch.nobs += (int32_t)(e - b);
-        ++ch.npts;
-        ++j;
+    std::vector<int32_t> cam_side_of((size_t)K, -1);
+    for (size_t q = 0; q < kc; ++q) cam_side_of[(size_t)S.c_obs[q]] = (int32_t)q;
+    std::vector<int32_t> src(kp), bcam, bpt;
+    std::vector<double2> buv;
+    for (size_t q = 0; q < kp; ++q) {
+      const int32_t r = cam_side_of[(size_t)S.p_obs[q]];
+      if (r >= 0) {
+        src[q] = r;
+        continue;
       }
-      if (ch.npts == 0) {  // a single point larger than a chunk
-        ch.large = 1;
-        ch.npts = 1;
-        ch.nobs = (int32_t)(S.pt_ptr[(size_t)j + 1] - S.pt_ptr[(size_t)j]);
-        ch.ncam = 0;
-        for (int64_t o = S.pt_ptr[(size_t)j]; o < S.pt_ptr[(size_t)j + 1]; ++o) stamp[(size_t)S.p_cam[(size_t)o]] = -1;
-        ++j;
-      }
-      max_cams = std::max(max_cams, ch.ncam);
-      pch.push_back(ch);
+      src[q] = (int32_t)(kc + bcam.size());
+      bcam.push_back(S.p_cam[q]);
+      bpt.push_back(S.p_pt[q]);
+      buv.push_back(make_double2(obs_uv[2 * S.p_obs[q]], obs_uv[2 * S.p_obs[q] + 1]));
     }
-    P.pt_table_cams = max_cams;
-    P.n_pt_blocks = (int32_t)pch.size();
-    const PtChunk* dpch;
-    if ((rc = upload(C, const_cast<PtChunk**>(&dpch), pch))) return bail(rc);
-    P.pchunks = dpch;
-    const int32_t* dpc;
-    if ((rc = upload(C, const_cast<int32_t**>(&dpc), pcams))) return bail(rc);
-    P.pchunk_cams = dpc;
-    const uint16_t* dsp;
-    if ((rc = upload(C, const_cast<uint16_t**>(&dsp), sp))) return bail(rc);
-    P.p_sp = dsp;
+    P.n_cam_side = (int64_t)kc;
+    P.n_boundary = (int64_t)bcam.size();
+    P.n_records = std::max<int64_t>(P.n_cam_side + P.n_boundary, 1);
+    if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
+    const int32_t *d0, *d1, *d2;
+    const double2* d4;
+    if ((rc = upload(C, const_cast<int32_t**>(&d0), src)) || (rc = upload(C, const_cast<int32_t**>(&d1), bcam)) ||
+        (rc = upload(C, const_cast<int32_t**>(&d2), bpt)) || (rc = upload(C, const_cast<double2**>(&d4), buv)))
+      return bail(rc);
+    P.p_src = d0;
+    P.b_cam = d1;
+    P.b_pt = d2;
+    P.b_uv = d4;
+    P.n_pt_blocks = (P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads;
   }
   // scratch
   P.n_cam_eval_blocks = (P.n_own_cams + 127) / 128;
@@ -520,10 +476,11 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   if ((rc = dalloc(C, &P.decisions, (size_t)std::max(P.n_own_cams, 1) * 2))) return bail(rc);
   if ((rc = dalloc(C, &P.cam_part, (size_t)std::max(P.n_cam_eval_blocks, 1) * kCamEvalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.pt_part, (size_t)std::max(P.n_pt_blocks, 1) * kPtCols))) return bail(rc);
+  if ((rc = dalloc(C, &P.red_part, (size_t)kReduceBlocks * kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.local, kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.global, kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.sched, 4))) return bail(rc);
+  if ((rc = dalloc(C, &P.sched, 8))) return bail(rc);
   if (nranks == 1) P.global = P.local;
   cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
   // halo plan
@@ -565,13 +522,14 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   double F0 = 0, nd = 0;
   if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
   {
-    const double sched[4] = {1.0, F0, 0.0, 0.0};
-    if (cudaMemcpyAsync(P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, C->stream) != cudaSuccess ||
-        cudaStreamSynchronize(C->stream) != cudaSuccess)
+    const double sched[8] = {1.0, F0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (cudaMemcpyAsync(P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, C->stream) != cudaSuccess)
       return bail(DABA_E_CUDA);
+    launch_lbar_all(P, C->stream);  // x-bar^0 = x^0 (gamma^{(0)} = 0)
+    if (cudaStreamSynchronize(C->stream) != cudaSuccess) return bail(DABA_E_CUDA);
   }
   // launches per iteration (for bookkeeping)
-  C->launches_per_iter = 7 - (P.n_chunks == 0) - (P.n_pt_blocks == 0) - (P.n_own_cams == 0) * 2;
+  C->launches_per_iter = 8 - (P.n_chunks == 0) - (P.n_pt_blocks == 0) - (P.n_own_cams == 0) * 2 + (P.n_boundary > 0);
   for (size_t q = 0; q < C->segs.size(); ++q)
     C->launches_per_iter += (C->peer_cam_idx[2 * q].second + C->peer_pt_idx[2 * q].second > 0) +
                             (C->peer_cam_idx[2 * q + 1].second + C->peer_pt_idx[2 * q + 1].second > 0);
@@ -725,6 +683,7 @@ extern "C" int daba_set_state_native(daba_ctx* ctx, const double* cams_k, const 
   sched[0] = s;
   sched[1] = Fbar;
   CUDA_OR(ctx, cudaMemcpyAsync(ctx->P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, ctx->stream));
+  launch_lbar_all(ctx->P, ctx->stream);  // x-bar^k of the resumed state
   CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
   return DABA_OK;
 }

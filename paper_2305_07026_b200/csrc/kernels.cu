@@ -28,6 +28,16 @@ __device__ __forceinline__ double sched_gamma(double s, int accelerate, double* 
   return accelerate ? (s - 1.0) / s_next : 0.0;
 }
 
+// 256-bit global access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): one instruction per 32-byte record.
+__device__ __forceinline__ double4 ld256(const double4* q) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
+  return v;
+}
+__device__ __forceinline__ void st256(double4* q, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+
 // Point record: 32 bytes (x, y, z, pad) — one sector per gather.
 __device__ __forceinline__ void ld_point(const double4* base, int64_t j, double& x, double& y, double& z) {
   const double2* q = reinterpret_cast<const double2*>(base + j);
@@ -41,7 +51,18 @@ __device__ __forceinline__ void ld_point(const double4* base, int64_t j, double&
 __global__ void k_extrapolate(IterParams p) {
   const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) p.sched[3] = gamma;
+  if (i == 0) {
+    p.sched[3] = gamma;
+    double s1;
+    sched_gamma(p.sched[0], p.accelerate, &s1);
+    p.sched[4] = sched_gamma(s1, p.accelerate, nullptr);  // gamma^{(k+1)}
+  }
+  if (i < p.n_pts - p.n_own_pts) {  // halo points: eq. nesterov_l from the exchanged x^k and the cached x^{k-1}
+    const int j = p.n_own_pts + i;
+    const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
+    p.lbar[p.roles[4]][j] = make_double4(fma(gamma, k4.x - p4.x, k4.x), fma(gamma, k4.y - p4.y, k4.y),
+                                         fma(gamma, k4.z - p4.z, k4.z), 0.0);
+  }
   if (i >= p.n_cams) return;
   const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
   const double* cp = p.cams[p.roles[0]] + (size_t)i * kCamStride;
@@ -64,33 +85,68 @@ __global__ void k_extrapolate(IterParams p) {
 //  14 w lam ux  15 w lam uy  16-18 w lam s^m  19 w lam^2
 //  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e
 //  38 w |e|^2   39 a   [40 degenerate pairs]
+// Camera record kept in shared memory and re-read at every use (volatile shared loads are not hoisted into
+// registers): frees ~30 registers per thread in the camera pass, i.e. one more resident CTA per SM.
+#ifdef DABA_CAM_REGS
 struct CamRegs {
-  double R0, R1, R2, R3, R4, R5, R6, R7, R8, tx, ty, tz, d0, d1, d2;
+  double v[15];
+  __device__ __forceinline__ double operator[](int k) const { return v[k]; }
 };
+#else
+struct CamRegs {
+  const double* sm;  // shared-memory camera record (16 doubles)
+  __device__ __forceinline__ double operator[](int k) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(sm + k)));
+    return v;
+  }
+};
+#endif
+#ifndef DABA_RING
+#define DABA_RING 4
+#endif
+#ifndef DABA_MINB
+#define DABA_MINB 4
+#endif
 
 // One observation's contribution to the camera moments at one anchor.
 template <int LOSS, bool ACC>
 __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, double2 u, double lx, double ly,
-                                        double lz, double* acc) {
+                                        double lz, double* acc, int64_t rec) {
   const double s = fma(u.x, u.x, u.y * u.y);
   const double s2 = s * s;
-  const double pz = fma(s, fma(s, c.d2, c.d1), c.d0);  // eq. ray
-  const double vx = lx - c.tx, vy = ly - c.ty, vz = lz - c.tz;
+  const double pz = fma(s, fma(s, c[14], c[13]), c[12]);  // eq. ray
+  const double vx = lx - c[9], vy = ly - c[10], vz = lz - c[11];
   const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
   if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
     acc[40] += 1.0;
+    st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec, make_double4(0.0, 0.0, 0.0, 0.0));
     return;
   }
   // camera-frame point R^T (l - t)
-  const double cx = fma(c.R0, vx, fma(c.R3, vy, c.R6 * vz));
-  const double cy = fma(c.R1, vx, fma(c.R4, vy, c.R7 * vz));
-  const double cz = fma(c.R2, vx, fma(c.R5, vy, c.R8 * vz));
+  const double cx = fma(c[0], vx, fma(c[3], vy, c[6] * vz));
+  const double cy = fma(c[1], vx, fma(c[4], vy, c[7] * vz));
+  const double cz = fma(c[2], vx, fma(c[5], vy, c[8] * vz));
+#ifdef DABA_FASTRCP
+  double rn = (double)__frcp_rn((float)nv);
+  rn = rn * fma(-nv, rn, 2.0);
+  rn = rn * fma(-nv, rn, 2.0);
+  rn = fma(rn, fma(-nv, rn, 1.0), rn);
+  const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * rn;
+#else
   const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
+#endif
   const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
   const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
   double rho = 0;
   const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
   const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
+#ifdef DABA_NOMOM
+  acc[0] += w; acc[1] += wx * lam; acc[2] += wy * ex; acc[3] += ws * ey + ez;
+  if (!ACC) { acc[38] = fma(w, sh, acc[38]); acc[39] += 0.5 * fma(-w, sh, rho); }
+  const double wl = w * lam;
+  if (false) {
+#endif
   acc[0] = fma(wx, u.x, acc[0]);
   acc[1] = fma(wx, u.y, acc[1]);
   acc[2] = fma(wy, u.y, acc[2]);
@@ -135,73 +191,76 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
     acc[38] = fma(w, sh, acc[38]);
     acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
   }
+#ifdef DABA_NOMOM
+  }
+#endif
+#ifdef DABA_NOEMIT
+  if (rec < 0) {
+#endif
+  // point side of the same pair: (w lam^2, w lam R e) with the world-frame error R e (eq. Q's sums), written
+  // coalesced at the camera-side index (one 32-byte record per anchor)
+  const double gx = fma(c[0], ex, fma(c[1], ey, c[2] * ez));
+  const double gy = fma(c[3], ex, fma(c[4], ey, c[5] * ez));
+  const double gz = fma(c[6], ex, fma(c[7], ey, c[8] * ez));
+  st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec,
+        make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
+#ifdef DABA_NOEMIT
+  }
+#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Per-thread prefetch ring of the camera pass: every thread streams its own observations
-// (o0 + tid + k * kCamPassThreads), so no block synchronisation is needed between the async copies and the math.
-// Units of 16 B, SoA over threads (conflict-free): 0 u, 1 l^k.xy, 2 l^k.z, 3 l^{k-1}.xy, 4 l^{k-1}.z
-constexpr int kRing = 4;
-constexpr int kUnits = 5;
-constexpr int kMaxObsPerThread = kCamChunkObs / kCamPassThreads;
+// Camera-pass streaming: u (coalesced) goes through a per-thread cp.async ring; the anchor point record
+// (x-bar^k for the accelerated anchor, x^k for the MM anchor; 32 B) is gathered with one 256-bit load,
+// prefetched one observation ahead in registers.  The chunk's point indices are staged in shared memory.
+constexpr int kRing = DABA_RING;
 
 template <int LOSS, bool ACC>
-__device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc, double gamma,
-                                              double2* ring) {
+__device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc,
+                                              double2* ring, int32_t* sidx) {
   const double* cam = (ACC ? p.cbar : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
+#ifdef DABA_CAM_REGS
   CamRegs c;
-  c.R0 = cam[0]; c.R1 = cam[1]; c.R2 = cam[2]; c.R3 = cam[3]; c.R4 = cam[4]; c.R5 = cam[5];
-  c.R6 = cam[6]; c.R7 = cam[7]; c.R8 = cam[8];
-  c.tx = cam[9]; c.ty = cam[10]; c.tz = cam[11];
-  c.d0 = cam[12]; c.d1 = cam[13]; c.d2 = cam[14];
-  const double4* __restrict__ Lk = p.pts[p.roles[1]];
-  const double4* __restrict__ Lp = p.pts[p.roles[0]];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) c.v[k] = cam[k];
+#else
+  __shared__ double scam[kCamStride];
+  if (threadIdx.x < kCamStride) scam[threadIdx.x] = cam[threadIdx.x];
+  CamRegs c{scam};
+#endif
+  const double4* __restrict__ L = ACC ? p.lbar[p.roles[4]] : p.pts[p.roles[1]];
   const int tid = threadIdx.x;
   const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
-  int32_t idx[kMaxObsPerThread];
-#pragma unroll
-  for (int k = 0; k < kMaxObsPerThread; ++k)
-    idx[k] = k < n ? __ldg(p.c_pt + ch.o0 + tid + (int64_t)k * kCamPassThreads) : 0;
-  auto slot = [&](int k, int unit) { return ring + ((k % kRing) * kUnits + unit) * kCamPassThreads + tid; };
+  for (int o = tid; o < ch.n; o += kCamPassThreads) sidx[o] = __ldg(p.c_pt + ch.o0 + o);
+  __syncthreads();
+  auto uslot = [&](int k) { return ring + (k & (kRing - 1)) * kCamPassThreads + tid; };
   auto issue = [&](int k) {
-    if (k < n) {
-      cp_async16(slot(k, 0), p.c_uv + ch.o0 + tid + (int64_t)k * kCamPassThreads);
-      const double2* lk = reinterpret_cast<const double2*>(Lk + idx[k]);
-      cp_async16(slot(k, 1), lk);
-      cp_async16(slot(k, 2), lk + 1);
-      if (ACC) {
-        const double2* lp = reinterpret_cast<const double2*>(Lp + idx[k]);
-        cp_async16(slot(k, 3), lp);
-        cp_async16(slot(k, 4), lp + 1);
-      }
-    }
+    if (k < n) cp_async16(uslot(k), p.c_uv + ch.o0 + tid + (int64_t)k * kCamPassThreads);
     cp_async_commit();
   };
 #pragma unroll
   for (int k = 0; k < kRing - 1; ++k) issue(k);
-#pragma unroll
-  for (int k = 0; k < kMaxObsPerThread; ++k) {
+  double4 lnext = make_double4(0, 0, 0, 0);
+  if (n > 0) lnext = ld256(L + sidx[tid]);
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const double4 l = lnext;
+    if (k + 1 < n) lnext = ld256(L + sidx[tid + (k + 1) * kCamPassThreads]);
     issue(k + kRing - 1);
     cp_async_wait<kRing - 1>();
-    if (k < n) {
-      const double2 u = *slot(k, 0);
-      const double2 a = *slot(k, 1), b = *slot(k, 2);
-      double lx = a.x, ly = a.y, lz = b.x;
-      if (ACC) {  // eq. nesterov_l, on the fly
-        const double2 pa = *slot(k, 3), pb = *slot(k, 4);
-        lx = fma(gamma, lx - pa.x, lx);
-        ly = fma(gamma, ly - pa.y, ly);
-        lz = fma(gamma, lz - pb.x, lz);
-      }
-      cam_obs<LOSS, ACC>(p, c, u, lx, ly, lz, acc);
-    }
+    const double2 u = *uslot(k);
+    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
   }
   cp_async_wait<0>();
 }
@@ -230,13 +289,13 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, d
   }
 }
 
-constexpr int kCamSmemDoubles = (kRing * kUnits * 2 * kCamPassThreads > 4 * 32 * kPartialStride)
-                                    ? kRing * kUnits * 2 * kCamPassThreads
-                                    : 4 * 32 * kPartialStride;
+constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs / 2;  // ring + indices
+constexpr int kCamSmemDoubles =
+    kCamRingDoubles > 4 * 32 * kPartialStride ? kCamRingDoubles : 4 * 32 * kPartialStride;
 
 template <int LOSS>
-__global__ void __launch_bounds__(kCamPassThreads, 3) k_cam_pass(IterParams p) {
-  __shared__ __align__(16) double smem[kCamSmemDoubles];
+__global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterParams p) {
+  extern __shared__ __align__(16) double smem[];  // kCamSmemDoubles
   const int chunk = blockIdx.x >> 1;
   const bool acc_anchor = (blockIdx.x & 1) == 0;
   const CamChunk ch = p.chunks[chunk];
@@ -244,10 +303,11 @@ __global__ void __launch_bounds__(kCamPassThreads, 3) k_cam_pass(IterParams p) {
 #pragma unroll
   for (int k = 0; k < kPartialStride; ++k) acc[k] = 0.0;
   double2* ring = reinterpret_cast<double2*>(smem);
+  int32_t* sidx = reinterpret_cast<int32_t*>(smem + kRing * 2 * kCamPassThreads);
   if (acc_anchor)
-    cam_pass_body<LOSS, true>(p, ch, acc, p.sched[3], ring);
+    cam_pass_body<LOSS, true>(p, ch, acc, ring, sidx);
   else
-    cam_pass_body<LOSS, false>(p, ch, acc, 0.0, ring);
+    cam_pass_body<LOSS, false>(p, ch, acc, ring, sidx);
   __syncthreads();  // the ring is reused as the reduction buffer
   block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride, smem);
 }
@@ -353,7 +413,12 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
   const double ax = fma(a[1], ib, lb[0]), ay = fma(a[2], ib, lb[1]), az = fma(a[3], ib, lb[2]);  // l_acc
   const double mx = a[5] * ik, my = a[6] * ik, mz = a[7] * ik;                                  // l_mm - l^k
   p.pts[p.roles[2]][j] = make_double4(ax, ay, az, 0.0);
-  p.pts[p.roles[3]][j] = make_double4(lk[0] + mx, lk[1] + my, lk[2] + mz, 0.0);
+  const double nx = lk[0] + mx, ny = lk[1] + my, nz = lk[2] + mz;
+  p.pts[p.roles[3]][j] = make_double4(nx, ny, nz, 0.0);
+  // x-bar^{k+1} for either outcome of the restart test (eq. nesterov_l with gamma^{(k+1)}); k_select keeps one
+  const double g1 = p.sched[4];
+  p.lbar[0][j] = make_double4(fma(g1, ax - lk[0], ax), fma(g1, ay - lk[1], ay), fma(g1, az - lk[2], az), 0.0);
+  p.lbar[1][j] = make_double4(fma(g1, nx - lk[0], nx), fma(g1, ny - lk[1], ny), fma(g1, nz - lk[2], nz), 0.0);
   // Q-part of E(x|x^k) - E(x^k|x^k): (A_k + xi/2) |dl|^2 - C_k . dl  (eq. Q expanded at the anchor)
   const double dx = ax - lk[0], dy = ay - lk[1], dz = az - lk[2];
   const double n_acc = fma(dx, dx, fma(dy, dy, dz * dz));
@@ -365,130 +430,72 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
   q[3] = n_mm;
 }
 
-__device__ __forceinline__ void pt_block_store(double* q, double* red, double* out) {
-  // deterministic block tree over kPtPassThreads threads, kPtCols columns (red: kPtCols x kPtPassThreads)
-#pragma unroll
-  for (int c = 0; c < kPtCols; ++c) red[c * kPtPassThreads + threadIdx.x] = q[c];
-  __syncthreads();
-  for (int st = kPtPassThreads / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st)
-#pragma unroll
-      for (int c = 0; c < kPtCols; ++c) red[c * kPtPassThreads + threadIdx.x] += red[c * kPtPassThreads + threadIdx.x + st];
-    __syncthreads();
-  }
-  if (threadIdx.x < kPtCols) out[threadIdx.x] = red[threadIdx.x * kPtPassThreads];
-}
-
-// A single point with more observations / distinct cameras than a chunk holds: one CTA, cameras from global.
+// Boundary observations (their camera is owned by another rank, N > 1 only): recompute the point-side
+// contribution from the halo camera and write it into the staging record, like the camera pass does.
 template <int LOSS>
-__device__ void pt_pass_large(const IterParams& p, const PtChunk& ch, double* red) {
-  const int j = ch.p0;
-  const double gamma = p.sched[3];
-  const double4 lk4 = p.pts[p.roles[1]][j], lp4 = p.pts[p.roles[0]][j];
-  const double lk[3] = {lk4.x, lk4.y, lk4.z};
-  const double lb[3] = {fma(gamma, lk4.x - lp4.x, lk4.x), fma(gamma, lk4.y - lp4.y, lk4.y),
-                        fma(gamma, lk4.z - lp4.z, lk4.z)};
+__global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= p.n_boundary) return;
+  const int32_t i = p.b_cam[b], j = p.b_pt[b];
+  const double2 u = p.b_uv[b];
+  const double4 lk = p.pts[p.roles[1]][j], lb = p.lbar[p.roles[4]][j];
   double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const double* cams_k = p.cams[p.roles[1]];
-  for (int o = threadIdx.x; o < ch.nobs; o += kPtPassThreads) {
-    const int32_t i = p.p_cam[ch.o0 + o];
-    const double2 u = p.p_uv[ch.o0 + o];
-    pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, lb[0], lb[1], lb[2], u, p, a[0], a[1], a[2], a[3]);
-    pt_terms<LOSS>(cams_k + (size_t)i * kCamStride, lk[0], lk[1], lk[2], u, p, a[4], a[5], a[6], a[7]);
-  }
-  // block sum of the 8 sums (two rounds of the kPtCols-wide tree)
-  double tot[8];
-  for (int h = 0; h < 2; ++h) {
-    double q[kPtCols] = {a[4 * h], a[4 * h + 1], a[4 * h + 2], a[4 * h + 3]};
-    double r[kPtCols];
-    pt_block_store(q, red, r);
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int c = 0; c < 4; ++c) tot[4 * h + c] = red[c * kPtPassThreads];
-    __syncthreads();
-  }
-  double q[kPtCols] = {0, 0, 0, 0};
-  if (threadIdx.x == 0) pt_finish(p, j, lb, lk, tot, q);
-  if (threadIdx.x == 0)
-    for (int c = 0; c < kPtCols; ++c) p.pt_part[(size_t)blockIdx.x * kPtCols + c] = q[c];
+  pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
+  pt_terms<LOSS>(p.cams[p.roles[1]] + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
+  const int64_t r = p.n_cam_side + b;
+  reinterpret_cast<double4*>(p.staging)[r] = make_double4(a[0], a[1], a[2], a[3]);
+  reinterpret_cast<double4*>(p.staging + 4 * p.n_records)[r] = make_double4(a[4], a[5], a[6], a[7]);
 }
 
-// Point pass over one chunk (a7 fused with a4/a5 on the point side): the chunk's cameras (both anchors) are
-// staged in shared memory once; each round, one observation per thread computes its contributions
-// (w lam^2, w lam R e) at both anchors into a shared stage; then each point's owner thread adds its
-// observations' entries in ascending order.  No atomics; sums are deterministic.
-template <int LOSS>
-__global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_pass(IterParams p) {
-  extern __shared__ double smem[];
-  const PtChunk ch = p.pchunks[blockIdx.x];
-  const int T = p.pt_table_cams;
-  double* scam = smem;                             // [2][T][kPtCamStride]
-  double* spt = scam + 2 * T * kPtCamStride;       // [kPtPassThreads][8]: x-bar, x^k
-  double* stage = spt + 8 * kPtPassThreads;        // [8][kPtPassThreads]
-  if (ch.large) {
-    pt_pass_large<LOSS>(p, ch, stage);
-    return;
-  }
-  const double gamma = p.sched[3];
-  const double* cb = p.cbar;
-  const double* ck = p.cams[p.roles[1]];
-  for (int idx = threadIdx.x; idx < ch.ncam * 32; idx += kPtPassThreads) {
-    const int slot = idx >> 5, a = (idx >> 4) & 1, k = idx & 15;
-    if (k < 15) {
-      const int32_t cam = p.pchunk_cams[ch.c0 + slot];
-      scam[(a * T + slot) * kPtCamStride + k] = (a ? ck : cb)[(size_t)cam * kCamStride + k];
+// Point solve (a7): each owned point adds its observations' staged contributions in ascending (camera) order
+// and takes the exact minimiser for both anchors; deterministic, no atomics.
+__global__ void __launch_bounds__(kPtPassThreads) k_pt_sum(IterParams p) {
+  const int j = blockIdx.x * kPtPassThreads + threadIdx.x;
+  double qv[kPtCols] = {0, 0, 0, 0};
+  if (j < p.n_own_pts) {
+    const double4 k4 = p.pts[p.roles[1]][j], b4 = p.lbar[p.roles[4]][j];
+    const double lk[3] = {k4.x, k4.y, k4.z};
+    const double lb[3] = {b4.x, b4.y, b4.z};
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const double2* ra = reinterpret_cast<const double2*>(p.staging);
+    const double2* rm = reinterpret_cast<const double2*>(p.staging + 4 * p.n_records);
+    const int64_t o0 = p.p_ptr[j], o1 = p.p_ptr[j + 1];
+    int64_t o = o0;
+    for (; o + 2 <= o1; o += 2) {  // two records in flight per thread
+      const int64_t r0 = p.p_src[o], r1 = p.p_src[o + 1];
+      const double2 a0 = __ldcg(ra + 2 * r0), b0 = __ldcg(ra + 2 * r0 + 1), c0 = __ldcg(rm + 2 * r0),
+                    d0 = __ldcg(rm + 2 * r0 + 1);
+      const double2 a1 = __ldcg(ra + 2 * r1), b1 = __ldcg(ra + 2 * r1 + 1), c1 = __ldcg(rm + 2 * r1),
+                    d1 = __ldcg(rm + 2 * r1 + 1);
+      acc[0] += a0.x; acc[1] += a0.y; acc[2] += b0.x; acc[3] += b0.y;
+      acc[4] += c0.x; acc[5] += c0.y; acc[6] += d0.x; acc[7] += d0.y;
+      acc[0] += a1.x; acc[1] += a1.y; acc[2] += b1.x; acc[3] += b1.y;
+      acc[4] += c1.x; acc[5] += c1.y; acc[6] += d1.x; acc[7] += d1.y;
     }
+    if (o < o1) {
+      const int64_t r0 = p.p_src[o];
+      const double2 a0 = __ldcg(ra + 2 * r0), b0 = __ldcg(ra + 2 * r0 + 1), c0 = __ldcg(rm + 2 * r0),
+                    d0 = __ldcg(rm + 2 * r0 + 1);
+      acc[0] += a0.x; acc[1] += a0.y; acc[2] += b0.x; acc[3] += b0.y;
+      acc[4] += c0.x; acc[5] += c0.y; acc[6] += d0.x; acc[7] += d0.y;
+    }
+    pt_finish(p, j, lb, lk, acc, qv);
   }
-  const int q = threadIdx.x;
-  const bool own = q < ch.npts;
-  double lb[3] = {0, 0, 0}, lk[3] = {0, 0, 0};
-  int64_t pb = 0, pe = 0;
-  if (own) {
-    const int j = ch.p0 + q;
-    const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
-    lk[0] = k4.x;
-    lk[1] = k4.y;
-    lk[2] = k4.z;
-    lb[0] = fma(gamma, k4.x - p4.x, k4.x);  // eq. nesterov_l
-    lb[1] = fma(gamma, k4.y - p4.y, k4.y);
-    lb[2] = fma(gamma, k4.z - p4.z, k4.z);
-    double* P = spt + 8 * q;
-    P[0] = lb[0];
-    P[1] = lb[1];
-    P[2] = lb[2];
-    P[3] = lk[0];
-    P[4] = lk[1];
-    P[5] = lk[2];
-    pb = p.p_ptr[j] - ch.o0;
-    pe = p.p_ptr[j + 1] - ch.o0;
+  // block sums: warp shuffles, then one shared-memory step (deterministic order)
+  __shared__ double ws[kPtPassThreads / 32][kPtCols];
+#pragma unroll
+  for (int c = 0; c < kPtCols; ++c) {
+    double v = qv[c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5][c] = v;
   }
   __syncthreads();
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r0 = 0; r0 < ch.nobs; r0 += kPtPassThreads) {
-    const int o = r0 + threadIdx.x;
-    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (o < ch.nobs) {
-      const uint32_t sp = p.p_sp[ch.o0 + o];
-      const int slot = sp & 255, lp = sp >> 8;
-      const double2 u = p.p_uv[ch.o0 + o];
-      const double* P = spt + 8 * lp;
-      pt_terms<LOSS>(scam + slot * kPtCamStride, P[0], P[1], P[2], u, p, c[0], c[1], c[2], c[3]);
-      pt_terms<LOSS>(scam + (T + slot) * kPtCamStride, P[3], P[4], P[5], u, p, c[4], c[5], c[6], c[7]);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) stage[k * kPtPassThreads + threadIdx.x] = c[k];
-    __syncthreads();
-    if (own) {
-      const int64_t a0 = pb > r0 ? pb : r0, a1 = pe < r0 + kPtPassThreads ? pe : r0 + kPtPassThreads;
-      for (int64_t pos = a0; pos < a1; ++pos)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += stage[k * kPtPassThreads + (pos - r0)];
-    }
-    __syncthreads();
+  if (threadIdx.x < kPtCols) {
+    double v = 0;
+    for (int w = 0; w < kPtPassThreads / 32; ++w) v += ws[w][threadIdx.x];
+    p.pt_part[(size_t)blockIdx.x * kPtCols + threadIdx.x] = v;
   }
-  double qv[kPtCols] = {0, 0, 0, 0};
-  if (own) pt_finish(p, ch.p0 + q, lb, lk, acc, qv);
-  pt_block_store(qv, stage, p.pt_part + (size_t)blockIdx.x * kPtCols);
 }
 
 // ------------------------------------------------------------------ a6: camera solve
@@ -759,12 +766,16 @@ __global__ void __launch_bounds__(128) k_cam_eval(IterParams p) {
   if (threadIdx.x < kCamEvalCols) p.cam_part[(size_t)blockIdx.x * kCamEvalCols + threadIdx.x] = sq[threadIdx.x][0];
 }
 
-// ------------------------------------------------------------------ a9: rank-local sums
-__global__ void __launch_bounds__(256) k_reduce_local(IterParams p) {
+// ------------------------------------------------------------------ a9: rank-local sums (two stages)
+// Stage 1: kReduceBlocks CTAs, CTA b sums a contiguous, fixed range of the partials (deterministic).
+__global__ void __launch_bounds__(256) k_reduce_partial(IterParams p) {
   __shared__ double s[kGlobalCols][256];
   double v[kGlobalCols];
   for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
-  for (int b = threadIdx.x; b < p.n_cam_eval_blocks; b += 256) {
+  const int nb = gridDim.x;
+  const int64_t c0 = (int64_t)p.n_cam_eval_blocks * blockIdx.x / nb, c1 = (int64_t)p.n_cam_eval_blocks * (blockIdx.x + 1) / nb;
+  const int64_t q0 = (int64_t)p.n_pt_blocks * blockIdx.x / nb, q1 = (int64_t)p.n_pt_blocks * (blockIdx.x + 1) / nb;
+  for (int64_t b = c0 + threadIdx.x; b < c1; b += 256) {
     const double* q = p.cam_part + (size_t)b * kCamEvalCols;
     v[0] += q[0];
     v[1] += q[1];
@@ -775,13 +786,30 @@ __global__ void __launch_bounds__(256) k_reduce_local(IterParams p) {
     v[8] += q[6];
     v[9] += q[7];
   }
-  for (int b = threadIdx.x; b < p.n_pt_blocks; b += 256) {
+  for (int64_t b = q0 + threadIdx.x; b < q1; b += 256) {
     const double* q = p.pt_part + (size_t)b * kPtCols;
     v[2] += q[0];
     v[4] += q[1];
     v[5] += q[2];
     v[6] += q[3];
   }
+  for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < kGlobalCols) p.red_part[(size_t)blockIdx.x * kGlobalCols + threadIdx.x] = s[threadIdx.x][0];
+}
+
+// Stage 2: one CTA over the stage-1 partials.
+__global__ void __launch_bounds__(256) k_reduce_local(IterParams p) {
+  __shared__ double s[kGlobalCols][256];
+  double v[kGlobalCols];
+  for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
+  if (threadIdx.x < kReduceBlocks)
+    for (int c = 0; c < kGlobalCols; ++c) v[c] = p.red_part[(size_t)threadIdx.x * kGlobalCols + c];
   for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
   __syncthreads();
   for (int st = 128; st > 0; st >>= 1) {
@@ -820,9 +848,20 @@ __global__ void k_select(IterParams p) {
   p.roles[1] = restart ? r3 : r2;  // x^{k+1} = x_mm (restart, Alg. 1) or x_acc (L414)
   p.roles[2] = r0;
   p.roles[3] = restart ? r2 : r3;
+  p.roles[4] = restart ? 1 : 0;    // x-bar^{k+1} computed from the selected candidate
   p.sched[0] = s_next;
   p.sched[1] = Fbar;
   p.sched[2] = (double)(k + 1);
+}
+
+// x-bar^k of every local point from x^k, x^{k-1} (create / set_state); writes lbar[roles[4]]
+__global__ void k_lbar_all(IterParams p) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p.n_pts) return;
+  const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
+  const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
+  p.lbar[p.roles[4]][j] = make_double4(fma(gamma, k4.x - p4.x, k4.x), fma(gamma, k4.y - p4.y, k4.y),
+                                       fma(gamma, k4.z - p4.z, k4.z), 0.0);
 }
 
 // ------------------------------------------------------------------ halo pack / unpack (x^k)
@@ -860,43 +899,54 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, int32_t n_cam, co
 static inline int blocks(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 int launch_extrapolate(const IterParams& p, cudaStream_t st) {
-  k_extrapolate<<<blocks(p.n_cams > 0 ? p.n_cams : 1, 128), 128, 0, st>>>(p);
+  const int64_t n = p.n_cams > p.n_pts - p.n_own_pts ? p.n_cams : p.n_pts - p.n_own_pts;
+  k_extrapolate<<<blocks(n > 0 ? n : 1, 128), 128, 0, st>>>(p);
   return 1;
+}
+
+int launch_lbar_all(const IterParams& p, cudaStream_t st) {
+  if (p.n_pts == 0) return 0;
+  k_lbar_all<<<blocks(p.n_pts, 256), 256, 0, st>>>(p);
+  return 1;
+}
+
+template <int LOSS>
+static void cam_launch(const IterParams& p, cudaStream_t st) {
+  constexpr size_t sm = sizeof(double) * kCamSmemDoubles;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_cam_pass<LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  k_cam_pass<LOSS><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
 }
 
 int launch_cam_pass(const IterParams& p, cudaStream_t st) {
   if (p.n_chunks == 0) return 0;
   switch (p.loss) {
-    case kHuber: k_cam_pass<kHuber><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
-    case kCauchy: k_cam_pass<kCauchy><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
-    default: k_cam_pass<kTrivial><<<2 * p.n_chunks, kCamPassThreads, 0, st>>>(p); break;
+    case kHuber: cam_launch<kHuber>(p, st); break;
+    case kCauchy: cam_launch<kCauchy>(p, st); break;
+    default: cam_launch<kTrivial>(p, st); break;
   }
   return 1;
-}
-
-size_t pt_pass_smem(const IterParams& p) {
-  return sizeof(double) * ((size_t)2 * p.pt_table_cams * kPtCamStride + 16 * kPtPassThreads);
-}
-
-template <int LOSS>
-static void pt_launch(const IterParams& p, cudaStream_t st) {
-  const size_t sm = pt_pass_smem(p);
-  static size_t configured = 0;
-  if (sm > configured) {
-    cudaFuncSetAttribute(k_pt_pass<LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = sm;
-  }
-  k_pt_pass<LOSS><<<p.n_pt_blocks, kPtPassThreads, sm, st>>>(p);
 }
 
 int launch_pt_pass(const IterParams& p, cudaStream_t st) {
-  if (p.n_pt_blocks == 0) return 0;
-  switch (p.loss) {
-    case kHuber: pt_launch<kHuber>(p, st); break;
-    case kCauchy: pt_launch<kCauchy>(p, st); break;
-    default: pt_launch<kTrivial>(p, st); break;
+  int n = 0;
+  if (p.n_boundary > 0) {
+    const int nb = blocks(p.n_boundary, 256);
+    switch (p.loss) {
+      case kHuber: k_pt_boundary<kHuber><<<nb, 256, 0, st>>>(p); break;
+      case kCauchy: k_pt_boundary<kCauchy><<<nb, 256, 0, st>>>(p); break;
+      default: k_pt_boundary<kTrivial><<<nb, 256, 0, st>>>(p); break;
+    }
+    ++n;
   }
-  return 1;
+  if (p.n_pt_blocks > 0) {
+    k_pt_sum<<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p);
+    ++n;
+  }
+  return n;
 }
 
 int launch_cam_solve(const IterParams& p, cudaStream_t st) {
@@ -912,8 +962,9 @@ int launch_cam_eval(const IterParams& p, cudaStream_t st) {
 }
 
 int launch_reduce_local(const IterParams& p, cudaStream_t st) {
+  k_reduce_partial<<<kReduceBlocks, 256, 0, st>>>(p);
   k_reduce_local<<<1, 256, 0, st>>>(p);
-  return 1;
+  return 2;
 }
 
 int launch_select(const IterParams& p, cudaStream_t st) {

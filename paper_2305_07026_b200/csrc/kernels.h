@@ -12,22 +12,12 @@ constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camer
 constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
 constexpr int kCamPassThreads = 128;
 constexpr int kCamChunkObs = 128 * 16;  // observations per camera-pass chunk (one CTA)
-constexpr int kPtPassThreads = 256;     // point pass: threads per CTA = max points per chunk
-constexpr int kPtMaxCams = 256;         // camera-table slots per point chunk (uint8 slot ids)
-constexpr int kPtChunkObs = 4096;       // observations per point chunk (larger single points: "large" chunks)
-constexpr int kPtCamStride = 17;        // doubles per camera in the shared-memory table (bank spread)
+constexpr int kPtPassThreads = 256;     // point solve: threads (points) per CTA
 constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
 constexpr int kGlobalCols = 10;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kTraceCols = 10;    // = DABA_TRACE_COLS
-
-// A point chunk: consecutive owned points [p0, p0 + npts) whose observations [o0, o0 + nobs) (point side) read at
-// most kPtMaxCams distinct cameras, listed at chunk_cams[c0 .. c0 + ncam).  large = 1: a single point with more
-// observations / cameras than a chunk holds (its cameras are read from global memory).
-struct PtChunk {
-  int64_t o0;
-  int32_t nobs, p0, npts, c0, ncam, large;
-};
+constexpr int kReduceBlocks = 128; // stage-1 CTAs of the rank-local reduction
 
 struct CamChunk {
   int32_t cam;    // local camera index (owned)
@@ -51,22 +41,28 @@ struct IterParams {
   // state
   double* cams[4];       // n_cams x 16
   double4* pts[4];       // n_pts
+  double4* lbar[2];      // x-bar^k of the points: roles[4] selects the valid buffer
   double* cbar;          // extrapolated cameras x-bar^k, n_cams x 16
-  int32_t* roles;        // [4]
-  double* sched;         // [0] s^{(k)}, [1] F-bar^{(k-1)}, [2] iteration counter k (as double), [3] gamma^{(k)}
+  int32_t* roles;        // [5]: x^{k-1}, x^k, acc, mm buffers; valid x-bar point buffer
+  double* sched;         // [0] s^{(k)}, [1] F-bar^{(k-1)}, [2] iteration counter k (as double), [3] gamma^{(k)},
+                         // [4] gamma^{(k+1)}
   // camera-side observations (sorted by camera, then point)
   const CamChunk* chunks;
   const int32_t* cam_chunk_ptr;  // n_own_cams + 1
   const double2* c_uv;
   const int32_t* c_pt;
-  // point-side observations (sorted by point, then camera)
+  // point side: the camera pass writes, per camera-side observation o, the record (w lam^2, w lam R e) at
+  // staging[o] (x-bar anchor) and staging[n_records + o] (x^k anchor), 4 doubles each; boundary observations
+  // get records n_cam_side + b.  p_src lists each owned point's records in (point, camera) order.
   const int64_t* p_ptr;          // n_own_pts + 1
-  const double2* p_uv;
-  const int32_t* p_cam;          // local camera of each point-side observation
-  const uint16_t* p_sp;          // (camera slot in the chunk table) | (point index in the chunk) << 8
-  const PtChunk* pchunks;
-  const int32_t* pchunk_cams;
-  int32_t pt_table_cams;         // max ncam over chunks (shared-memory table size)
+  const int32_t* p_src;          // record of each point-side observation
+  double* staging;               // 2 x n_records x 4
+  int64_t n_cam_side, n_records;
+  // boundary observations (point owned here, camera owned elsewhere): recomputed from halo cameras
+  int64_t n_boundary;
+  const int32_t* b_cam;
+  const int32_t* b_pt;
+  const double2* b_uv;
   // scratch
   double* partial;        // n_chunks * 2 * kPartialStride
   double* moments;        // n_own_cams * 2 * kNumMoments (summed per camera)
@@ -75,6 +71,7 @@ struct IterParams {
   double* cam_part;       // camera-eval blocks x kCamEvalCols
   double* pt_part;        // point-pass blocks x kPtCols
   int32_t n_cam_eval_blocks, n_pt_blocks;
+  double* red_part;       // kReduceBlocks x kGlobalCols
   double* local;          // kGlobalCols (this rank's sums)
   double* global;         // kGlobalCols (allreduced)
   double* trace;          // trace ring, trace_cap x kTraceCols
@@ -83,6 +80,7 @@ struct IterParams {
 
 // Launchers (all asynchronous on `st`).  They return the number of kernels launched.
 int launch_extrapolate(const IterParams& p, cudaStream_t st);
+int launch_lbar_all(const IterParams& p, cudaStream_t st);
 int launch_cam_pass(const IterParams& p, cudaStream_t st);
 int launch_pt_pass(const IterParams& p, cudaStream_t st);
 int launch_cam_solve(const IterParams& p, cudaStream_t st);

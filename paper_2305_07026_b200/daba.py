@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdaba.so")
+LIB_PATH = os.environ.get("DABA_LIB", os.path.join(_HERE, "libdaba.so"))
 _lib = None
 
 LOSS_TRIVIAL, LOSS_HUBER, LOSS_CAUCHY = 0, 1, 2
@@ -40,7 +40,8 @@ class Options(ctypes.Structure):
 EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate", "daba_iterate_trace",
            "daba_objective", "daba_get_state", "daba_get_state_native", "daba_set_state_native",
            "daba_get_schedule", "daba_last_decisions", "daba_shard_info", "daba_stream", "daba_kernel_times",
-           "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy"]
+           "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
+           "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy"]
 
 
 def lib():
@@ -75,6 +76,14 @@ def lib():
         L.daba_last_error.restype = ctypes.c_char_p
         L.daba_destroy.argtypes = [V]
         L.daba_destroy.restype = None
+        L.daba_plan_create.argtypes = [I64, I64, V, V, I64, V, V, I32, I32]
+        L.daba_plan_create.restype = V
+        L.daba_plan_counts.argtypes = [V, V]
+        L.daba_plan_array.argtypes = [V, I32, V]
+        L.daba_plan_peer_list.argtypes = [V, I32, I32, V]
+        L.daba_plan_peer_list.restype = I64
+        L.daba_plan_destroy.argtypes = [V]
+        L.daba_plan_destroy.restype = None
         _lib = L
     return _lib
 
@@ -99,6 +108,43 @@ def comm_id() -> bytes:
 
 def _c(x, dtype):
     return np.ascontiguousarray(x, dtype=dtype)
+
+
+class Plan:
+    """Host-only shard plan of one rank (the partition daba_create uses); no GPU needed."""
+
+    def __init__(self, M, N, obs_cam, obs_pt, rank=0, nranks=1, cam_owner=None, pt_owner=None):
+        oc, op = _c(obs_cam, np.int32), _c(obs_pt, np.int32)
+        co = _c(cam_owner, np.int32) if cam_owner is not None else None
+        po = _c(pt_owner, np.int32) if pt_owner is not None else None
+        self.M, self.N = M, N
+        self.h = lib().daba_plan_create(M, N, oc.ctypes.data, op.ctypes.data, oc.size,
+                                        co.ctypes.data if co is not None else None,
+                                        po.ctypes.data if po is not None else None, rank, nranks)
+        if not self.h:
+            raise DabaError(-1, "daba_plan_create")
+        c = np.zeros(10, np.int64)
+        lib().daba_plan_counts(self.h, c.ctypes.data)
+        self.counts = dict(zip(["own_cams", "own_pts", "halo_cams", "halo_pts", "cam_side_obs", "pt_side_obs",
+                                "send_doubles", "recv_doubles", "peers"], (int(v) for v in c[:9])))
+
+    def array(self, which):
+        n = {0: self.counts["own_cams"] + self.counts["halo_cams"], 1: self.counts["own_pts"] + self.counts["halo_pts"],
+             2: self.M, 3: self.N, 4: self.counts["peers"]}[which]
+        out = np.zeros(n, np.int32)
+        lib().daba_plan_array(self.h, which, out.ctypes.data)
+        return out
+
+    def peer_list(self, peer, kind):
+        n = lib().daba_plan_peer_list(self.h, peer, kind, None)
+        out = np.zeros(max(n, 0), np.int32)
+        lib().daba_plan_peer_list(self.h, peer, kind, out.ctypes.data)
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().daba_plan_destroy(self.h)
+            self.h = None
 
 
 class Solver:
