@@ -86,7 +86,8 @@ typedef struct daba_ctx daba_ctx; /* opaque; owned by the library until daba_des
  *   cam_owner M ranks, or NULL: contiguous camera ranges balanced by observation count;
  *   pt_owner  N ranks, or NULL: the rank owning most of the point's observations, ties -> lowest rank;
  *   comm_id   128 bytes: an ncclUniqueId from daba_comm_id (DABA_COMM_NCCL) or any 128-byte key shared by the
- *             ranks of one DABA_COMM_LOCAL group; may be NULL iff nranks == 1;
+ *             ranks of one DABA_COMM_LOCAL group; may be NULL iff nranks == 1 (a single rank given an id still
+ *             routes its sums through the communicator);
  *   opt       options or NULL for defaults.
  * Every rank passes the same global arrays; each keeps its shard (owned cameras/points and the observations
  * touching them) plus the boundary (halo) states it reads.  Collective when nranks > 1: all ranks must call it.

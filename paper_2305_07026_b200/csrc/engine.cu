@@ -225,7 +225,7 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
   n += timed(c, "k_cam_eval", [&] { return launch_cam_eval(P, c->stream); });
   n += timed(c, "k_reduce_local", [&] { return launch_reduce_local(P, c->stream); });
-  if (c->nranks > 1) {
+  if (c->comm) {
     std::string e = c->comm->allreduce(P.local, P.global, kGlobalCols, c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
   }
@@ -239,12 +239,12 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
 
 int compute_objective(daba_ctx* c, double* F, double* ndeg) {
   launch_objective(c->P, c->stream);
-  if (c->nranks > 1) {
+  if (c->comm) {
     std::string e = c->comm->allreduce(c->P.local, c->P.global, kGlobalCols, c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
   }
   double g[kGlobalCols];
-  CUDA_OR(c, cudaMemcpyAsync(g, c->nranks > 1 ? c->P.global : c->P.local, sizeof g, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR(c, cudaMemcpyAsync(g, c->comm ? c->P.global : c->P.local, sizeof g, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR(c, cudaStreamSynchronize(c->stream));
   *F = g[0];
   if (ndeg) *ndeg = g[7];
@@ -357,7 +357,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking) != cudaSuccess) return DABA_E_CUDA;
     C->own_stream = true;
   }
-  if (nranks > 1) {
+  if (nranks > 1 || comm_id) {  // a single rank with a comm id still routes its sums through the communicator
     std::string ce;
     C->comm.reset(make_comm(o.comm, comm_id, rank, nranks, &ce));
     if (!C->comm) {
@@ -481,7 +481,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   if ((rc = dalloc(C, &P.global, kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return bail(rc);
   if ((rc = dalloc(C, &P.sched, 8))) return bail(rc);
-  if (nranks == 1) P.global = P.local;
+  if (!C->comm) P.global = P.local;
   cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
   // halo plan
   if (nranks > 1) {
@@ -541,7 +541,7 @@ static int iterate_impl(daba_ctx* c, int n, double* trace_rows) {
   if (!c) return DABA_E_INVALID_ARG;
   if (n < 0) return fail(c, DABA_E_INVALID_ARG, "n_iters < 0");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, DABA_E_CUDA, "cudaSetDevice");
-  const bool graphable = c->opt.use_graph && !c->opt.profile && (c->nranks == 1 || c->comm->capturable());
+  const bool graphable = c->opt.use_graph && !c->opt.profile && (!c->comm || c->comm->capturable());
   int done = 0;
   while (done < n) {
     const int batch = std::min(n - done, c->P.trace_cap);

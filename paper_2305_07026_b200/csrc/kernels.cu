@@ -251,16 +251,27 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   };
 #pragma unroll
   for (int k = 0; k < kRing - 1; ++k) issue(k);
-  double4 lnext = make_double4(0, 0, 0, 0);
-  if (n > 0) lnext = ld256(L + sidx[tid]);
+#ifndef DABA_PF
+#define DABA_PF 1
+#endif
+  constexpr int PF = DABA_PF;  // gathers in flight per thread (register ring, statically indexed)
+  double4 lbuf[PF];
+#pragma unroll
+  for (int r = 0; r < PF; ++r) lbuf[r] = r < n ? ld256(L + sidx[tid + r * kCamPassThreads]) : make_double4(0, 0, 0, 0);
 #pragma unroll 1
-  for (int k = 0; k < n; ++k) {
-    const double4 l = lnext;
-    if (k + 1 < n) lnext = ld256(L + sidx[tid + (k + 1) * kCamPassThreads]);
-    issue(k + kRing - 1);
-    cp_async_wait<kRing - 1>();
-    const double2 u = *uslot(k);
-    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+  for (int k0 = 0; k0 < n; k0 += PF) {
+#pragma unroll
+    for (int r = 0; r < PF; ++r) {
+      const int k = k0 + r;
+      if (k < n) {
+        const double4 l = lbuf[r];
+        if (k + PF < n) lbuf[r] = ld256(L + sidx[tid + (k + PF) * kCamPassThreads]);
+        issue(k + kRing - 1);
+        cp_async_wait<kRing - 1>();
+        const double2 u = *uslot(k);
+        cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+      }
+    }
   }
   cp_async_wait<0>();
 }
@@ -457,27 +468,26 @@ __global__ void __launch_bounds__(kPtPassThreads) k_pt_sum(IterParams p) {
     const double lk[3] = {k4.x, k4.y, k4.z};
     const double lb[3] = {b4.x, b4.y, b4.z};
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const double2* ra = reinterpret_cast<const double2*>(p.staging);
-    const double2* rm = reinterpret_cast<const double2*>(p.staging + 4 * p.n_records);
-    const int64_t o0 = p.p_ptr[j], o1 = p.p_ptr[j + 1];
-    int64_t o = o0;
-    for (; o + 2 <= o1; o += 2) {  // two records in flight per thread
-      const int64_t r0 = p.p_src[o], r1 = p.p_src[o + 1];
-      const double2 a0 = __ldcg(ra + 2 * r0), b0 = __ldcg(ra + 2 * r0 + 1), c0 = __ldcg(rm + 2 * r0),
-                    d0 = __ldcg(rm + 2 * r0 + 1);
-      const double2 a1 = __ldcg(ra + 2 * r1), b1 = __ldcg(ra + 2 * r1 + 1), c1 = __ldcg(rm + 2 * r1),
-                    d1 = __ldcg(rm + 2 * r1 + 1);
-      acc[0] += a0.x; acc[1] += a0.y; acc[2] += b0.x; acc[3] += b0.y;
-      acc[4] += c0.x; acc[5] += c0.y; acc[6] += d0.x; acc[7] += d0.y;
-      acc[0] += a1.x; acc[1] += a1.y; acc[2] += b1.x; acc[3] += b1.y;
-      acc[4] += c1.x; acc[5] += c1.y; acc[6] += d1.x; acc[7] += d1.y;
-    }
-    if (o < o1) {
-      const int64_t r0 = p.p_src[o];
-      const double2 a0 = __ldcg(ra + 2 * r0), b0 = __ldcg(ra + 2 * r0 + 1), c0 = __ldcg(rm + 2 * r0),
-                    d0 = __ldcg(rm + 2 * r0 + 1);
-      acc[0] += a0.x; acc[1] += a0.y; acc[2] += b0.x; acc[3] += b0.y;
-      acc[4] += c0.x; acc[5] += c0.y; acc[6] += d0.x; acc[7] += d0.y;
+    const double4* ra = reinterpret_cast<const double4*>(p.staging);
+    const double4* rm = reinterpret_cast<const double4*>(p.staging + 4 * p.n_records);
+    const int64_t o1 = p.p_ptr[j + 1];
+    for (int64_t o = p.p_ptr[j]; o < o1; o += 4) {  // up to 4 records (8 x 32 B) in flight per thread
+      int32_t r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? p.p_src[o + i] : -1;
+      double4 A[4], B[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r[i] >= 0) {
+          A[i] = ld256(ra + r[i]);
+          B[i] = ld256(rm + r[i]);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r[i] >= 0) {  // ascending observation order within the point
+          acc[0] += A[i].x; acc[1] += A[i].y; acc[2] += A[i].z; acc[3] += A[i].w;
+          acc[4] += B[i].x; acc[5] += B[i].y; acc[6] += B[i].z; acc[7] += B[i].w;
+        }
     }
     pt_finish(p, j, lb, lk, acc, qv);
   }

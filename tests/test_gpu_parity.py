@@ -277,3 +277,16 @@ def test_full_size_sampled(name):
     cexp, pexp = (cm, pm) if restart else (ca, pa)
     errs = state_errors(c1[cam_ids], l1[pt_ids], cexp, pexp)
     assert max(errs) < 1e-11, errs
+
+
+# ---------------------------------------------------------------- NCCL transport (one rank on one GPU)
+def test_nccl_transport_single_rank():
+    """The NCCL code path (dlopen, ncclCommInitRank, ncclAllReduce captured in the iteration graph) with one
+    rank: identical iterates to the communicator-free context."""
+    p = gen.generate("small_huber")
+    key = D.comm_id()
+    with solver(p) as a, solver(p, nranks=1, rank=0, comm_key=key, comm=D.COMM_NCCL) as b:
+        ta, tb = a.iterate_trace(12), b.iterate_trace(12)
+        np.testing.assert_array_equal(ta, tb)
+        assert a.objective() == b.objective()
+        np.testing.assert_array_equal(a.state_native(0)[0], b.state_native(0)[0])
