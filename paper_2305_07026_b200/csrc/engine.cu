@@ -11,6 +11,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <atomic>
+#include <thread>
 #include <vector>
 
 #include "../../include/daba.h"
@@ -54,6 +56,19 @@ struct daba_ctx {
 };
 
 namespace {
+
+// Split [0, n) over the host's cores (create-time setup loops only; the iteration itself never runs here).
+template <class F>
+void parallel_for(int64_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < (1 << 16) || hw == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < hw; ++t) th.emplace_back([&, t] { f(n * t / hw, n * (t + 1) / hw); });
+  for (auto& x : th) x.join();
+}
 
 int fail(daba_ctx* c, int code, const std::string& m) {
   if (c) c->err = m;
@@ -343,12 +358,16 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     bal_to_native(cameras + 9 * i, tmp);
     std::memcpy(&nat[(size_t)i * 15], tmp, 15 * sizeof(double));
   }
-  for (int64_t k = 0; k < K; ++k) {
-    const double* t = &nat[(size_t)obs_cam[k] * 15 + 9];
-    const double* l = points + 3 * (int64_t)obs_pt[k];
-    const double dx = l[0] - t[0], dy = l[1] - t[1], dz = l[2] - t[2];
-    if (!(dx * dx + dy * dy + dz * dz > o.eps * o.eps)) return DABA_E_DEGENERATE;
-  }
+  std::atomic<bool> degenerate(false);
+  parallel_for(K, [&](int64_t k0, int64_t k1) {
+    for (int64_t k = k0; k < k1; ++k) {
+      const double* t = &nat[(size_t)obs_cam[k] * 15 + 9];
+      const double* l = points + 3 * (int64_t)obs_pt[k];
+      const double dx = l[0] - t[0], dy = l[1] - t[1], dz = l[2] - t[2];
+      if (!(dx * dx + dy * dy + dz * dz > o.eps * o.eps)) degenerate = true;
+    }
+  });
+  if (degenerate) return DABA_E_DEGENERATE;
   // device and stream
   if (cudaSetDevice(cuda_device) != cudaSuccess) return DABA_E_CUDA;
   if (o.stream) {
@@ -403,7 +422,9 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   {
     const size_t kc = S.c_obs.size();
     std::vector<double2> uv(kc);
-    for (size_t q = 0; q < kc; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
+    parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
+    });
     const double2* duv;
     if ((rc = upload(C, const_cast<double2**>(&duv), uv))) return bail(rc);
     P.c_uv = duv;
@@ -438,15 +459,16 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
     P.p_ptr = dptr;
     std::vector<int32_t> cam_side_of((size_t)K, -1);
-    for (size_t q = 0; q < kc; ++q) cam_side_of[(size_t)S.c_obs[q]] = (int32_t)q;
+    parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) cam_side_of[(size_t)S.c_obs[q]] = (int32_t)q;
+    });
     std::vector<int32_t> src(kp), bcam, bpt;
     std::vector<double2> buv;
+    parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) src[q] = cam_side_of[(size_t)S.p_obs[q]];
+    });
     for (size_t q = 0; q < kp; ++q) {
-      const int32_t r = cam_side_of[(size_t)S.p_obs[q]];
-      if (r >= 0) {
-        src[q] = r;
-        continue;
-      }
+      if (src[q] >= 0) continue;  // written by this rank's camera pass
       src[q] = (int32_t)(kc + bcam.size());
       bcam.push_back(S.p_cam[q]);
       bpt.push_back(S.p_pt[q]);

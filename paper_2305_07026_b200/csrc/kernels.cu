@@ -102,11 +102,14 @@ struct CamRegs {
   }
 };
 #endif
+#ifndef DABA_SINGLE
+#define DABA_DUAL  // two observations per step (measured: 0.97 vs 1.02 ms on Final-13682)
+#endif
 #ifndef DABA_RING
-#define DABA_RING 4
+#define DABA_RING 8
 #endif
 #ifndef DABA_MINB
-#define DABA_MINB 4
+#define DABA_MINB 3
 #endif
 
 // One observation's contribution to the camera moments at one anchor.
@@ -251,28 +254,37 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   };
 #pragma unroll
   for (int k = 0; k < kRing - 1; ++k) issue(k);
-#ifndef DABA_PF
-#define DABA_PF 1
-#endif
-  constexpr int PF = DABA_PF;  // gathers in flight per thread (register ring, statically indexed)
-  double4 lbuf[PF];
-#pragma unroll
-  for (int r = 0; r < PF; ++r) lbuf[r] = r < n ? ld256(L + sidx[tid + r * kCamPassThreads]) : make_double4(0, 0, 0, 0);
+#ifdef DABA_DUAL
+  // two observations per step: two independent dependency chains feed the same accumulators
+  double4 la = n > 0 ? ld256(L + sidx[tid]) : make_double4(0, 0, 0, 0);
+  double4 lb = n > 1 ? ld256(L + sidx[tid + kCamPassThreads]) : make_double4(0, 0, 0, 0);
+  issue(kRing - 1);
 #pragma unroll 1
-  for (int k0 = 0; k0 < n; k0 += PF) {
-#pragma unroll
-    for (int r = 0; r < PF; ++r) {
-      const int k = k0 + r;
-      if (k < n) {
-        const double4 l = lbuf[r];
-        if (k + PF < n) lbuf[r] = ld256(L + sidx[tid + (k + PF) * kCamPassThreads]);
-        issue(k + kRing - 1);
-        cp_async_wait<kRing - 1>();
-        const double2 u = *uslot(k);
-        cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
-      }
-    }
+  for (int k = 0; k < n; k += 2) {
+    const double4 l0 = la, l1 = lb;
+    if (k + 2 < n) la = ld256(L + sidx[tid + (k + 2) * kCamPassThreads]);
+    if (k + 3 < n) lb = ld256(L + sidx[tid + (k + 3) * kCamPassThreads]);
+    cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
+    const double2 u0 = *uslot(k);
+    const double2 u1 = *uslot(k + 1);
+    issue(k + kRing);  // refills the two slots just read
+    issue(k + kRing + 1);
+    cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+    if (k + 1 < n) cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, ch.o0 + tid + (int64_t)(k + 1) * kCamPassThreads);
   }
+#else
+  double4 lnext = make_double4(0, 0, 0, 0);
+  if (n > 0) lnext = ld256(L + sidx[tid]);
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const double4 l = lnext;
+    if (k + 1 < n) lnext = ld256(L + sidx[tid + (k + 1) * kCamPassThreads]);
+    issue(k + kRing - 1);
+    cp_async_wait<kRing - 1>();
+    const double2 u = *uslot(k);
+    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+  }
+#endif
   cp_async_wait<0>();
 }
 

@@ -30,11 +30,11 @@ struct ShardPlan {
   int32_t n_own_cams = 0, n_own_pts = 0;
   // camera side (sorted by camera, then point): local camera, local point, global observation id
   std::vector<int32_t> c_cam, c_pt;
-  std::vector<int64_t> c_obs;
+  std::vector<int32_t> c_obs;
   std::vector<int64_t> cam_ptr;                 // n_own_cams + 1 offsets into the camera side
   // point side (sorted by point, then camera)
   std::vector<int32_t> p_cam, p_pt;
-  std::vector<int64_t> p_obs;
+  std::vector<int32_t> p_obs;
   std::vector<int64_t> pt_ptr;                  // n_own_pts + 1
   std::vector<Peer> peers;
   int64_t send_doubles = 0, recv_doubles = 0;   // per iteration
