@@ -27,14 +27,16 @@ METRIC = "observations/sec per DABA iteration"
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_FMA_PEAK = 17.06e12  # measured DFMA/s, profiles/r01_day0_micro.log (148 SMs, full chip, independent chains)
 
-# Algorithmic bytes: what the kernel must move at least once per launch.
-#   camera pass (both anchors): per observation u (16 B) + point index (4 B); per point x^k and x^{k-1} (2 x 24 B)
-#   point pass: per observation u (16 B) + camera index (4 B); per point ptr (8 B) + read x^k, x^{k-1} (48 B) +
-#               write two candidates (48 B)
+# Algorithmic bytes per launch: what each kernel must read or write at least once.
+#   k_cam_pass (both anchors): per observation u (16 B) + point index (4 B) read, the point-side record of both
+#     anchors written (2 x 32 B); per point the two anchor states read once (2 x 32 B); cameras 2 x 128 B.
+#   k_pt_pass (= k_pt_sum): per observation both records (64 B) + record index (4 B); per point read x^k and
+#     x-bar^k (64 B), write both candidates and both next x-bar (4 x 32 B), offsets (8 B).
 BYTES = {
-    "k_cam_pass": lambda K, N, M: 20 * K + 48 * N + 2 * 128 * M,
-    "k_pt_pass": lambda K, N, M: 20 * K + 104 * N + 2 * 128 * M,
+    "k_cam_pass": lambda K, N, M: 84 * K + 64 * N + 2 * 128 * M,
+    "k_pt_pass": lambda K, N, M: 68 * K + 200 * N,
 }
+TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
 def parse():
@@ -170,16 +172,21 @@ def main():
     if world > 1:
         dist.init_process_group("gloo", init_method="env://")
     p = gen.generate(a.config)
-    comm_key = None
-    if world > 1:
+
+    def fresh_key():
+        # every context gets its own NCCL communicator, hence its own unique id (rank 0 draws, all receive)
+        if world == 1:
+            return None
         obj = [daba.comm_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        comm_key = obj[0]
+        return obj[0]
+
     stream = torch.cuda.Stream(device=local)
-    kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, comm_key=comm_key, device=local)
+    kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, device=local)
 
     # ---------------- device-resident timed region (production path: one CUDA graph per iteration)
-    s = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, **kw)
+    s = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, comm_key=fresh_key(),
+                    **kw)
     lpi = s.launches_per_iteration()
     with torch.cuda.stream(stream):
         s.iterate(a.warmup)
@@ -205,7 +212,8 @@ def main():
     s.close()
 
     # ---------------- per-kernel times: the same steps with CUDA events around every launch (same stream)
-    sp_ = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, profile=1, **kw)
+    sp_ = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, profile=1,
+                      comm_key=fresh_key(), **kw)
     with torch.cuda.stream(stream):
         sp_.iterate(a.warmup)
         torch.cuda.synchronize()
@@ -226,11 +234,12 @@ def main():
     if not a.no_e2e:
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
         hc, hpnt, hoc, hop, huv = map(pin, (p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv))
+        key = fresh_key()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        se = daba.Solver(hc, hpnt, hoc, hop, huv, stream=stream.cuda_stream, **kw)
+        se = daba.Solver(hc, hpnt, hoc, hop, huv, stream=stream.cuda_stream, comm_key=key, **kw)
         Ftr, _ = se.iterate(a.steps, F_trace=True)
         cams_out, pts_out, _ = se.state()
         torch.cuda.synchronize()
@@ -266,13 +275,24 @@ def main():
     per_launch_ms = dms / max(dl, 1)
     kshare = {k: round(v[0] / prof_ms, 4) for k, v in kt.items()}
     roof = None
+    kbytes = {k: f(info["cam_side_obs"] if k == "k_cam_pass" else info["pt_side_obs"],
+                   info["own_pts"] + info["halo_pts"], info["own_cams"]) for k, f in BYTES.items()}
+    traffic = None
+    try:
+        traffic = json.load(open(TRAFFIC)).get(dname, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     if dname in BYTES:
-        byt = BYTES[dname](info["cam_side_obs"] if dname == "k_cam_pass" else info["pt_side_obs"],
-                           info["own_pts"] + info["halo_pts"], info["own_cams"])
+        byt = kbytes[dname]
         ach = byt / (per_launch_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": None, "kernel": dname, "bytes_per_launch": int(byt),
-                "kernel_ms_per_launch": round(per_launch_ms, 5), "peak_source": hbm_src}
+                "traffic": traffic, "kernel": dname, "bytes_per_launch": int(byt),
+                "kernel_ms_per_launch": round(per_launch_ms, 5), "peak_source": hbm_src,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None}
+        # whole iteration: algorithmic bytes of both passes over the device-timed step
+        tot_b = sum(kbytes.values())
+        roof["iteration"] = {"bytes": int(tot_b), "achieved": round(tot_b / (ms / a.steps * 1e-3) / 1e9, 1),
+                             "frac": round(tot_b / (ms / a.steps * 1e-3) / 1e9 / hbm, 4)}
     out = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3), "higher_is_better": True,

@@ -42,6 +42,7 @@ struct daba_ctx {
   double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
   // graph
   cudaGraphExec_t graph = nullptr;
+  bool graph_failed = false;
   int launches_per_iter = 0;
   // profiling
   std::vector<std::string> knames;
@@ -563,23 +564,30 @@ static int iterate_impl(daba_ctx* c, int n, double* trace_rows) {
   if (!c) return DABA_E_INVALID_ARG;
   if (n < 0) return fail(c, DABA_E_INVALID_ARG, "n_iters < 0");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, DABA_E_CUDA, "cudaSetDevice");
-  const bool graphable = c->opt.use_graph && !c->opt.profile && (!c->comm || c->comm->capturable());
+  const bool graphable =
+      c->opt.use_graph && !c->opt.profile && !c->graph_failed && (!c->comm || c->comm->capturable());
   int done = 0;
   while (done < n) {
     const int batch = std::min(n - done, c->P.trace_cap);
-    if (graphable) {
-      if (!c->graph) {
-        cudaGraph_t g;
-        CUDA_OR(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        int launches = 0;
-        int rc = enqueue_iteration(c, &launches);
-        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-        if (rc) return rc;
-        if (ce != cudaSuccess) return fail(c, DABA_E_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
-        ce = cudaGraphInstantiate(&c->graph, g, 0);
-        cudaGraphDestroy(g);
-        if (ce != cudaSuccess) return fail(c, DABA_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
+    if (graphable && !c->graph) {
+      cudaGraph_t g = nullptr;
+      CUDA_OR(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      int launches = 0;
+      const int rc = enqueue_iteration(c, &launches);
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (rc == DABA_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&c->graph, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (rc != DABA_OK || ce != cudaSuccess || !c->graph) {
+        // Capture is an optimisation: on failure (e.g. a transport that cannot be captured) launch the same
+        // kernels eagerly from now on.  Nothing was executed during the failed capture.
+        cudaGetLastError();
+        c->graph = nullptr;
+        c->graph_failed = true;
+        fprintf(stderr, "daba: iteration graph capture failed (%s); launching eagerly\n",
+                rc != DABA_OK ? c->err.c_str() : cudaGetErrorString(ce));
       }
+    }
+    if (c->graph) {
       for (int it = 0; it < batch; ++it) CUDA_OR(c, cudaGraphLaunch(c->graph, c->stream));
     } else {
       for (int it = 0; it < batch; ++it) {
