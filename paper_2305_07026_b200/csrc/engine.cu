@@ -37,8 +37,9 @@ struct daba_ctx {
   int64_t host_k = 0;
   // halo exchange
   std::vector<PeerSeg> segs;
-  std::vector<std::pair<int64_t, int64_t>> peer_cam_idx, peer_pt_idx;  // (offset, count) into the index arrays
   int32_t *d_send_cam = nullptr, *d_send_pt = nullptr, *d_recv_cam = nullptr, *d_recv_pt = nullptr;
+  int64_t *d_send_cam_off = nullptr, *d_send_pt_off = nullptr, *d_recv_cam_off = nullptr, *d_recv_pt_off = nullptr;
+  int32_t n_send_cam = 0, n_send_pt = 0, n_recv_cam = 0, n_recv_pt = 0;
   double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
   // graph
   cudaGraphExec_t graph = nullptr;
@@ -206,27 +207,16 @@ void collect_times(daba_ctx* c) {
 
 int exchange_halo(daba_ctx* c, int* launches) {
   if (c->segs.empty()) return DABA_OK;
-  int n = 0;
-  for (size_t q = 0; q < c->segs.size(); ++q) {
-    const PeerSeg& s = c->segs[q];
-    const auto& sc = c->peer_cam_idx[2 * q];
-    const auto& sp = c->peer_pt_idx[2 * q];
-    n += timed(c, "k_pack", [&] {
-      return launch_pack(c->P, c->d_send_cam + sc.first, (int32_t)sc.second, c->d_send_pt + sp.first,
-                         (int32_t)sp.second, c->d_sendbuf + s.send_off, c->stream);
-    });
-  }
+  int n = timed(c, "k_pack", [&] {
+    return launch_pack(c->P, c->d_send_cam, c->d_send_cam_off, c->n_send_cam, c->d_send_pt, c->d_send_pt_off,
+                       c->n_send_pt, c->d_sendbuf, c->stream);
+  });
   std::string e = c->comm->exchange(c->d_sendbuf, c->d_recvbuf, c->segs, c->stream);
   if (!e.empty()) return fail(c, DABA_E_NCCL, e);
-  for (size_t q = 0; q < c->segs.size(); ++q) {
-    const PeerSeg& s = c->segs[q];
-    const auto& rc = c->peer_cam_idx[2 * q + 1];
-    const auto& rp = c->peer_pt_idx[2 * q + 1];
-    n += timed(c, "k_unpack", [&] {
-      return launch_unpack(c->P, c->d_recv_cam + rc.first, (int32_t)rc.second, c->d_recv_pt + rp.first,
-                           (int32_t)rp.second, c->d_recvbuf + s.recv_off, c->stream);
-    });
-  }
+  n += timed(c, "k_unpack", [&] {
+    return launch_unpack(c->P, c->d_recv_cam, c->d_recv_cam_off, c->n_recv_cam, c->d_recv_pt, c->d_recv_pt_off,
+                         c->n_recv_pt, c->d_recvbuf, c->stream);
+  });
   *launches += n;
   return DABA_OK;
 }
@@ -235,17 +225,15 @@ int exchange_halo(daba_ctx* c, int* launches) {
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
-  n += timed(c, "k_extrapolate", [&] { return launch_extrapolate(P, c->stream); });
   n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
-  n += timed(c, "k_pt_pass", [&] { return launch_pt_pass(P, c->stream); });
+  n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
   n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
-  n += timed(c, "k_cam_eval", [&] { return launch_cam_eval(P, c->stream); });
-  n += timed(c, "k_reduce_local", [&] { return launch_reduce_local(P, c->stream); });
+  n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
   if (c->comm) {
     std::string e = c->comm->allreduce(P.local, P.global, kGlobalCols, c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
+    n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
   }
-  n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
   *launches += n;
   int rc = exchange_halo(c, launches);
   if (rc) return rc;
@@ -412,7 +400,11 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = dalloc(C, &P.cams[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
     if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return bail(rc);
   }
-  if ((rc = dalloc(C, &P.cbar, (size_t)P.n_cams * kCamStride))) return bail(rc);
+  for (int r = 0; r < 2; ++r)
+    if ((rc = dalloc(C, &P.cbarb[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
+  if ((rc = dalloc(C, &P.counter, 1))) return bail(rc);
+  cudaMemsetAsync(P.counter, 0, sizeof(int32_t), C->stream);
+  P.has_comm = C->comm ? 1 : 0;
   for (int r = 0; r < 2; ++r)
     if ((rc = dalloc(C, &P.lbar[r], (size_t)P.n_pts))) return bail(rc);
   {
@@ -488,10 +480,10 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.b_cam = d1;
     P.b_pt = d2;
     P.b_uv = d4;
-    P.n_pt_blocks = (P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads;
+    P.n_pt_blocks = std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, 148 * 8));
   }
   // scratch
-  P.n_cam_eval_blocks = (P.n_own_cams + 127) / 128;
+  P.n_cam_eval_blocks = (2 * P.n_own_cams + 127) / 128;  // k_cam_solve blocks
   P.trace_cap = 1024;
   if ((rc = dalloc(C, &P.partial, (size_t)std::max(P.n_chunks, 1) * 2 * kPartialStride))) return bail(rc);
   if ((rc = dalloc(C, &P.moments, (size_t)std::max(P.n_own_cams, 1) * 2 * kPartialStride))) return bail(rc);
@@ -499,16 +491,17 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   if ((rc = dalloc(C, &P.decisions, (size_t)std::max(P.n_own_cams, 1) * 2))) return bail(rc);
   if ((rc = dalloc(C, &P.cam_part, (size_t)std::max(P.n_cam_eval_blocks, 1) * kCamEvalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.pt_part, (size_t)std::max(P.n_pt_blocks, 1) * kPtCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.red_part, (size_t)kReduceBlocks * kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.local, kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.global, kGlobalCols))) return bail(rc);
   if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return bail(rc);
   if ((rc = dalloc(C, &P.sched, 8))) return bail(rc);
   if (!C->comm) P.global = P.local;
   cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
-  // halo plan
+  // halo plan: per peer a segment [cameras x 15 | points x 3] of the send / receive buffers; the pack and unpack
+  // items of all peers are flattened so that one kernel does each
   if (nranks > 1) {
-    std::vector<int32_t> sc, sp, rcam, rpt;
+    std::vector<int32_t> sc, sp, rcm, rpt;
+    std::vector<int64_t> sco, spo, rco, rpo;
     int64_t soff = 0, roff = 0;
     for (const Peer& pe : S.peers) {
       PeerSeg sg;
@@ -517,20 +510,34 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       sg.send_cnt = 15 * (int64_t)pe.send_cams.size() + 3 * (int64_t)pe.send_pts.size();
       sg.recv_off = roff;
       sg.recv_cnt = 15 * (int64_t)pe.recv_cams.size() + 3 * (int64_t)pe.recv_pts.size();
+      for (size_t q = 0; q < pe.send_cams.size(); ++q) {
+        sc.push_back(pe.send_cams[q]);
+        sco.push_back(soff + 15 * (int64_t)q);
+      }
+      for (size_t q = 0; q < pe.send_pts.size(); ++q) {
+        sp.push_back(pe.send_pts[q]);
+        spo.push_back(soff + 15 * (int64_t)pe.send_cams.size() + 3 * (int64_t)q);
+      }
+      for (size_t q = 0; q < pe.recv_cams.size(); ++q) {
+        rcm.push_back(pe.recv_cams[q]);
+        rco.push_back(roff + 15 * (int64_t)q);
+      }
+      for (size_t q = 0; q < pe.recv_pts.size(); ++q) {
+        rpt.push_back(pe.recv_pts[q]);
+        rpo.push_back(roff + 15 * (int64_t)pe.recv_cams.size() + 3 * (int64_t)q);
+      }
       soff += sg.send_cnt;
       roff += sg.recv_cnt;
       C->segs.push_back(sg);
-      C->peer_cam_idx.push_back({(int64_t)sc.size(), (int64_t)pe.send_cams.size()});
-      C->peer_cam_idx.push_back({(int64_t)rcam.size(), (int64_t)pe.recv_cams.size()});
-      C->peer_pt_idx.push_back({(int64_t)sp.size(), (int64_t)pe.send_pts.size()});
-      C->peer_pt_idx.push_back({(int64_t)rpt.size(), (int64_t)pe.recv_pts.size()});
-      sc.insert(sc.end(), pe.send_cams.begin(), pe.send_cams.end());
-      sp.insert(sp.end(), pe.send_pts.begin(), pe.send_pts.end());
-      rcam.insert(rcam.end(), pe.recv_cams.begin(), pe.recv_cams.end());
-      rpt.insert(rpt.end(), pe.recv_pts.begin(), pe.recv_pts.end());
     }
+    C->n_send_cam = (int32_t)sc.size();
+    C->n_send_pt = (int32_t)sp.size();
+    C->n_recv_cam = (int32_t)rcm.size();
+    C->n_recv_pt = (int32_t)rpt.size();
     if ((rc = upload(C, &C->d_send_cam, sc)) || (rc = upload(C, &C->d_send_pt, sp)) ||
-        (rc = upload(C, &C->d_recv_cam, rcam)) || (rc = upload(C, &C->d_recv_pt, rpt)))
+        (rc = upload(C, &C->d_recv_cam, rcm)) || (rc = upload(C, &C->d_recv_pt, rpt)) ||
+        (rc = upload(C, &C->d_send_cam_off, sco)) || (rc = upload(C, &C->d_send_pt_off, spo)) ||
+        (rc = upload(C, &C->d_recv_cam_off, rco)) || (rc = upload(C, &C->d_recv_pt_off, rpo)))
       return bail(rc);
     if ((rc = dalloc(C, &C->d_sendbuf, (size_t)std::max<int64_t>(soff, 1))) ||
         (rc = dalloc(C, &C->d_recvbuf, (size_t)std::max<int64_t>(roff, 1))))
@@ -552,10 +559,8 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (cudaStreamSynchronize(C->stream) != cudaSuccess) return bail(DABA_E_CUDA);
   }
   // launches per iteration (for bookkeeping)
-  C->launches_per_iter = 8 - (P.n_chunks == 0) - (P.n_pt_blocks == 0) - (P.n_own_cams == 0) * 2 + (P.n_boundary > 0);
-  for (size_t q = 0; q < C->segs.size(); ++q)
-    C->launches_per_iter += (C->peer_cam_idx[2 * q].second + C->peer_pt_idx[2 * q].second > 0) +
-                            (C->peer_cam_idx[2 * q + 1].second + C->peer_pt_idx[2 * q + 1].second > 0);
+  C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) + (C->comm ? 1 : 0);
+  C->launches_per_iter += (C->n_send_cam + C->n_send_pt > 0) + (C->n_recv_cam + C->n_recv_pt > 0);
   *out = c.release();
   return DABA_OK;
 }

@@ -1,19 +1,21 @@
 // kernels.cu — fp64 CUDA kernels of one DABA iteration for sm_100a.
 //
 // Step map:
-//   a1+a2  k_extrapolate    schedule s, gamma (eq. nesterov_scalar) and x-bar cameras
-//                           (eqs. nesterov_R/t/d P:L312-323, ProjRot3D eq. proj_rot3d)
 //   a4+a5  k_cam_pass       per observation, both anchors: ray (eq. ray), lambda (eq. gamma
 //                           P:L222-224), error (eq. error), w and a (eqs. w, a P:L216-221);
-//                           block-reduced into 40 per-camera moments (the camera part of eq. P)
-//   a4+a5+a7 k_pt_pass      per point: both anchors' sums over its observations and the exact minimiser of
-//                           sum_i Q_ij + xi/2 ||l - l_hat||^2 (eq. Q, eq. Ealpha); the
-//                           point part of E(x_acc|x^k) (eq. Eak)
-//   a6     k_cam_solve      per camera and anchor: Gauss-Newton normal equations from the moments, one
-//                           successful Levenberg-Marquardt step by Jacobi-scaled 9x9 Cholesky
-//   a8     k_cam_eval       camera part of E(x_acc|x^k) and F(x^k) per camera
-//   a9     k_reduce_local   deterministic tree sums (-> allreduce when nranks > 1)
-//   a9+a10 k_select         F-bar (eq. lFak), restart test (Alg. 1), role rotation
+//                           block-reduced into 40 per-camera moments (the camera part of eq. P); the point
+//                           side of each pair emitted as a record (w lam^2, w lam R e)
+//   a7     k_pt_sum         per point: adds its records, exact minimiser of sum_i Q_ij + xi/2 ||l - l_hat||^2
+//                           (eq. Q, eq. Ealpha), the point part of E(x_acc|x^k) (eq. Eak
+//                           P:L374-376), and x-bar^{k+1} of both candidates (eq. nesterov_l)
+//          k_pt_boundary    records of observations whose camera lives on another rank (N > 1)
+//   a6+a8  k_cam_solve      per camera and anchor: Gauss-Newton normal equations from the moments, one
+//                           successful Levenberg-Marquardt step by Jacobi-scaled 9x9 Cholesky, the
+//                           candidates' x-bar^{k+1} (eqs. nesterov_R/t/d, ProjRot3D eq. proj_rot3d
+//                           P:L332-337), and the camera part of E(x_acc|x^k) and F(x^k)
+//   a9     k_reduce         deterministic sums (-> allreduce when nranks > 1)
+//   a9+a10 k_select         F-bar (eq. lFak), restart test (Alg. 1), role rotation;
+//                           folded into k_reduce when the rank has no communicator
 #include <cstdio>
 
 #include "kernels.h"
@@ -47,36 +49,22 @@ __device__ __forceinline__ void ld_point(const double4* base, int64_t j, double&
   z = b.x;
 }
 
-// ------------------------------------------------------------------ a1 + a2
-__global__ void k_extrapolate(IterParams p) {
-  const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) {
-    p.sched[3] = gamma;
-    double s1;
-    sched_gamma(p.sched[0], p.accelerate, &s1);
-    p.sched[4] = sched_gamma(s1, p.accelerate, nullptr);  // gamma^{(k+1)}
-  }
-  if (i < p.n_pts - p.n_own_pts) {  // halo points: eq. nesterov_l from the exchanged x^k and the cached x^{k-1}
-    const int j = p.n_own_pts + i;
-    const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
-    p.lbar[p.roles[4]][j] = make_double4(fma(gamma, k4.x - p4.x, k4.x), fma(gamma, k4.y - p4.y, k4.y),
-                                         fma(gamma, k4.z - p4.z, k4.z), 0.0);
-  }
-  if (i >= p.n_cams) return;
-  const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
-  const double* cp = p.cams[p.roles[0]] + (size_t)i * kCamStride;
-  double* cb = p.cbar + (size_t)i * kCamStride;
+// gamma^{(k+1)} from s^{(k)} (two schedule steps), for the x-bar of the next iteration
+__device__ __forceinline__ double sched_gamma_next(double s, int accelerate) {
+  double s1;
+  sched_gamma(s, accelerate, &s1);
+  return sched_gamma(s1, accelerate, nullptr);
+}
+
+// x-bar camera (eqs. nesterov_R/t/d): ProjRot3D(R + g (R - R_prev)), t, d linear
+__device__ __forceinline__ void extrapolate_camera(const double* ck, const double* cp, double gamma, double* out) {
   double M[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) M[k] = ck[k] + gamma * (ck[k] - cp[k]);  // eq. nesterov_R before ProjRot3D
-  double R[9];
-  proj_rot3d(M, R);
+  for (int k = 0; k < 9; ++k) M[k] = ck[k] + gamma * (ck[k] - cp[k]);
+  proj_rot3d(M, out);
 #pragma unroll
-  for (int k = 0; k < 9; ++k) cb[k] = R[k];
-#pragma unroll
-  for (int k = 9; k < 15; ++k) cb[k] = ck[k] + gamma * (ck[k] - cp[k]);  // eqs. nesterov_t, nesterov_d
-  cb[15] = 0.0;
+  for (int k = 9; k < 15; ++k) out[k] = ck[k] + gamma * (ck[k] - cp[k]);
+  out[15] = 0.0;
 }
 
 // ------------------------------------------------------------------ a4 + a5: camera pass
@@ -232,7 +220,7 @@ constexpr int kRing = DABA_RING;
 template <int LOSS, bool ACC>
 __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc,
                                               double2* ring, int32_t* sidx) {
-  const double* cam = (ACC ? p.cbar : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
+  const double* cam = (ACC ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
 #ifdef DABA_CAM_REGS
   CamRegs c;
 #pragma unroll
@@ -439,7 +427,7 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
   const double nx = lk[0] + mx, ny = lk[1] + my, nz = lk[2] + mz;
   p.pts[p.roles[3]][j] = make_double4(nx, ny, nz, 0.0);
   // x-bar^{k+1} for either outcome of the restart test (eq. nesterov_l with gamma^{(k+1)}); k_select keeps one
-  const double g1 = p.sched[4];
+  const double g1 = sched_gamma_next(p.sched[0], p.accelerate);
   p.lbar[0][j] = make_double4(fma(g1, ax - lk[0], ax), fma(g1, ay - lk[1], ay), fma(g1, az - lk[2], az), 0.0);
   p.lbar[1][j] = make_double4(fma(g1, nx - lk[0], nx), fma(g1, ny - lk[1], ny), fma(g1, nz - lk[2], nz), 0.0);
   // Q-part of E(x|x^k) - E(x^k|x^k): (A_k + xi/2) |dl|^2 - C_k . dl  (eq. Q expanded at the anchor)
@@ -463,25 +451,61 @@ __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
   const double2 u = p.b_uv[b];
   const double4 lk = p.pts[p.roles[1]][j], lb = p.lbar[p.roles[4]][j];
   double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  pt_terms<LOSS>(p.cbar + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
+  pt_terms<LOSS>(p.cbarb[p.roles[4]] + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
   pt_terms<LOSS>(p.cams[p.roles[1]] + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
   const int64_t r = p.n_cam_side + b;
   reinterpret_cast<double4*>(p.staging)[r] = make_double4(a[0], a[1], a[2], a[3]);
   reinterpret_cast<double4*>(p.staging + 4 * p.n_records)[r] = make_double4(a[4], a[5], a[6], a[7]);
 }
 
-// Point solve (a7): each owned point adds its observations' staged contributions in ascending (camera) order
-// and takes the exact minimiser for both anchors; deterministic, no atomics.
-__global__ void __launch_bounds__(kPtPassThreads) k_pt_sum(IterParams p) {
-  const int j = blockIdx.x * kPtPassThreads + threadIdx.x;
+__device__ void do_select(const IterParams& p);
+
+// Rank-local sums of the camera partials (k_cam_solve blocks, 8 columns) and point partials (k_pt_sum blocks,
+// 4 columns) in a fixed order by one 256-thread block -> p.local (a9).
+__device__ void final_reduce(const IterParams& p, int n_pt_parts) {
+  __shared__ double s[kGlobalCols][256];
+  double v[kGlobalCols];
+  for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
+  for (int b = threadIdx.x; b < p.n_cam_eval_blocks; b += 256) {
+    const double* q = p.cam_part + (size_t)b * kCamEvalCols;
+    v[0] += __ldcg(q + 0);
+    v[1] += __ldcg(q + 1);
+    v[3] += __ldcg(q + 2);
+    v[5] += __ldcg(q + 3);
+    v[6] += __ldcg(q + 4);
+    v[7] += __ldcg(q + 5);
+    v[8] += __ldcg(q + 6);
+    v[9] += __ldcg(q + 7);
+  }
+  for (int b = threadIdx.x; b < n_pt_parts; b += 256) {
+    const double* q = p.pt_part + (size_t)b * kPtCols;
+    v[2] += __ldcg(q + 0);
+    v[4] += __ldcg(q + 1);
+    v[5] += __ldcg(q + 2);
+    v[6] += __ldcg(q + 3);
+  }
+  for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < kGlobalCols) p.local[threadIdx.x] = s[threadIdx.x][0];
+}
+
+// Point solve (a7) over a grid-stride set of owned points: each point adds its observations' records in
+// ascending (camera) order and takes the exact minimiser for both anchors.  The last block to finish forms the
+// rank-local sums (a9) and, without a communicator, takes the restart decision (a9 + a10).  Deterministic.
+__global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   double qv[kPtCols] = {0, 0, 0, 0};
-  if (j < p.n_own_pts) {
+  const double4* ra = reinterpret_cast<const double4*>(p.staging);
+  const double4* rm = reinterpret_cast<const double4*>(p.staging + 4 * p.n_records);
+  for (int j = blockIdx.x * kPtPassThreads + threadIdx.x; j < p.n_own_pts; j += gridDim.x * kPtPassThreads) {
     const double4 k4 = p.pts[p.roles[1]][j], b4 = p.lbar[p.roles[4]][j];
     const double lk[3] = {k4.x, k4.y, k4.z};
     const double lb[3] = {b4.x, b4.y, b4.z};
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const double4* ra = reinterpret_cast<const double4*>(p.staging);
-    const double4* rm = reinterpret_cast<const double4*>(p.staging + 4 * p.n_records);
     const int64_t o1 = p.p_ptr[j + 1];
     for (int64_t o = p.p_ptr[j]; o < o1; o += 4) {  // up to 4 records (8 x 32 B) in flight per thread
       int32_t r[4];
@@ -501,10 +525,14 @@ __global__ void __launch_bounds__(kPtPassThreads) k_pt_sum(IterParams p) {
           acc[4] += B[i].x; acc[5] += B[i].y; acc[6] += B[i].z; acc[7] += B[i].w;
         }
     }
-    pt_finish(p, j, lb, lk, acc, qv);
+    double q[kPtCols];
+    pt_finish(p, j, lb, lk, acc, q);
+#pragma unroll
+    for (int c = 0; c < kPtCols; ++c) qv[c] += q[c];
   }
   // block sums: warp shuffles, then one shared-memory step (deterministic order)
   __shared__ double ws[kPtPassThreads / 32][kPtCols];
+  __shared__ bool last;
 #pragma unroll
   for (int c = 0; c < kPtCols; ++c) {
     double v = qv[c];
@@ -517,6 +545,18 @@ __global__ void __launch_bounds__(kPtPassThreads) k_pt_sum(IterParams p) {
     double v = 0;
     for (int w = 0; w < kPtPassThreads / 32; ++w) v += ws[w][threadIdx.x];
     p.pt_part[(size_t)blockIdx.x * kPtCols + threadIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  final_reduce(p, gridDim.x);
+  if (threadIdx.x == 0) {
+    *p.counter = 0;
+    __threadfence();
+    if (!p.has_comm) do_select(p);
   }
 }
 
@@ -654,128 +694,136 @@ __device__ void normal_equations(const double* Rh, const Sums& S, double xi, dou
   }
 }
 
+__host__ __device__ constexpr int tri(int r, int c) { return r * (r + 1) / 2 + c; }  // packed lower triangle
+
+// a6 + a8, one thread per (camera, anchor); lanes 2i and 2i+1 hold camera i's accelerated (x-bar^k) and MM
+// (x^k) subproblems.  Each thread sums its chunk partials (fixed order), builds the normal equations from the
+// moments, takes one successful LM step, writes its candidate and the candidate's x-bar for the next iteration;
+// the MM lane then evaluates the camera's part of E(x_acc|x^k) - F(x^k) and F(x^k) from its own (x^k) sums.
 __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * p.n_own_cams) return;
-  const int i = t >> 1, a = t & 1;  // a = 0: accelerated anchor x-bar^k, a = 1: x^k
-  // sum this camera's chunk partials in chunk order (deterministic)
+  const bool valid = t < 2 * p.n_own_cams;
+  const int i = valid ? (t >> 1) : 0, a = t & 1;  // a = 0: accelerated anchor x-bar^k, a = 1: x^k
   double m[kPartialStride];
   for (int k = 0; k < kPartialStride; ++k) m[k] = 0.0;
-  for (int c = p.cam_chunk_ptr[i]; c < p.cam_chunk_ptr[i + 1]; ++c) {
-    const double* src = p.partial + ((size_t)c * 2 + a) * kPartialStride;
-    for (int k = 0; k < kPartialStride; ++k) m[k] += src[k];
-  }
-  double* mdst = p.moments + ((size_t)i * 2 + a) * kPartialStride;
-  for (int k = 0; k < kPartialStride; ++k) mdst[k] = m[k];
-  const double* anchor = (a == 0 ? p.cbar : p.cams[p.roles[1]]) + (size_t)i * kCamStride;
-  double Rh[9], th[3], dh[3];
-  for (int k = 0; k < 9; ++k) Rh[k] = anchor[k];
-  for (int k = 0; k < 3; ++k) th[k] = anchor[9 + k];
-  for (int k = 0; k < 3; ++k) dh[k] = anchor[12 + k];
+  double out[15], Rh[9], th[3], dh[3];
   Sums S;
-  derive_sums(m, dh, S);
-  double H[81], g[9];
-  normal_equations(Rh, S, p.xi, H, g);
-  double sc[9];
-  for (int k = 0; k < 9; ++k) sc[k] = 1.0 / sqrt(H[9 * k + k]);
-  for (int r = 0; r < 9; ++r) {
-    g[r] *= sc[r];
-    for (int c = 0; c < 9; ++c) H[9 * r + c] *= sc[r] * sc[c];
-  }
-  double out[15];
-  for (int k = 0; k < 15; ++k) out[k] = anchor[k];
   int accepted = -1;
   double dP_acc = 0.0;
-  double mu = p.mu0;
-  for (int tau = 0; tau < p.max_trials; ++tau, mu *= p.mu_up) {
-    // Cholesky of (H + mu diag H) in the Jacobi-scaled variables (lower triangle in L)
-    double L[81];
-    bool ok = true;
-    for (int j = 0; j < 9 && ok; ++j) {
-      double s = H[9 * j + j] * (1.0 + mu);
-      for (int k = 0; k < j; ++k) s -= L[9 * j + k] * L[9 * j + k];
-      if (!(s > 0)) {
-        ok = false;
+  const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
+  if (valid) {
+    for (int c = p.cam_chunk_ptr[i]; c < p.cam_chunk_ptr[i + 1]; ++c) {
+      const double* src = p.partial + ((size_t)c * 2 + a) * kPartialStride;
+      for (int k = 0; k < kPartialStride; ++k) m[k] += src[k];
+    }
+    const double* anchor = (a == 0 ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]]) + (size_t)i * kCamStride;
+    for (int k = 0; k < 9; ++k) Rh[k] = anchor[k];
+    for (int k = 0; k < 3; ++k) th[k] = anchor[9 + k];
+    for (int k = 0; k < 3; ++k) dh[k] = anchor[12 + k];
+    derive_sums(m, dh, S);
+    double H[81], g[9];
+    normal_equations(Rh, S, p.xi, H, g);
+    double sc[9];
+    for (int k = 0; k < 9; ++k) sc[k] = 1.0 / sqrt(H[9 * k + k]);
+    for (int r = 0; r < 9; ++r) {
+      g[r] *= sc[r];
+      for (int c = 0; c < 9; ++c) H[9 * r + c] *= sc[r] * sc[c];
+    }
+    for (int k = 0; k < 15; ++k) out[k] = anchor[k];
+    double mu = p.mu0;
+#pragma unroll 1
+    for (int tau = 0; tau < p.max_trials; ++tau, mu *= p.mu_up) {
+      // Cholesky of (H + mu diag H) in the Jacobi-scaled variables; fully unrolled (packed lower triangle in
+      // registers).  A non-positive pivot makes the trial fail (Q3).
+      double L[45];
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        double s = H[9 * j + j] * (1.0 + mu);
+#pragma unroll
+        for (int k = 0; k < j; ++k) s -= L[tri(j, k)] * L[tri(j, k)];
+        ok = ok && (s > 0);
+        const double ljj = sqrt(s > 0 ? s : 1.0);
+        L[tri(j, j)] = ljj;
+        const double il = 1.0 / ljj;
+#pragma unroll
+        for (int r = j + 1; r < 9; ++r) {
+          double v = H[9 * r + j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) v -= L[tri(r, k)] * L[tri(j, k)];
+          L[tri(r, j)] = v * il;
+        }
+      }
+      if (!ok) continue;
+      double y[9], x[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        double v = -g[r];
+#pragma unroll
+        for (int k = 0; k < r; ++k) v -= L[tri(r, k)] * y[k];
+        y[r] = v / L[tri(r, r)];
+      }
+#pragma unroll
+      for (int r = 8; r >= 0; --r) {
+        double v = y[r];
+#pragma unroll
+        for (int k = r + 1; k < 9; ++k) v -= L[tri(k, r)] * x[k];
+        x[r] = v / L[tri(r, r)];
+      }
+      double delta[9];
+      for (int k = 0; k < 9; ++k) delta[k] = x[k] * sc[k];
+      double EmI[9], dR[9];
+      expm_minus_identity(delta, EmI);
+      mat3_mul(EmI, Rh, dR);  // (Exp(dtheta) - I) R_hat
+      const double dP = delta_P(Rh, S, dR, delta + 3, delta + 6, p.xi);
+      if (dP < 0.0) {  // strict decrease: accept ("one successful inner LM step")
+        for (int k = 0; k < 9; ++k) out[k] = Rh[k] + dR[k];
+        for (int k = 0; k < 3; ++k) out[9 + k] = th[k] + delta[3 + k];
+        for (int k = 0; k < 3; ++k) out[12 + k] = dh[k] + delta[6 + k];
+        accepted = tau;
+        dP_acc = dP;
         break;
       }
-      const double ljj = sqrt(s);
-      L[9 * j + j] = ljj;
-      const double il = 1.0 / ljj;
-      for (int r = j + 1; r < 9; ++r) {
-        double v = H[9 * r + j];
-        for (int k = 0; k < j; ++k) v -= L[9 * r + k] * L[9 * j + k];
-        L[9 * r + j] = v * il;
-      }
-    }
-    if (!ok) continue;  // non-positive pivot: a failed trial (Q3)
-    double y[9], x[9];
-    for (int r = 0; r < 9; ++r) {
-      double v = -g[r];
-      for (int k = 0; k < r; ++k) v -= L[9 * r + k] * y[k];
-      y[r] = v / L[9 * r + r];
-    }
-    for (int r = 8; r >= 0; --r) {
-      double v = y[r];
-      for (int k = r + 1; k < 9; ++k) v -= L[9 * k + r] * x[k];
-      x[r] = v / L[9 * r + r];
-    }
-    double delta[9];
-    for (int k = 0; k < 9; ++k) delta[k] = x[k] * sc[k];
-    double EmI[9], dR[9];
-    expm_minus_identity(delta, EmI);
-    mat3_mul(EmI, Rh, dR);  // (Exp(dtheta) - I) R_hat
-    const double dP = delta_P(Rh, S, dR, delta + 3, delta + 6, p.xi);
-    if (dP < 0.0) {  // strict decrease: accept ("one successful inner LM step")
-      for (int k = 0; k < 9; ++k) out[k] = Rh[k] + dR[k];
-      for (int k = 0; k < 3; ++k) out[9 + k] = th[k] + delta[3 + k];
-      for (int k = 0; k < 3; ++k) out[12 + k] = dh[k] + delta[6 + k];
-      accepted = tau;
-      dP_acc = dP;
-      break;
     }
   }
-  double* dst = p.cams[p.roles[2 + a]] + (size_t)i * kCamStride;
-  for (int k = 0; k < 15; ++k) dst[k] = out[k];
-  dst[15] = 0.0;
-  p.decisions[2 * i + a] = accepted;
-  if (a == 1) p.dP_mm[i] = dP_acc;
-}
-
-// ------------------------------------------------------------------ a8: camera part of E(x_acc|x^k), F(x^k)
-__global__ void __launch_bounds__(128) k_cam_eval(IterParams p) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  __syncwarp();  // every lane has read the current x-bar before any lane overwrites an x-bar buffer
+  if (valid) {
+    double* dst = p.cams[p.roles[2 + a]] + (size_t)i * kCamStride;
+    for (int k = 0; k < 15; ++k) dst[k] = out[k];
+    dst[15] = 0.0;
+    p.decisions[2 * i + a] = accepted;
+    // x-bar^{k+1} of this candidate (used if the restart test selects it): eqs. nesterov_x with gamma^{(k+1)}
+    double cb[16];
+    extrapolate_camera(out, ck, sched_gamma_next(p.sched[0], p.accelerate), cb);
+    double* cdst = p.cbarb[a] + (size_t)i * kCamStride;
+    for (int k = 0; k < 16; ++k) cdst[k] = cb[k];
+  }
+  // camera part of E(x_acc|x^k) on the MM lane: the accelerated candidate comes from the partner lane
+  double ca[15];
+  for (int k = 0; k < 15; ++k) ca[k] = __shfl_xor_sync(0xffffffffu, out[k], 1);
+  const int acc_accepted = __shfl_xor_sync(0xffffffffu, accepted, 1);
   double q[kCamEvalCols];
   for (int k = 0; k < kCamEvalCols; ++k) q[k] = 0.0;
-  if (i < p.n_own_cams) {
-    const double* m = p.moments + ((size_t)i * 2 + 1) * kPartialStride;
-    const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
-    const double* ca = p.cams[p.roles[2]] + (size_t)i * kCamStride;
-    const double* cm = p.cams[p.roles[3]] + (size_t)i * kCamStride;
-    double Rh[9], dR[9], dt[3], dd[3], dh[3];
-    for (int k = 0; k < 9; ++k) {
-      Rh[k] = ck[k];
-      dR[k] = ca[k] - ck[k];
-    }
+  if (valid && a == 1) {
+    double dR[9], dt[3], dd[3];
+    for (int k = 0; k < 9; ++k) dR[k] = ca[k] - Rh[k];
     for (int k = 0; k < 3; ++k) {
-      dt[k] = ca[9 + k] - ck[9 + k];
-      dd[k] = ca[12 + k] - ck[12 + k];
-      dh[k] = ck[12 + k];
+      dt[k] = ca[9 + k] - th[k];
+      dd[k] = ca[12 + k] - dh[k];
     }
-    Sums S;
-    derive_sums(m, dh, S);
     q[0] = m[39] + 0.5 * m[38];  // F_i = sum (a + w |e|^2 / 2) = sum rho / 2
     q[1] = delta_P(Rh, S, dR, dt, dd, p.xi);
-    q[2] = p.dP_mm[i];
+    q[2] = dP_acc;
     double sa = 0, sm = 0;
     for (int k = 0; k < 15; ++k) {
       sa += (ca[k] - ck[k]) * (ca[k] - ck[k]);
-      sm += (cm[k] - ck[k]) * (cm[k] - ck[k]);
+      sm += (out[k] - ck[k]) * (out[k] - ck[k]);
     }
     q[3] = sa;
     q[4] = sm;
     q[5] = m[40];
-    q[6] = p.decisions[2 * i] < 0 ? 1.0 : 0.0;
-    q[7] = p.decisions[2 * i + 1] < 0 ? 1.0 : 0.0;
+    q[6] = acc_accepted < 0 ? 1.0 : 0.0;
+    q[7] = accepted < 0 ? 1.0 : 0.0;
   }
   __shared__ double sq[kCamEvalCols][128];
   for (int c = 0; c < kCamEvalCols; ++c) sq[c][threadIdx.x] = q[c];
@@ -788,63 +836,8 @@ __global__ void __launch_bounds__(128) k_cam_eval(IterParams p) {
   if (threadIdx.x < kCamEvalCols) p.cam_part[(size_t)blockIdx.x * kCamEvalCols + threadIdx.x] = sq[threadIdx.x][0];
 }
 
-// ------------------------------------------------------------------ a9: rank-local sums (two stages)
-// Stage 1: kReduceBlocks CTAs, CTA b sums a contiguous, fixed range of the partials (deterministic).
-__global__ void __launch_bounds__(256) k_reduce_partial(IterParams p) {
-  __shared__ double s[kGlobalCols][256];
-  double v[kGlobalCols];
-  for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
-  const int nb = gridDim.x;
-  const int64_t c0 = (int64_t)p.n_cam_eval_blocks * blockIdx.x / nb, c1 = (int64_t)p.n_cam_eval_blocks * (blockIdx.x + 1) / nb;
-  const int64_t q0 = (int64_t)p.n_pt_blocks * blockIdx.x / nb, q1 = (int64_t)p.n_pt_blocks * (blockIdx.x + 1) / nb;
-  for (int64_t b = c0 + threadIdx.x; b < c1; b += 256) {
-    const double* q = p.cam_part + (size_t)b * kCamEvalCols;
-    v[0] += q[0];
-    v[1] += q[1];
-    v[3] += q[2];
-    v[5] += q[3];
-    v[6] += q[4];
-    v[7] += q[5];
-    v[8] += q[6];
-    v[9] += q[7];
-  }
-  for (int64_t b = q0 + threadIdx.x; b < q1; b += 256) {
-    const double* q = p.pt_part + (size_t)b * kPtCols;
-    v[2] += q[0];
-    v[4] += q[1];
-    v[5] += q[2];
-    v[6] += q[3];
-  }
-  for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
-  __syncthreads();
-  for (int st = 128; st > 0; st >>= 1) {
-    if (threadIdx.x < st)
-      for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
-    __syncthreads();
-  }
-  if (threadIdx.x < kGlobalCols) p.red_part[(size_t)blockIdx.x * kGlobalCols + threadIdx.x] = s[threadIdx.x][0];
-}
-
-// Stage 2: one CTA over the stage-1 partials.
-__global__ void __launch_bounds__(256) k_reduce_local(IterParams p) {
-  __shared__ double s[kGlobalCols][256];
-  double v[kGlobalCols];
-  for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
-  if (threadIdx.x < kReduceBlocks)
-    for (int c = 0; c < kGlobalCols; ++c) v[c] = p.red_part[(size_t)threadIdx.x * kGlobalCols + c];
-  for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
-  __syncthreads();
-  for (int st = 128; st > 0; st >>= 1) {
-    if (threadIdx.x < st)
-      for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
-    __syncthreads();
-  }
-  if (threadIdx.x < kGlobalCols) p.local[threadIdx.x] = s[threadIdx.x][0];
-}
-
 // ------------------------------------------------------------------ a9 + a10: restart test and selection
-__global__ void k_select(IterParams p) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void do_select(const IterParams& p) {
   const double* G = p.global;
   double s_next;
   const double gamma = sched_gamma(p.sched[0], p.accelerate, &s_next);
@@ -870,65 +863,76 @@ __global__ void k_select(IterParams p) {
   p.roles[1] = restart ? r3 : r2;  // x^{k+1} = x_mm (restart, Alg. 1) or x_acc (L414)
   p.roles[2] = r0;
   p.roles[3] = restart ? r2 : r3;
-  p.roles[4] = restart ? 1 : 0;    // x-bar^{k+1} computed from the selected candidate
+  p.roles[4] = restart ? 1 : 0;    // x-bar^{k+1} buffers written from the selected candidate
   p.sched[0] = s_next;
   p.sched[1] = Fbar;
   p.sched[2] = (double)(k + 1);
 }
 
-// x-bar^k of every local point from x^k, x^{k-1} (create / set_state); writes lbar[roles[4]]
+__global__ void k_select(IterParams p) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) do_select(p);
+}
+
+// x-bar^k of every local camera and point from x^k, x^{k-1} (create / set_state); writes the role-selected
+// x-bar buffers
 __global__ void k_lbar_all(IterParams p) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= p.n_pts) return;
   const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
-  const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
-  p.lbar[p.roles[4]][j] = make_double4(fma(gamma, k4.x - p4.x, k4.x), fma(gamma, k4.y - p4.y, k4.y),
-                                       fma(gamma, k4.z - p4.z, k4.z), 0.0);
+  if (j < p.n_pts) {
+    const double4 k4 = p.pts[p.roles[1]][j], p4 = p.pts[p.roles[0]][j];
+    p.lbar[p.roles[4]][j] = make_double4(fma(gamma, k4.x - p4.x, k4.x), fma(gamma, k4.y - p4.y, k4.y),
+                                         fma(gamma, k4.z - p4.z, k4.z), 0.0);
+  }
+  if (j < p.n_cams)
+    extrapolate_camera(p.cams[p.roles[1]] + (size_t)j * kCamStride, p.cams[p.roles[0]] + (size_t)j * kCamStride, gamma,
+                       p.cbarb[p.roles[4]] + (size_t)j * kCamStride);
 }
 
 // ------------------------------------------------------------------ halo pack / unpack (x^k)
-__global__ void k_pack(IterParams p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                       double* buf) {
+__global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                       const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_cam) {
     const double* c = p.cams[p.roles[1]] + (size_t)cam_idx[t] * kCamStride;
-    for (int k = 0; k < 15; ++k) buf[(size_t)t * 15 + k] = c[k];
+    double* b = buf + cam_off[t];
+    for (int k = 0; k < 15; ++k) b[k] = c[k];
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
     const double4 l = p.pts[p.roles[1]][pt_idx[q]];
-    double* b = buf + (size_t)n_cam * 15 + (size_t)q * 3;
+    double* b = buf + pt_off[q];
     b[0] = l.x;
     b[1] = l.y;
     b[2] = l.z;
   }
 }
 
-__global__ void k_unpack(IterParams p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                         const double* buf) {
+__global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                         const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
   if (t < n_cam) {
-    double* c = p.cams[p.roles[1]] + (size_t)cam_idx[t] * kCamStride;
-    for (int k = 0; k < 15; ++k) c[k] = buf[(size_t)t * 15 + k];
+    const size_t i = (size_t)cam_idx[t] * kCamStride;
+    double* c = p.cams[p.roles[1]] + i;
+    for (int k = 0; k < 15; ++k) c[k] = buf[cam_off[t] + k];
     c[15] = 0.0;
+    extrapolate_camera(c, p.cams[p.roles[0]] + i, gamma, p.cbarb[p.roles[4]] + i);
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
-    const double* b = buf + (size_t)n_cam * 15 + (size_t)q * 3;
+    const double* b = buf + pt_off[q];
+    const double4 lp = p.pts[p.roles[0]][pt_idx[q]];
     p.pts[p.roles[1]][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);
+    p.lbar[p.roles[4]][pt_idx[q]] = make_double4(fma(gamma, b[0] - lp.x, b[0]), fma(gamma, b[1] - lp.y, b[1]),
+                                                 fma(gamma, b[2] - lp.z, b[2]), 0.0);
   }
 }
 
 // ------------------------------------------------------------------ launchers
 static inline int blocks(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-int launch_extrapolate(const IterParams& p, cudaStream_t st) {
-  const int64_t n = p.n_cams > p.n_pts - p.n_own_pts ? p.n_cams : p.n_pts - p.n_own_pts;
-  k_extrapolate<<<blocks(n > 0 ? n : 1, 128), 128, 0, st>>>(p);
-  return 1;
-}
-
 int launch_lbar_all(const IterParams& p, cudaStream_t st) {
-  if (p.n_pts == 0) return 0;
-  k_lbar_all<<<blocks(p.n_pts, 256), 256, 0, st>>>(p);
+  const int64_t n = p.n_pts > p.n_cams ? p.n_pts : p.n_cams;
+  if (n == 0) return 0;
+  k_lbar_all<<<blocks(n, 256), 256, 0, st>>>(p);
   return 1;
 }
 
@@ -964,11 +968,12 @@ int launch_pt_pass(const IterParams& p, cudaStream_t st) {
     }
     ++n;
   }
-  if (p.n_pt_blocks > 0) {
-    k_pt_sum<<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p);
-    ++n;
-  }
   return n;
+}
+
+int launch_pt_sum(const IterParams& p, cudaStream_t st) {
+  k_pt_sum<<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p);
+  return 1;
 }
 
 int launch_cam_solve(const IterParams& p, cudaStream_t st) {
@@ -977,17 +982,6 @@ int launch_cam_solve(const IterParams& p, cudaStream_t st) {
   return 1;
 }
 
-int launch_cam_eval(const IterParams& p, cudaStream_t st) {
-  if (p.n_cam_eval_blocks == 0) return 0;
-  k_cam_eval<<<p.n_cam_eval_blocks, 128, 0, st>>>(p);
-  return 1;
-}
-
-int launch_reduce_local(const IterParams& p, cudaStream_t st) {
-  k_reduce_partial<<<kReduceBlocks, 256, 0, st>>>(p);
-  k_reduce_local<<<1, 256, 0, st>>>(p);
-  return 2;
-}
 
 int launch_select(const IterParams& p, cudaStream_t st) {
   k_select<<<1, 32, 0, st>>>(p);
@@ -1008,17 +1002,17 @@ int launch_objective(const IterParams& p, cudaStream_t st) {
   return n + 1;
 }
 
-int launch_pack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                double* buf, cudaStream_t st) {
+int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, n_cam, pt_idx, n_pt, buf);
+  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf);
   return 1;
 }
 
-int launch_unpack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                  const double* buf, cudaStream_t st) {
+int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, n_cam, pt_idx, n_pt, buf);
+  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf);
   return 1;
 }
 

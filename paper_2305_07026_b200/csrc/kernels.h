@@ -17,7 +17,6 @@ constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
 constexpr int kGlobalCols = 10;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kTraceCols = 10;    // = DABA_TRACE_COLS
-constexpr int kReduceBlocks = 128; // stage-1 CTAs of the rank-local reduction
 
 struct CamChunk {
   int32_t cam;    // local camera index (owned)
@@ -42,10 +41,11 @@ struct IterParams {
   double* cams[4];       // n_cams x 16
   double4* pts[4];       // n_pts
   double4* lbar[2];      // x-bar^k of the points: roles[4] selects the valid buffer
-  double* cbar;          // extrapolated cameras x-bar^k, n_cams x 16
+  double* cbarb[2];      // x-bar^k cameras, n_cams x 16: roles[4] selects the valid buffer
   int32_t* roles;        // [5]: x^{k-1}, x^k, acc, mm buffers; valid x-bar point buffer
-  double* sched;         // [0] s^{(k)}, [1] F-bar^{(k-1)}, [2] iteration counter k (as double), [3] gamma^{(k)},
-                         // [4] gamma^{(k+1)}
+  double* sched;         // [0] s^{(k)}, [1] F-bar^{(k-1)}, [2] iteration counter k (as double)
+  int32_t* counter;      // last-block detection of k_reduce (zero between launches)
+  int32_t has_comm;      // 1: sums are allreduced, k_select runs after the collective
   // camera-side observations (sorted by camera, then point)
   const CamChunk* chunks;
   const int32_t* cam_chunk_ptr;  // n_own_cams + 1
@@ -71,7 +71,6 @@ struct IterParams {
   double* cam_part;       // camera-eval blocks x kCamEvalCols
   double* pt_part;        // point-pass blocks x kPtCols
   int32_t n_cam_eval_blocks, n_pt_blocks;
-  double* red_part;       // kReduceBlocks x kGlobalCols
   double* local;          // kGlobalCols (this rank's sums)
   double* global;         // kGlobalCols (allreduced)
   double* trace;          // trace ring, trace_cap x kTraceCols
@@ -79,20 +78,19 @@ struct IterParams {
 };
 
 // Launchers (all asynchronous on `st`).  They return the number of kernels launched.
-int launch_extrapolate(const IterParams& p, cudaStream_t st);
 int launch_lbar_all(const IterParams& p, cudaStream_t st);
 int launch_cam_pass(const IterParams& p, cudaStream_t st);
 int launch_pt_pass(const IterParams& p, cudaStream_t st);
 int launch_cam_solve(const IterParams& p, cudaStream_t st);
-int launch_cam_eval(const IterParams& p, cudaStream_t st);
-int launch_reduce_local(const IterParams& p, cudaStream_t st);
+int launch_pt_sum(const IterParams& p, cudaStream_t st);  // + rank-local sums (+ select without comm)
 int launch_select(const IterParams& p, cudaStream_t st);
 // F(x^k) only (create-time F-bar^{(-1)} and daba_objective): writes local[0] (and local[7] = degenerate count)
 int launch_objective(const IterParams& p, cudaStream_t st);
 // halo exchange helpers: gather owned boundary entries of x^k into a send buffer / scatter received entries
-int launch_pack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                double* buf, cudaStream_t st);
-int launch_unpack(const IterParams& p, const int32_t* cam_idx, int32_t n_cam, const int32_t* pt_idx, int32_t n_pt,
-                  const double* buf, cudaStream_t st);
+int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, cudaStream_t st);
+// also writes x-bar of the received halo entries (gamma of the next iteration)
+int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
+                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, cudaStream_t st);
 
 }  // namespace daba
