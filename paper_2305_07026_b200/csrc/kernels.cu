@@ -243,22 +243,35 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
 #pragma unroll
   for (int k = 0; k < kRing - 1; ++k) issue(k);
 #ifdef DABA_DUAL
-  // two observations per step: two independent dependency chains feed the same accumulators
-  double4 la = n > 0 ? ld256(L + sidx[tid]) : make_double4(0, 0, 0, 0);
-  double4 lb = n > 1 ? ld256(L + sidx[tid + kCamPassThreads]) : make_double4(0, 0, 0, 0);
+  // two observations per step: two independent dependency chains feed the same accumulators; the point
+  // records of the next DABA_PFS steps are in flight (registers)
+#ifndef DABA_PFS
+#define DABA_PFS 1
+#endif
+  constexpr int PS = DABA_PFS;
+  double4 lq[2 * PS];
+#pragma unroll
+  for (int r = 0; r < 2 * PS; ++r) lq[r] = r < n ? ld256(L + sidx[tid + r * kCamPassThreads]) : make_double4(0, 0, 0, 0);
   issue(kRing - 1);
 #pragma unroll 1
-  for (int k = 0; k < n; k += 2) {
-    const double4 l0 = la, l1 = lb;
-    if (k + 2 < n) la = ld256(L + sidx[tid + (k + 2) * kCamPassThreads]);
-    if (k + 3 < n) lb = ld256(L + sidx[tid + (k + 3) * kCamPassThreads]);
-    cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
-    const double2 u0 = *uslot(k);
-    const double2 u1 = *uslot(k + 1);
-    issue(k + kRing);  // refills the two slots just read
-    issue(k + kRing + 1);
-    cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
-    if (k + 1 < n) cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, ch.o0 + tid + (int64_t)(k + 1) * kCamPassThreads);
+  for (int k0 = 0; k0 < n; k0 += 2 * PS) {
+#pragma unroll
+    for (int h = 0; h < PS; ++h) {
+      const int k = k0 + 2 * h;
+      if (k < n) {
+        const double4 l0 = lq[2 * h], l1 = lq[2 * h + 1];
+        if (k + 2 * PS < n) lq[2 * h] = ld256(L + sidx[tid + (k + 2 * PS) * kCamPassThreads]);
+        if (k + 2 * PS + 1 < n) lq[2 * h + 1] = ld256(L + sidx[tid + (k + 2 * PS + 1) * kCamPassThreads]);
+        cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
+        const double2 u0 = *uslot(k);
+        const double2 u1 = *uslot(k + 1);
+        issue(k + kRing);  // refills the two slots just read
+        issue(k + kRing + 1);
+        cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+        if (k + 1 < n)
+          cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, ch.o0 + tid + (int64_t)(k + 1) * kCamPassThreads);
+      }
+    }
   }
 #else
   double4 lnext = make_double4(0, 0, 0, 0);
