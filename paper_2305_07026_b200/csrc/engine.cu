@@ -427,11 +427,14 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     std::vector<CamChunk> chunks;
     std::vector<int32_t> cptr(1, 0);
     for (int32_t i = 0; i < S.n_own_cams; ++i) {
-      for (int64_t o0 = S.cam_ptr[(size_t)i]; o0 < S.cam_ptr[(size_t)i + 1]; o0 += kCamChunkObs) {
+      // balanced chunks: a camera's observations split into equal parts of at most kCamChunkObs
+      const int64_t b = S.cam_ptr[(size_t)i], e = S.cam_ptr[(size_t)i + 1];
+      const int64_t parts = (e - b + kCamChunkObs - 1) / kCamChunkObs;
+      for (int64_t q = 0; q < parts; ++q) {
         CamChunk ch;
         ch.cam = i;
-        ch.o0 = o0;
-        ch.n = (int32_t)std::min<int64_t>(kCamChunkObs, S.cam_ptr[(size_t)i + 1] - o0);
+        ch.o0 = b + (e - b) * q / parts;
+        ch.n = (int32_t)(b + (e - b) * (q + 1) / parts - ch.o0);
         chunks.push_back(ch);
       }
       cptr.push_back((int32_t)chunks.size());

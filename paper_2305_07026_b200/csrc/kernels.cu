@@ -233,7 +233,10 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   const double4* __restrict__ L = ACC ? p.lbar[p.roles[4]] : p.pts[p.roles[1]];
   const int tid = threadIdx.x;
   const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
-  for (int o = tid; o < ch.n; o += kCamPassThreads) sidx[o] = __ldg(p.c_pt + ch.o0 + o);
+  // stage the chunk's point indices: every 4-byte copy in flight at once (cp.async), one wait
+  for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(sidx + o, p.c_pt + ch.o0 + o);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   auto uslot = [&](int k) { return ring + (k & (kRing - 1)) * kCamPassThreads + tid; };
   auto issue = [&](int k) {

@@ -11,7 +11,10 @@ constexpr int kCamStride = 16;
 constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camera moments"
 constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
 constexpr int kCamPassThreads = 128;
-constexpr int kCamChunkObs = 128 * 16;  // observations per camera-pass chunk (one CTA)
+#ifndef DABA_CHUNK
+#define DABA_CHUNK 4096
+#endif
+constexpr int kCamChunkObs = DABA_CHUNK;  // max observations per camera-pass chunk (one CTA)
 constexpr int kPtPassThreads = 256;     // point solve: threads (points) per CTA
 constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
