@@ -92,6 +92,21 @@ class NcclComm : public Comm {
     if (r != ncclSuccess) return nccl_err("ncclSend/Recv", r);
     return r2 == ncclSuccess ? "" : nccl_err("ncclGroupEnd", r2);
   }
+  std::string allreduce_exchange(const double* d_in, double* d_out, int n, const double* d_send, double* d_recv,
+                                 const std::vector<PeerSeg>& segs, cudaStream_t st) override {
+    ncclResult_t r = nccl().GroupStart();
+    if (r != ncclSuccess) return nccl_err("ncclGroupStart", r);
+    r = nccl().AllReduce(d_in, d_out, (size_t)n, ncclFloat64, ncclSum, comm, st);
+    for (const PeerSeg& s : segs) {
+      if (r != ncclSuccess) break;
+      if (s.send_cnt > 0) r = nccl().Send(d_send + s.send_off, (size_t)s.send_cnt, ncclFloat64, s.rank, comm, st);
+      if (r == ncclSuccess && s.recv_cnt > 0)
+        r = nccl().Recv(d_recv + s.recv_off, (size_t)s.recv_cnt, ncclFloat64, s.rank, comm, st);
+    }
+    ncclResult_t r2 = nccl().GroupEnd();
+    if (r != ncclSuccess) return nccl_err("ncclAllReduce/Send/Recv", r);
+    return r2 == ncclSuccess ? "" : nccl_err("ncclGroupEnd", r2);
+  }
   bool capturable() const override { return true; }
 };
 

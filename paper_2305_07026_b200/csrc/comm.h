@@ -27,6 +27,13 @@ class Comm {
   virtual std::string allreduce(const double* d_in, double* d_out, int n, cudaStream_t st) = 0;
   virtual std::string exchange(const double* d_send, double* d_recv, const std::vector<PeerSeg>& segs,
                                cudaStream_t st) = 0;
+  // the allreduce and the exchange issued together (one NCCL group: the transfers overlap)
+  virtual std::string allreduce_exchange(const double* d_in, double* d_out, int n, const double* d_send,
+                                         double* d_recv, const std::vector<PeerSeg>& segs, cudaStream_t st) {
+    std::string e = allreduce(d_in, d_out, n, st);
+    if (!e.empty() || segs.empty()) return e;
+    return exchange(d_send, d_recv, segs, st);
+  }
   virtual bool capturable() const = 0;
 };
 

@@ -205,23 +205,9 @@ void collect_times(daba_ctx* c) {
   c->pending.clear();
 }
 
-int exchange_halo(daba_ctx* c, int* launches) {
-  if (c->segs.empty()) return DABA_OK;
-  int n = timed(c, "k_pack", [&] {
-    return launch_pack(c->P, c->d_send_cam, c->d_send_cam_off, c->n_send_cam, c->d_send_pt, c->d_send_pt_off,
-                       c->n_send_pt, c->d_sendbuf, c->stream);
-  });
-  std::string e = c->comm->exchange(c->d_sendbuf, c->d_recvbuf, c->segs, c->stream);
-  if (!e.empty()) return fail(c, DABA_E_NCCL, e);
-  n += timed(c, "k_unpack", [&] {
-    return launch_unpack(c->P, c->d_recv_cam, c->d_recv_cam_off, c->n_recv_cam, c->d_recv_pt, c->d_recv_pt_off,
-                         c->n_recv_pt, c->d_recvbuf, c->stream);
-  });
-  *launches += n;
-  return DABA_OK;
-}
-
-// Enqueue one iteration of Algorithm 1.
+// Enqueue one iteration of Algorithm 1.  With a communicator, both candidates of every boundary variable are
+// packed as soon as they exist and exchanged in the same NCCL group as the allreduce of the restart sums (the two
+// transfers overlap); after the restart decision the unpack keeps the selected candidate.
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
@@ -230,13 +216,23 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
   n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
   if (c->comm) {
-    std::string e = c->comm->allreduce(P.local, P.global, kGlobalCols, c->stream);
+    const bool halo = !c->segs.empty();
+    if (halo)
+      n += timed(c, "k_pack", [&] {
+        return launch_pack(P, c->d_send_cam, c->d_send_cam_off, c->n_send_cam, c->d_send_pt, c->d_send_pt_off,
+                           c->n_send_pt, c->d_sendbuf, c->stream);
+      });
+    std::string e = c->comm->allreduce_exchange(P.local, P.global, kGlobalCols, c->d_sendbuf, c->d_recvbuf,
+                                                halo ? c->segs : std::vector<PeerSeg>(), c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
     n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
+    if (halo)
+      n += timed(c, "k_unpack", [&] {
+        return launch_unpack(P, c->d_recv_cam, c->d_recv_cam_off, c->n_recv_cam, c->d_recv_pt, c->d_recv_pt_off,
+                             c->n_recv_pt, c->d_recvbuf, c->stream);
+      });
   }
   *launches += n;
-  int rc = exchange_halo(c, launches);
-  if (rc) return rc;
   CUDA_OR(c, cudaGetLastError());
   return DABA_OK;
 }
@@ -510,24 +506,24 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       PeerSeg sg;
       sg.rank = pe.rank;
       sg.send_off = soff;
-      sg.send_cnt = 15 * (int64_t)pe.send_cams.size() + 3 * (int64_t)pe.send_pts.size();
+      sg.send_cnt = 30 * (int64_t)pe.send_cams.size() + 6 * (int64_t)pe.send_pts.size();  // both candidates
       sg.recv_off = roff;
-      sg.recv_cnt = 15 * (int64_t)pe.recv_cams.size() + 3 * (int64_t)pe.recv_pts.size();
+      sg.recv_cnt = 30 * (int64_t)pe.recv_cams.size() + 6 * (int64_t)pe.recv_pts.size();
       for (size_t q = 0; q < pe.send_cams.size(); ++q) {
         sc.push_back(pe.send_cams[q]);
-        sco.push_back(soff + 15 * (int64_t)q);
+        sco.push_back(soff + 30 * (int64_t)q);
       }
       for (size_t q = 0; q < pe.send_pts.size(); ++q) {
         sp.push_back(pe.send_pts[q]);
-        spo.push_back(soff + 15 * (int64_t)pe.send_cams.size() + 3 * (int64_t)q);
+        spo.push_back(soff + 30 * (int64_t)pe.send_cams.size() + 6 * (int64_t)q);
       }
       for (size_t q = 0; q < pe.recv_cams.size(); ++q) {
         rcm.push_back(pe.recv_cams[q]);
-        rco.push_back(roff + 15 * (int64_t)q);
+        rco.push_back(roff + 30 * (int64_t)q);
       }
       for (size_t q = 0; q < pe.recv_pts.size(); ++q) {
         rpt.push_back(pe.recv_pts[q]);
-        rpo.push_back(roff + 15 * (int64_t)pe.recv_cams.size() + 3 * (int64_t)q);
+        rpo.push_back(roff + 30 * (int64_t)pe.recv_cams.size() + 6 * (int64_t)q);
       }
       soff += sg.send_cnt;
       roff += sg.recv_cnt;
@@ -760,7 +756,7 @@ extern "C" int daba_shard_info(daba_ctx* ctx, int64_t info[8]) {
   info[3] = (int64_t)S.pt_g.size() - S.n_own_pts;
   info[4] = (int64_t)S.c_obs.size();
   info[5] = (int64_t)S.p_obs.size();
-  info[6] = 8 * S.send_doubles;
+  info[6] = 16 * S.send_doubles;  // both candidates of each boundary variable, 8 B each
   info[7] = (int64_t)ctx->dev_bytes;
   return DABA_OK;
 }

@@ -905,36 +905,47 @@ __global__ void k_lbar_all(IterParams p) {
 }
 
 // ------------------------------------------------------------------ halo pack / unpack (x^k)
+// Both candidates of each boundary variable (before the restart decision): camera [acc 15 | mm 15],
+// point [acc 3 | mm 3].
 __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                        const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_cam) {
-    const double* c = p.cams[p.roles[1]] + (size_t)cam_idx[t] * kCamStride;
+    const double* ca = p.cams[p.roles[2]] + (size_t)cam_idx[t] * kCamStride;
+    const double* cm = p.cams[p.roles[3]] + (size_t)cam_idx[t] * kCamStride;
     double* b = buf + cam_off[t];
-    for (int k = 0; k < 15; ++k) b[k] = c[k];
+    for (int k = 0; k < 15; ++k) b[k] = ca[k];
+    for (int k = 0; k < 15; ++k) b[15 + k] = cm[k];
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
-    const double4 l = p.pts[p.roles[1]][pt_idx[q]];
+    const double4 la = p.pts[p.roles[2]][pt_idx[q]], lm = p.pts[p.roles[3]][pt_idx[q]];
     double* b = buf + pt_off[q];
-    b[0] = l.x;
-    b[1] = l.y;
-    b[2] = l.z;
+    b[0] = la.x;
+    b[1] = la.y;
+    b[2] = la.z;
+    b[3] = lm.x;
+    b[4] = lm.y;
+    b[5] = lm.z;
   }
 }
 
+// After the restart decision (roles rotated, roles[4] = 1 iff the MM candidate was kept): the selected candidate
+// becomes the halo entry of x^{k+1}, and its x-bar^{k+1} is formed from the cached x^k (eqs. nesterov_x).
 __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                          const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
+  const int sel = p.roles[4];
   if (t < n_cam) {
     const size_t i = (size_t)cam_idx[t] * kCamStride;
     double* c = p.cams[p.roles[1]] + i;
-    for (int k = 0; k < 15; ++k) c[k] = buf[cam_off[t] + k];
+    const double* src = buf + cam_off[t] + 15 * sel;
+    for (int k = 0; k < 15; ++k) c[k] = src[k];
     c[15] = 0.0;
     extrapolate_camera(c, p.cams[p.roles[0]] + i, gamma, p.cbarb[p.roles[4]] + i);
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
-    const double* b = buf + pt_off[q];
+    const double* b = buf + pt_off[q] + 3 * sel;
     const double4 lp = p.pts[p.roles[0]][pt_idx[q]];
     p.pts[p.roles[1]][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);
     p.lbar[p.roles[4]][pt_idx[q]] = make_double4(fma(gamma, b[0] - lp.x, b[0]), fma(gamma, b[1] - lp.y, b[1]),
