@@ -56,18 +56,16 @@ __device__ __forceinline__ double det3(const double* A) {
 __device__ __forceinline__ void expm_minus_identity(const double* w, double* E) {
   const double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
   double a, b;
-  if (th2 < 1e-16) {
-    a = 1.0 - th2 * (1.0 / 6.0);
-    b = 0.5 - th2 * (1.0 / 24.0);
+  if (th2 < 1e-4) {
+    // |th| < 1e-2 (LM steps): Taylor series of sin(th)/th and (1 - cos th)/th^2, truncation < 1e-20 relative
+    a = 1.0 + th2 * (-1.0 / 6.0 + th2 * (1.0 / 120.0 + th2 * (-1.0 / 5040.0 + th2 * (1.0 / 362880.0))));
+    b = 0.5 + th2 * (-1.0 / 24.0 + th2 * (1.0 / 720.0 + th2 * (-1.0 / 40320.0 + th2 * (1.0 / 3628800.0))));
   } else {
     const double th = sqrt(th2);
-    double sn, cs;
-    sincos(th, &sn, &cs);
-    a = sn / th;
+    a = sin(th) / th;
     // 1 - cos(th) = 2 sin^2(th/2), no cancellation
     const double sh = sin(0.5 * th);
     b = 2.0 * sh * sh / th2;
-    (void)cs;
   }
   const double x = w[0], y = w[1], z = w[2];
   // a [w]x + b [w]x^2,  [w]x^2 = w w^T - th2 I

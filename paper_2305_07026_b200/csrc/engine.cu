@@ -25,7 +25,8 @@ using namespace daba;
 struct daba_ctx {
   std::string err;
   int device = 0, rank = 0, nranks = 1;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr, side = nullptr;  // side: the k_cam_solve branch of an iteration
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool own_stream = false;
   daba_options opt{};
   daba_loss loss{};
@@ -213,8 +214,18 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   int n = 0;
   n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
   n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
-  n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
-  n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
+  if (c->opt.profile) {  // serialised, so that each kernel's events bracket only that kernel
+    n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
+    n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
+  } else {
+    // k_cam_solve and k_pt_sum are independent: fork a second stream (captured as parallel graph branches)
+    CUDA_OR(c, cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_OR(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    n += launch_cam_solve(P, c->side);
+    CUDA_OR(c, cudaEventRecord(c->ev_join, c->side));
+    n += launch_pt_sum(P, c->stream);
+    CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
   if (c->comm) {
     const bool halo = !c->segs.empty();
     if (halo)
@@ -360,6 +371,12 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   } else {
     if (cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking) != cudaSuccess) return DABA_E_CUDA;
     C->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&C->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    daba_destroy(c.release());
+    return DABA_E_CUDA;
   }
   if (nranks > 1 || comm_id) {  // a single rank with a comm id still routes its sums through the communicator
     std::string ce;
@@ -803,5 +820,8 @@ extern "C" void daba_destroy(daba_ctx* ctx) {
   ctx->comm.reset();
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }

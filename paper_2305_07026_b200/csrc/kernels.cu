@@ -31,13 +31,22 @@ __device__ __forceinline__ double sched_gamma(double s, int accelerate, double* 
 }
 
 // 256-bit global access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): one instruction per 32-byte record.
+#ifdef DABA_STRICT_ASM
+#define DABA_LD_ASM asm volatile
+#define DABA_ST_CLOBBER : "memory"
+#else
+#define DABA_LD_ASM asm
+#define DABA_ST_CLOBBER
+#endif
 __device__ __forceinline__ double4 ld256(const double4* q) {
   double4 v;
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
+  DABA_LD_ASM("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
   return v;
 }
+// plain store of a record nobody reads in the same kernel: no memory clobber, so the scheduler may move loads
+// across it
 __device__ __forceinline__ void st256(double4* q, double4 v) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) DABA_ST_CLOBBER);
 }
 
 // Point record: 32 bytes (x, y, z, pad) — one sector per gather.
@@ -477,12 +486,13 @@ __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
 __device__ void do_select(const IterParams& p);
 
 // Rank-local sums of the camera partials (k_cam_solve blocks, 8 columns) and point partials (k_pt_sum blocks,
-// 4 columns) in a fixed order by one 256-thread block -> p.local (a9).
-__device__ void final_reduce(const IterParams& p, int n_pt_parts) {
+// 4 columns) in a fixed order by one block (any power-of-two size <= 256) -> p.local (a9).
+__device__ void final_reduce(const IterParams& p) {
   __shared__ double s[kGlobalCols][256];
+  const int nt = blockDim.x;
   double v[kGlobalCols];
   for (int c = 0; c < kGlobalCols; ++c) v[c] = 0.0;
-  for (int b = threadIdx.x; b < p.n_cam_eval_blocks; b += 256) {
+  for (int b = threadIdx.x; b < p.n_cam_eval_blocks; b += nt) {
     const double* q = p.cam_part + (size_t)b * kCamEvalCols;
     v[0] += __ldcg(q + 0);
     v[1] += __ldcg(q + 1);
@@ -493,7 +503,7 @@ __device__ void final_reduce(const IterParams& p, int n_pt_parts) {
     v[8] += __ldcg(q + 6);
     v[9] += __ldcg(q + 7);
   }
-  for (int b = threadIdx.x; b < n_pt_parts; b += 256) {
+  for (int b = threadIdx.x; b < p.n_pt_blocks; b += nt) {
     const double* q = p.pt_part + (size_t)b * kPtCols;
     v[2] += __ldcg(q + 0);
     v[4] += __ldcg(q + 1);
@@ -502,12 +512,31 @@ __device__ void final_reduce(const IterParams& p, int n_pt_parts) {
   }
   for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
   __syncthreads();
-  for (int st = 128; st > 0; st >>= 1) {
+  for (int st = nt / 2; st > 0; st >>= 1) {
     if (threadIdx.x < st)
       for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + st];
     __syncthreads();
   }
   if (threadIdx.x < kGlobalCols) p.local[threadIdx.x] = s[threadIdx.x][0];
+}
+
+// Epilogue of every k_cam_solve and k_pt_sum block (the two kernels may run concurrently): after its partial is
+// written, the block that finishes last (across both kernels) forms the rank-local sums and, without a
+// communicator, takes the restart decision.
+__device__ void finish_block(const IterParams& p) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == p.n_cam_eval_blocks + p.n_pt_blocks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  final_reduce(p);
+  if (threadIdx.x == 0) {
+    *p.counter = 0;
+    __threadfence();
+    if (!p.has_comm) do_select(p);
+  }
 }
 
 // Point solve (a7) over a grid-stride set of owned points: each point adds its observations' records in
@@ -548,7 +577,6 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   }
   // block sums: warp shuffles, then one shared-memory step (deterministic order)
   __shared__ double ws[kPtPassThreads / 32][kPtCols];
-  __shared__ bool last;
 #pragma unroll
   for (int c = 0; c < kPtCols; ++c) {
     double v = qv[c];
@@ -562,18 +590,7 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
     for (int w = 0; w < kPtPassThreads / 32; ++w) v += ws[w][threadIdx.x];
     p.pt_part[(size_t)blockIdx.x * kPtCols + threadIdx.x] = v;
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  final_reduce(p, gridDim.x);
-  if (threadIdx.x == 0) {
-    *p.counter = 0;
-    __threadfence();
-    if (!p.has_comm) do_select(p);
-  }
+  finish_block(p);
 }
 
 // ------------------------------------------------------------------ a6: camera solve
@@ -850,6 +867,7 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
     __syncthreads();
   }
   if (threadIdx.x < kCamEvalCols) p.cam_part[(size_t)blockIdx.x * kCamEvalCols + threadIdx.x] = sq[threadIdx.x][0];
+  finish_block(p);
 }
 
 // ------------------------------------------------------------------ a9 + a10: restart test and selection
