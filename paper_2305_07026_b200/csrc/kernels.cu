@@ -120,7 +120,8 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
   if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
     acc[40] += 1.0;
-    st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec, make_double4(0.0, 0.0, 0.0, 0.0));
+    if (rec >= 0)
+      st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec, make_double4(0.0, 0.0, 0.0, 0.0));
     return;
   }
   // camera-frame point R^T (l - t)
@@ -202,8 +203,9 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   const double gx = fma(c[0], ex, fma(c[1], ey, c[2] * ez));
   const double gy = fma(c[3], ex, fma(c[4], ey, c[5] * ez));
   const double gz = fma(c[6], ex, fma(c[7], ey, c[8] * ez));
-  st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec,
-        make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
+  if (rec >= 0)
+    st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec,
+          make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
 #ifdef DABA_NOEMIT
   }
 #endif
@@ -244,6 +246,13 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
   // stage the chunk's point indices: every 4-byte copy in flight at once (cp.async), one wait
   for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(sidx + o, p.c_pt + ch.o0 + o);
+#ifdef DABA_PTMAJOR
+  int32_t* srec = sidx + kCamChunkObs;  // record (point-major position) of each observation
+  for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(srec + o, p.c_rec + ch.o0 + o);
+#define REC(kk) (int64_t) srec[tid + (kk) * kCamPassThreads]
+#else
+#define REC(kk) (ch.o0 + tid + (int64_t)(kk) * kCamPassThreads)
+#endif
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
@@ -279,9 +288,9 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
         const double2 u1 = *uslot(k + 1);
         issue(k + kRing);  // refills the two slots just read
         issue(k + kRing + 1);
-        cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+        cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, REC(k));
         if (k + 1 < n)
-          cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, ch.o0 + tid + (int64_t)(k + 1) * kCamPassThreads);
+          cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, REC(k + 1));
       }
     }
   }
@@ -295,7 +304,7 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
     issue(k + kRing - 1);
     cp_async_wait<kRing - 1>();
     const double2 u = *uslot(k);
-    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, ch.o0 + tid + (int64_t)k * kCamPassThreads);
+    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, REC(k));
   }
 #endif
   cp_async_wait<0>();
@@ -325,7 +334,11 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, d
   }
 }
 
+#ifdef DABA_PTMAJOR
+constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs;  // ring + indices + records
+#else
 constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs / 2;  // ring + indices
+#endif
 constexpr int kCamSmemDoubles =
     kCamRingDoubles > 4 * 32 * kPartialStride ? kCamRingDoubles : 4 * 32 * kPartialStride;
 
@@ -478,7 +491,11 @@ __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
   double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   pt_terms<LOSS>(p.cbarb[p.roles[4]] + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
   pt_terms<LOSS>(p.cams[p.roles[1]] + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
+#ifdef DABA_PTMAJOR
+  const int64_t r = p.b_rec[b];
+#else
   const int64_t r = p.n_cam_side + b;
+#endif
   reinterpret_cast<double4*>(p.staging)[r] = make_double4(a[0], a[1], a[2], a[3]);
   reinterpret_cast<double4*>(p.staging + 4 * p.n_records)[r] = make_double4(a[4], a[5], a[6], a[7]);
 }
@@ -555,7 +572,11 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
     for (int64_t o = p.p_ptr[j]; o < o1; o += 4) {  // up to 4 records (8 x 32 B) in flight per thread
       int32_t r[4];
 #pragma unroll
+#ifdef DABA_PTMAJOR
+      for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? (int32_t)(o + i) : -1;
+#else
       for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? p.p_src[o + i] : -1;
+#endif
       double4 A[4], B[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
