@@ -290,3 +290,49 @@ def test_nccl_transport_single_rank():
         np.testing.assert_array_equal(ta, tb)
         assert a.objective() == b.objective()
         np.testing.assert_array_equal(a.state_native(0)[0], b.state_native(0)[0])
+
+
+def test_random_ownership_four_ranks():
+    """Irregular partition (random camera and point owners over 4 ranks: every rank talks to every other, many
+    boundary observations recomputed from halo cameras) gives the 1-rank iterates (reading D1)."""
+    p = gen.generate("small_cauchy")
+    rng = np.random.default_rng(11)
+    cam_owner = rng.integers(0, 4, p.M).astype(np.int32)
+    pt_owner = rng.integers(0, 4, p.N).astype(np.int32)
+    with solver(p) as s:
+        t1 = s.iterate_trace(15)
+        c1, l1, _ = s.state_native(0)
+    key = rng.bytes(128)
+    out = [None] * 4
+    err = []
+
+    def work(r):
+        try:
+            with solver(p, rank=r, nranks=4, comm_key=key, comm=D.COMM_LOCAL, cam_owner=cam_owner,
+                        pt_owner=pt_owner) as sr:
+                out[r] = (sr.iterate_trace(15), *sr.state_native(0), sr.shard_info())
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(4)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not err, err
+    cams, pts = np.full((p.M, 15), np.nan), np.full((p.N, 3), np.nan)
+    for tr, c, l, mask, info in out:
+        cams[mask[:p.M] == 1] = c[mask[:p.M] == 1]
+        pts[mask[p.M:] == 1] = l[mask[p.M:] == 1]
+        assert info["halo_cams"] > 0 and info["halo_pts"] > 0 and info["send_bytes_per_iter"] > 0
+    assert np.abs(out[0][0][:, 0] - t1[:, 0]).max() <= 1e-13 * t1[0, 0]
+    np.testing.assert_array_equal(out[0][0][:, D.daba.TR_RESTART], t1[:, D.daba.TR_RESTART])
+    assert max(state_errors(cams, pts, c1, l1)) <= 1e-12
+
+
+def test_shuffled_point_ids():
+    # worst-case gather order (random point numbering): same parity bar
+    p = gen.generate("small_huber", shuffle_points=True)
+    o = oracle_for(p)
+    tro = o.iterate(20)
+    with solver(p) as s:
+        trg = s.iterate_trace(20)
+        assert (np.abs(trg[:, 0] - tro[:, 0]) / tro[:, 0]).max() <= F_TOL
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
