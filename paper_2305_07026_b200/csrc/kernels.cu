@@ -106,7 +106,7 @@ struct CamRegs {
 #define DABA_RING 8
 #endif
 #ifndef DABA_MINB
-#define DABA_MINB 3
+#define DABA_MINB (384 / DABA_CPT)  // 12 warps per SM: the 170-register budget of the moment accumulators
 #endif
 
 // One observation's contribution to the camera moments at one anchor.
@@ -313,7 +313,7 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
 // Deterministic block reduction of kPartialStride doubles per thread (128 threads) via shared-memory transposes.
 __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, double* smem) {
   double(*red)[32][kPartialStride] = reinterpret_cast<double(*)[32][kPartialStride]>(smem);
-  __shared__ double wsum[4][kPartialStride];
+  __shared__ double wsum[kCamWarps][kPartialStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < kPartialStride; ++k) red[warp][lane][k] = acc[k];
@@ -330,7 +330,12 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, d
   __syncthreads();
   if (threadIdx.x < kPartialStride) {
     const int k = threadIdx.x;
-    out[k] = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
+    if (kCamWarps == 4)
+      out[k] = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
+    else if (kCamWarps == 2)
+      out[k] = wsum[0][k] + wsum[1][k];
+    else
+      out[k] = wsum[0][k];
   }
 }
 
@@ -340,7 +345,7 @@ constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs;  // 
 constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs / 2;  // ring + indices
 #endif
 constexpr int kCamSmemDoubles =
-    kCamRingDoubles > 4 * 32 * kPartialStride ? kCamRingDoubles : 4 * 32 * kPartialStride;
+    kCamRingDoubles > kCamPassThreads * kPartialStride ? kCamRingDoubles : kCamPassThreads * kPartialStride;
 
 template <int LOSS>
 __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterParams p) {

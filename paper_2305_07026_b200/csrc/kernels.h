@@ -10,7 +10,11 @@ namespace daba {
 constexpr int kCamStride = 16;
 constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camera moments"
 constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
-constexpr int kCamPassThreads = 128;
+#ifndef DABA_CPT
+#define DABA_CPT 64  // measured on Final-13682: 64 -> 0.758 ms, 128 -> 0.843 ms, 32 -> 1.18 ms (k_cam_pass)
+#endif
+constexpr int kCamPassThreads = DABA_CPT;  // 32, 64 or 128 threads per camera-pass CTA
+constexpr int kCamWarps = kCamPassThreads / 32;
 #ifndef DABA_CHUNK
 #define DABA_CHUNK 4096
 #endif
