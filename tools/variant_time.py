@@ -16,3 +16,17 @@ s.iterate(n)
 kt = s.kernel_times()
 tot = sum(v[0] for v in kt.values()) / n
 print(os.environ.get("DABA_LIB", "default"), f"total {tot:.4f} ms/iter", {k: round(v[0] / n, 4) for k, v in kt.items()})
+s.close()
+# graph-replayed iterations (production path), wall clock around n iterations minus one objective evaluation
+import time  # noqa: E402
+g = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, loss=p.loss)
+g.iterate(3)
+g.objective()
+t0 = time.perf_counter()
+g.objective()
+t_obj = time.perf_counter() - t0
+t0 = time.perf_counter()
+g.iterate(n)
+g.objective()
+dt = time.perf_counter() - t0 - t_obj
+print(os.environ.get("DABA_LIB", "default"), f"graph {1e3 * dt / n:.4f} ms/iter")
