@@ -277,9 +277,10 @@ def main():
     roof = None
     kbytes = {k: f(info["cam_side_obs"] if k == "k_cam_pass" else info["pt_side_obs"],
                    info["own_pts"] + info["halo_pts"], info["own_cams"]) for k, f in BYTES.items()}
-    traffic = None
+    traffic, fp64_pipe = None, None
     try:
-        traffic = json.load(open(TRAFFIC)).get(dname, {}).get("dram_bytes_per_launch")
+        tj = json.load(open(TRAFFIC)).get(dname, {})
+        traffic, fp64_pipe = tj.get("dram_bytes_per_launch"), tj.get("fp64_pipe_pct")
     except Exception:
         pass
     if dname in BYTES:
@@ -288,7 +289,8 @@ def main():
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "traffic": traffic, "kernel": dname, "bytes_per_launch": int(byt),
                 "kernel_ms_per_launch": round(per_launch_ms, 5), "peak_source": hbm_src,
-                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None}
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None,
+                "fp64_pipe_pct_ncu": fp64_pipe}
         # whole iteration: algorithmic bytes of both passes over the device-timed step
         tot_b = sum(kbytes.values())
         roof["iteration"] = {"bytes": int(tot_b), "achieved": round(tot_b / (ms / a.steps * 1e-3) / 1e9, 1),

@@ -19,9 +19,12 @@ for d in data:
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         b += float(d[ix[k]]) * scale.get(units[ix[k]], 1)
     t = float(d[ix["gpu__time_duration.sum"]]) * (1e-3 if units[ix["gpu__time_duration.sum"]] == "us" else 1)
-    res.setdefault(name, []).append({"dram_bytes": b, "ms": t})
+    f64 = float(d[ix["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]]) \
+        if "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active" in ix else None
+    res.setdefault(name, []).append({"dram_bytes": b, "ms": t, "fp64": f64})
 summary = {k: {"dram_bytes_per_launch": sum(x["dram_bytes"] for x in v) / len(v),
-               "ms_per_launch_ncu": sum(x["ms"] for x in v) / len(v), "launches_captured": len(v)}
+               "ms_per_launch_ncu": sum(x["ms"] for x in v) / len(v), "launches_captured": len(v),
+               "fp64_pipe_pct": v[0]["fp64"]}
            for k, v in res.items()}
 summary["_source"] = rep
 json.dump(summary, open(out, "w"), indent=1)
