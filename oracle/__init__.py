@@ -29,6 +29,9 @@ class Options(ctypes.Structure):
                 ("accelerate", ctypes.c_int), ("kind", ctypes.c_int), ("scale", ctypes.c_double)]
 
 
+DEV_F, DEV_FBAR, DEV_EACC, DEV_EMM, DEV_RESTART, DEV_COLS = range(6)
+
+
 def options(loss=LOSS_TRIVIAL, scale=1.0, xi=1e-4, eta=0.1, mu0=1e-3, mu_up=10.0, eps=1e-8, trials=5, accelerate=1):
     """Defaults are SURVEY.md D7 / DESIGN.md readings Q3, Q6, Q8, Q9."""
     return Options(xi, eta, mu0, mu_up, eps, trials, accelerate, loss, scale)
@@ -61,6 +64,8 @@ def lib():
         L.orc_candidates.argtypes = [V, ctypes.c_int64, V, V, V, ctypes.c_int64, V, V, V]
         L.orc_destroy.argtypes = [V]
         L.orc_destroy.restype = None
+        L.orc_set_devices.argtypes = [V, ctypes.c_int, V, V]
+        L.orc_device_metrics.argtypes = [V, V]
         L.orc_ray.argtypes = [V, V, V]
         L.orc_ray.restype = None
         L.orc_optimal_scale.argtypes = [V, V, V, V, ctypes.c_double, _dp]
@@ -269,6 +274,22 @@ class Oracle:
         if rc:
             raise ValueError("orc_candidates failed")
         return ca, cm, pa, pm
+
+    def set_devices(self, cam_dev, pt_dev):
+        """Decentralized adaptive restart (§5, eqs. DEalpha-Eak): device ownership of every camera and
+        point; each device then takes the restart decision for its own variables.  Before the first iterate."""
+        cd = np.ascontiguousarray(cam_dev, np.int32)
+        pd = np.ascontiguousarray(pt_dev, np.int32)
+        self.ndev = int(max(cd.max(initial=0), pd.max(initial=0))) + 1
+        if lib().orc_set_devices(self.h, self.ndev, cd.ctypes.data, pd.ctypes.data) != 0:
+            raise ValueError("orc_set_devices failed")
+
+    def device_metrics(self):
+        """Last iteration, per device: F^a(k), F-bar^a(k), E^a_acc(k+1), E^a_mm(k+1), restart^a."""
+        out = np.zeros((self.ndev, DEV_COLS))
+        if lib().orc_device_metrics(self.h, out.ctypes.data) != 0:
+            raise ValueError("no device metrics")
+        return out
 
     def close(self):
         if self.h:

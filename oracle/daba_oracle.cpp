@@ -256,6 +256,30 @@ double point_decrease(const double* l_hat, const double* l, const std::vector<Co
   return sum + 0.5 * o->xi * dot3(dl, dl);
 }
 
+// Per-pair anchor-relative changes of P_ij and Q_ij (eq. P, eq. Q expanded around the anchor, Q21), without
+// the proximal term: P_ij(c|x_hat) - P_ij(c_hat|x_hat) = w dr.(dr + R_hat e),
+// Q_ij(l|x_hat) - Q_ij(l_hat|x_hat) = w (lambda dl).(lambda dl - R_hat e).
+double pair_dP(const double* anchor, const double* cam, const Coef& c, const double* u) {
+  if (c.degenerate) return 0.0;
+  double p2[3], Rp2[3], Rph[3], dr[3];
+  orc_ray(cam + 12, u, p2);
+  mat_vec(cam, p2, Rp2);
+  mat_vec(anchor, c.p, Rph);
+  for (int r = 0; r < 3; ++r) dr[r] = (Rp2[r] - Rph[r]) + c.lambda * (cam[9 + r] - anchor[9 + r]);
+  double q = 0;
+  for (int r = 0; r < 3; ++r) q += dr[r] * (dr[r] + c.Re[r]);
+  return c.w * q;
+}
+double pair_dQ(const double* l_hat, const double* l, const Coef& c) {
+  if (c.degenerate) return 0.0;
+  double q = 0;
+  for (int r = 0; r < 3; ++r) {
+    const double x = c.lambda * (l[r] - l_hat[r]);
+    q += x * (x - c.Re[r]);
+  }
+  return c.w * q;
+}
+
 }  // namespace
 
 // ================================================================ geometry (§3)
@@ -541,7 +565,17 @@ struct orc_ctx {
   std::vector<double> cam, cam_prev, pt, pt_prev;          // x^k, x^{k-1}
   double s = 1.0, Fbar = 0.0;                              // s^{(k)}, F-bar^{(k-1)}
   std::vector<int32_t> trial_acc, trial_mm;
+  int64_t k = 0;                                           // iterations done
+  // decentralized adaptive restart (§5, eqs. DEalpha, Fainit, Fak, lFak, Eak)
+  int ndev = 0;                                            // 0: global restart test (D2)
+  std::vector<int32_t> cam_dev, pt_dev;
+  std::vector<double> dev_Fbar, dev_E;                     // F-bar^{alpha(k-1)}, E^{alpha(k)}
+  std::vector<double> dev_last;                            // last iteration: ndev x ORC_DEV_COLS
 };
+
+void device_restart(orc_ctx* h, const std::vector<double>& c_acc, const std::vector<double>& c_mm,
+                    const std::vector<double>& l_acc, const std::vector<double>& l_mm, std::vector<double>& cn,
+                    std::vector<double>& ln, double* Fbar_sum, double* Eacc_sum, double* Emm_sum, int* n_restart);
 
 namespace {
 
@@ -611,6 +645,157 @@ double objective(const orc_ctx* h, const double* cams, const double* pts, int64_
 }
 
 }  // namespace
+
+namespace {
+
+// eq. DEalpha at x = x^k with anchor x^{k-1}:
+//   Delta E^alpha(x^k | x^{k-1}) = -xi/2 ||x^{alpha(k)} - x^{alpha(k-1)}||^2
+//     + sum_{(i,j)} kappa^alpha_ij (F_ij(c_i^k, l_j^k) - P_ij(c_i^k | x^{k-1}) - Q_ij(l_j^k | x^{k-1})).
+// kappa = 1/2 for an inter-device pair touching alpha (the paper's E''_alpha).  Reading DN1: kappa = 1 for an
+// intra-device pair — under D1 those pairs are majorized too, so their surrogate gap is charged wholly to their
+// device (the paper keeps them exact, where the gap is 0).  With P_ij(c_hat|x_hat) = Q_ij(l_hat|x_hat) =
+// F_ij(x_hat)/2 (eqs. P, Q at the anchor, by eqs. a and g) each gap is
+//   F_ij(x^k) - F_ij(x^{k-1}) - dP_ij - dQ_ij    (anchor-relative changes, Q21).
+std::vector<double> device_delta_E(const orc_ctx* h) {
+  std::vector<Kahan> gap((size_t)h->ndev);
+  for (int64_t q = 0; q < h->K; ++q) {
+    const int32_t i = h->oc[(size_t)q], j = h->op[(size_t)q];
+    const double* u = &h->uv[(size_t)(2 * q)];
+    const Coef cp = coefficients(&h->cam_prev[(size_t)(15 * i)], &h->pt_prev[(size_t)(3 * j)], u, &h->o);
+    double Fk = 0;
+    if (orc_penalty(&h->cam[(size_t)(15 * i)], &h->pt[(size_t)(3 * j)], u, h->o.kind, h->o.scale, h->o.eps, &Fk) != 0)
+      Fk = 0;  // Q17
+    const double Fp = cp.degenerate ? 0.0 : 0.5 * cp.rho;  // eq. Fij at x^{k-1}
+    const double g = Fk - Fp - pair_dP(&h->cam_prev[(size_t)(15 * i)], &h->cam[(size_t)(15 * i)], cp, u) -
+                     pair_dQ(&h->pt_prev[(size_t)(3 * j)], &h->pt[(size_t)(3 * j)], cp);
+    const int a = h->cam_dev[(size_t)i], b = h->pt_dev[(size_t)j];
+    if (a == b) {
+      gap[(size_t)a].add(g);
+    } else {
+      gap[(size_t)a].add(0.5 * g);
+      gap[(size_t)b].add(0.5 * g);
+    }
+  }
+  std::vector<double> dE((size_t)h->ndev);
+  for (int a = 0; a < h->ndev; ++a) dE[(size_t)a] = gap[(size_t)a].s;
+  for (int64_t i = 0; i < h->M; ++i) {
+    double m = 0;
+    for (int r = 0; r < 15; ++r) {
+      const double x = h->cam[(size_t)(15 * i + r)] - h->cam_prev[(size_t)(15 * i + r)];
+      m += x * x;
+    }
+    dE[(size_t)h->cam_dev[(size_t)i]] -= 0.5 * h->o.xi * m;
+  }
+  for (int64_t j = 0; j < h->N; ++j) {
+    double m = 0;
+    for (int r = 0; r < 3; ++r) {
+      const double x = h->pt[(size_t)(3 * j + r)] - h->pt_prev[(size_t)(3 * j + r)];
+      m += x * x;
+    }
+    dE[(size_t)h->pt_dev[(size_t)j]] -= 0.5 * h->o.xi * m;
+  }
+  return dE;
+}
+
+}  // namespace
+
+// The decentralized restart of one iteration (Alg. 1 L416-420 on every device), after both candidates exist.
+void device_restart(orc_ctx* h, const std::vector<double>& c_acc, const std::vector<double>& c_mm,
+                    const std::vector<double>& l_acc, const std::vector<double>& l_mm, std::vector<double>& cn,
+                    std::vector<double>& ln, double* Fbar_sum, double* Eacc_sum, double* Emm_sum, int* n_restart) {
+  const int D = h->ndev;
+  const orc_options& o = h->o;
+  const std::vector<double> dE = device_delta_E(h);
+  // E^alpha(x^alpha | x^k) - E^alpha(x^{alpha(k)} | x^k) of both candidates: device alpha's camera and point
+  // surrogate decreases, proximal term included (eq. Ealpha restricted to alpha's variables, anchor-relative)
+  std::vector<Kahan> d_acc((size_t)D), d_mm((size_t)D);
+  std::vector<Coef> co;
+  std::vector<double> ul;
+  for (int64_t i = 0; i < h->M; ++i) {
+    camera_coefs(h, i, h->cam.data(), h->pt.data(), co, ul);
+    const double* ck = &h->cam[(size_t)(15 * i)];
+    const size_t a = (size_t)h->cam_dev[(size_t)i];
+    d_acc[a].add(camera_decrease(ck, &c_acc[(size_t)(15 * i)], co, ul.data(), &o));
+    d_mm[a].add(camera_decrease(ck, &c_mm[(size_t)(15 * i)], co, ul.data(), &o));
+  }
+  for (int64_t j = 0; j < h->N; ++j) {
+    point_coefs(h, j, h->cam.data(), h->pt.data(), co);
+    const double* lk = &h->pt[(size_t)(3 * j)];
+    const size_t a = (size_t)h->pt_dev[(size_t)j];
+    d_acc[a].add(point_decrease(lk, &l_acc[(size_t)(3 * j)], co, &o));
+    d_mm[a].add(point_decrease(lk, &l_mm[(size_t)(3 * j)], co, &o));
+  }
+  std::vector<char> rs((size_t)D, 0);
+  Kahan fb, ea, em;
+  int nrs = 0;
+  h->dev_last.assign((size_t)D * ORC_DEV_COLS, 0.0);
+  for (int a = 0; a < D; ++a) {
+    const double F = h->dev_E[(size_t)a] + dE[(size_t)a];                    // eq. Fak
+    const double Fbar = (1.0 - o.eta) * h->dev_Fbar[(size_t)a] + o.eta * F;  // eq. lFak
+    const double Eacc = F + d_acc[(size_t)a].s;                              // eq. Eak, x^{alpha(k+1)} = x_acc
+    const double Emm = F + d_mm[(size_t)a].s;                                // eq. Eak after a restart
+    const bool r = o.accelerate ? (Eacc > Fbar) : true;                      // Alg. 1, strict ">"
+    rs[(size_t)a] = r;
+    nrs += (o.accelerate && r) ? 1 : 0;
+    h->dev_Fbar[(size_t)a] = Fbar;
+    h->dev_E[(size_t)a] = r ? Emm : Eacc;
+    double* m = &h->dev_last[(size_t)a * ORC_DEV_COLS];
+    m[ORC_DEV_F] = F;
+    m[ORC_DEV_FBAR] = Fbar;
+    m[ORC_DEV_EACC] = Eacc;
+    m[ORC_DEV_EMM] = Emm;
+    m[ORC_DEV_RESTART] = (o.accelerate && r) ? 1.0 : 0.0;
+    fb.add(Fbar);
+    ea.add(Eacc);
+    em.add(Emm);
+  }
+  for (int64_t i = 0; i < h->M; ++i)
+    std::memcpy(&cn[(size_t)(15 * i)],
+                rs[(size_t)h->cam_dev[(size_t)i]] ? &c_mm[(size_t)(15 * i)] : &c_acc[(size_t)(15 * i)],
+                15 * sizeof(double));
+  for (int64_t j = 0; j < h->N; ++j)
+    std::memcpy(&ln[(size_t)(3 * j)], rs[(size_t)h->pt_dev[(size_t)j]] ? &l_mm[(size_t)(3 * j)] : &l_acc[(size_t)(3 * j)],
+                3 * sizeof(double));
+  *Fbar_sum = fb.s;
+  *Eacc_sum = ea.s;
+  *Emm_sum = em.s;
+  *n_restart = nrs;
+}
+
+extern "C" int orc_set_devices(orc_ctx* h, int ndev, const int32_t* cam_dev, const int32_t* pt_dev) {
+  // Alg. 1 L403-405 with eq. Fainit: x^{alpha(-1)} = x^{alpha(0)},
+  //   F^{alpha(-1)} = E^alpha(x^{alpha(-1)} | x^{(-1)}), F-bar^{alpha(-1)} = F^{alpha(-1)}, E^{alpha(0)} = F^{alpha(-1)}.
+  // At its own anchor E^alpha = sum_{i in alpha} sum_j P_ij + sum_{j in alpha} sum_i Q_ij, P_ij = Q_ij = F_ij / 2.
+  if (!h || ndev < 1 || !cam_dev || !pt_dev || h->k != 0) return -1;
+  for (int64_t i = 0; i < h->M; ++i)
+    if (cam_dev[i] < 0 || cam_dev[i] >= ndev) return -1;
+  for (int64_t j = 0; j < h->N; ++j)
+    if (pt_dev[j] < 0 || pt_dev[j] >= ndev) return -1;
+  h->ndev = ndev;
+  h->cam_dev.assign(cam_dev, cam_dev + h->M);
+  h->pt_dev.assign(pt_dev, pt_dev + h->N);
+  std::vector<Kahan> F0((size_t)ndev);
+  for (int64_t q = 0; q < h->K; ++q) {
+    const int32_t i = h->oc[(size_t)q], j = h->op[(size_t)q];
+    double F = 0;
+    if (orc_penalty(&h->cam[(size_t)(15 * i)], &h->pt[(size_t)(3 * j)], &h->uv[(size_t)(2 * q)], h->o.kind,
+                    h->o.scale, h->o.eps, &F) != 0)
+      continue;
+    F0[(size_t)h->cam_dev[(size_t)i]].add(0.5 * F);  // P_ij at its anchor
+    F0[(size_t)h->pt_dev[(size_t)j]].add(0.5 * F);   // Q_ij at its anchor
+  }
+  h->dev_Fbar.assign((size_t)ndev, 0.0);
+  h->dev_E.assign((size_t)ndev, 0.0);
+  for (int a = 0; a < ndev; ++a) h->dev_Fbar[(size_t)a] = h->dev_E[(size_t)a] = F0[(size_t)a].s;
+  h->dev_last.assign((size_t)ndev * ORC_DEV_COLS, 0.0);
+  return 0;
+}
+
+extern "C" int orc_device_metrics(const orc_ctx* h, double* out) {
+  if (!h || !out || h->ndev == 0) return -1;
+  std::memcpy(out, h->dev_last.data(), h->dev_last.size() * sizeof(double));
+  return 0;
+}
 
 extern "C" orc_ctx* orc_create(int64_t M, const double* cams_bal, int64_t N, const double* pts, int64_t K,
                                const int32_t* obs_cam, const int32_t* obs_pt, const double* obs_uv,
@@ -695,12 +880,15 @@ extern "C" int orc_iterate(orc_ctx* h, int n, double* trace) {
       dQ_mm.add(point_decrease(&h->pt[(size_t)(3 * j)], &l_mm[(size_t)(3 * j)], co, &o));
     }
     // ---- adaptive restart (Alg. 1; eqs. lFak, Eak in the global form D2)
-    const double Fbar_k = (1.0 - o.eta) * h->Fbar + o.eta * Fk;  // eq. lFak
-    const double E_acc = Fk + (dP_acc.s + dQ_acc.s);             // eq. Eak
-    const double E_mm = Fk + (dP_mm.s + dQ_mm.s);
+    double Fbar_k = (1.0 - o.eta) * h->Fbar + o.eta * Fk;  // eq. lFak
+    double E_acc = Fk + (dP_acc.s + dQ_acc.s);             // eq. Eak
+    double E_mm = Fk + (dP_mm.s + dQ_mm.s);
     const bool restart = o.accelerate ? (E_acc > Fbar_k) : true;  // strict ">" (Q12)
-    const std::vector<double>& cn = restart ? c_mm : c_acc;
-    const std::vector<double>& ln = restart ? l_mm : l_acc;
+    std::vector<double> cn = restart ? c_mm : c_acc;
+    std::vector<double> ln = restart ? l_mm : l_acc;
+    int n_restart = (o.accelerate && restart) ? 1 : 0;
+    if (h->ndev > 0)  // decentralized: every device decides for its own variables from its local metrics
+      device_restart(h, c_acc, c_mm, l_acc, l_mm, cn, ln, &Fbar_k, &E_acc, &E_mm, &n_restart);
     for (size_t q = 0; q < cn.size(); ++q) step2.add((cn[q] - h->cam[q]) * (cn[q] - h->cam[q]));
     for (size_t q = 0; q < ln.size(); ++q) step2.add((ln[q] - h->pt[q]) * (ln[q] - h->pt[q]));
     if (trace) {
@@ -708,7 +896,7 @@ extern "C" int orc_iterate(orc_ctx* h, int n, double* trace) {
       tr[ORC_TR_F] = Fk;
       tr[ORC_TR_FBAR] = Fbar_k;
       tr[ORC_TR_EACC] = E_acc;
-      tr[ORC_TR_RESTART] = (o.accelerate && restart) ? 1.0 : 0.0;
+      tr[ORC_TR_RESTART] = (double)n_restart;
       tr[ORC_TR_EMM] = E_mm;
       tr[ORC_TR_STEP2] = step2.s;
       tr[ORC_TR_GAMMA] = gamma;
@@ -723,6 +911,7 @@ extern "C" int orc_iterate(orc_ctx* h, int n, double* trace) {
     h->pt = ln;
     h->s = s_next;
     h->Fbar = Fbar_k;
+    ++h->k;
   }
   return 0;
 }

@@ -90,6 +90,15 @@ int orc_last_decisions(const orc_ctx* h, int32_t* trial_acc, int32_t* trial_mm);
  * and points, the accelerated (x-bar anchored) and MM (x^k anchored) solutions. */
 int orc_candidates(const orc_ctx* h, int64_t ncam, const int64_t* cam_ids, double* cam_acc, double* cam_mm,
                    int64_t npt, const int64_t* pt_ids, double* pt_acc, double* pt_mm);
+/* Decentralized adaptive restart (§5, eqs. DEalpha, Fainit, Fak, lFak, Eak; Alg. 1): from
+ * now on every device alpha (cam_dev: M entries, pt_dev: N entries, in [0, ndev)) keeps F^{alpha(k)},
+ * F-bar^{alpha(k)}, E^{alpha(k+1)} and takes the restart decision for its own variables.  Must be called
+ * before the first iteration.  The trace then holds F(x^k) in ORC_TR_F, sums over devices in FBAR / EACC /
+ * EMM and the number of restarting devices in RESTART. */
+enum { ORC_DEV_F = 0, ORC_DEV_FBAR, ORC_DEV_EACC, ORC_DEV_EMM, ORC_DEV_RESTART, ORC_DEV_COLS };
+int orc_set_devices(orc_ctx* h, int ndev, const int32_t* cam_dev, const int32_t* pt_dev);
+/* last iteration's per-device metrics, ndev x ORC_DEV_COLS */
+int orc_device_metrics(const orc_ctx* h, double* out);
 void orc_destroy(orc_ctx* h);
 
 #ifdef __cplusplus
