@@ -71,7 +71,13 @@ typedef struct {
   int use_graph;      /* 1: capture one iteration as a CUDA graph and replay it; default 1 */
   int profile;        /* 1: record CUDA events around every kernel (see daba_kernel_times); default 0 */
   void* stream;       /* cudaStream_t to launch on (NULL: a stream owned by the context) */
+  int restart_scope;  /* DABA_RESTART_GLOBAL: one restart test on the allreduced F(x^k) (reading D2, Lemma 1(a));
+                         DABA_RESTART_DEVICE: the paper's decentralized scheme — every rank keeps F^{a(k)},
+                         F-bar^{a(k)}, E^{a(k+1)} (eqs. DEalpha, Fainit, Fak, lFak, Eak) and decides
+                         for its own cameras and points (reading DN1 in DESIGN.md).  Default GLOBAL. */
 } daba_options;
+
+enum { DABA_RESTART_GLOBAL = 0, DABA_RESTART_DEVICE = 1 };
 
 /* Fill *o with the defaults above. */
 void daba_default_options(daba_options* o);
@@ -109,8 +115,12 @@ int daba_comm_id(void* id_out);
 int daba_iterate(daba_ctx* ctx, int n_iters, double* F_trace, uint8_t* restart_trace);
 
 /* Extended per-iteration trace: n_iters x DABA_TRACE_COLS doubles (host). */
+/* Columns: F(x^k) (global); F-bar^{(k)}; E(x_acc|x^k); restart; E(x_mm|x^k); ||x^{k+1} - x^k||^2; gamma_k;
+ * degenerate pairs (global); cameras without an accepted LM trial (acc, mm anchors; global); F^{a(k)}.
+ * With DABA_RESTART_DEVICE the columns FBAR, EACC, RESTART, EMM, STEP2 and FDEV are this rank's (device a's)
+ * values; with DABA_RESTART_GLOBAL they are global and FDEV = F. */
 enum { DABA_TR_F = 0, DABA_TR_FBAR, DABA_TR_EACC, DABA_TR_RESTART, DABA_TR_EMM, DABA_TR_STEP2, DABA_TR_GAMMA,
-       DABA_TR_NDEGEN, DABA_TR_NOACC_ACC, DABA_TR_NOACC_MM, DABA_TRACE_COLS };
+       DABA_TR_NDEGEN, DABA_TR_NOACC_ACC, DABA_TR_NOACC_MM, DABA_TR_FDEV, DABA_TRACE_COLS };
 int daba_iterate_trace(daba_ctx* ctx, int n_iters, double* trace);
 
 /* F(x^k) at the current iterate (eq. Fobj), identical on every rank (collective when nranks > 1). */

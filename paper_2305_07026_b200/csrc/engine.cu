@@ -215,6 +215,7 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   int n = 0;
   n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
   n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
+  n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
   // k_cam_solve and k_pt_sum are independent.  Run them as parallel branches when the solve is small (it then
   // hides behind the point pass); a large solve would crowd the point pass off the SMs (measured: +30 us at
   // 13.7K cameras), so it runs serialised.  Profiling always serialises so events bracket one kernel.
@@ -232,15 +233,22 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   }
   if (c->comm) {
     const bool halo = !c->segs.empty();
+    // global test: both candidates are sent before the decision (the exchange overlaps the allreduce) and
+    // k_select decides on the allreduced sums; per device: the rank has decided already (last block of
+    // k_cam_solve) and sends x^{k+1}; the allreduce only feeds the trace
+    const bool dev = P.restart_scope == 1;
     if (halo)
       n += timed(c, "k_pack", [&] {
         return launch_pack(P, c->d_send_cam, c->d_send_cam_off, c->n_send_cam, c->d_send_pt, c->d_send_pt_off,
-                           c->n_send_pt, c->d_sendbuf, c->stream);
+                           c->n_send_pt, c->d_sendbuf, dev ? 1 : 0, c->stream);
       });
     std::string e = c->comm->allreduce_exchange(P.local, P.global, kGlobalCols, c->d_sendbuf, c->d_recvbuf,
                                                 halo ? c->segs : std::vector<PeerSeg>(), c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
-    n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
+    if (dev)
+      n += timed(c, "k_trace_post", [&] { return launch_trace_post(P, c->stream); });
+    else
+      n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
     if (halo)
       n += timed(c, "k_unpack", [&] {
         return launch_unpack(P, c->d_recv_cam, c->d_recv_cam_off, c->n_recv_cam, c->d_recv_pt, c->d_recv_pt_off,
@@ -339,7 +347,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     return DABA_E_INVALID_ARG;
   if (!(loss.scale > 0) || loss.kind < DABA_LOSS_TRIVIAL || loss.kind > DABA_LOSS_CAUCHY) return DABA_E_INVALID_ARG;
   if (!(o.xi > 0) || !(o.eta > 0 && o.eta <= 1) || !(o.lm_mu0 > 0) || !(o.lm_mu_up >= 1) || !(o.eps >= 0) ||
-      o.lm_max_trials < 1 || o.lm_max_trials > 8)
+      o.lm_max_trials < 1 || o.lm_max_trials > 8 || o.restart_scope < 0 || o.restart_scope > 1)
     return DABA_E_INVALID_ARG;
   if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm_id)) return DABA_E_INVALID_ARG;
   C->loss = loss;
@@ -414,6 +422,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   P.eps2 = o.eps * o.eps;
   P.max_trials = o.lm_max_trials;
   P.accelerate = o.accelerate ? 1 : 0;
+  P.restart_scope = o.restart_scope;
   for (int r = 0; r < 4; ++r) {
     if ((rc = dalloc(C, &P.cams[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
     if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return bail(rc);
@@ -517,6 +526,37 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.b_cam = d1;
     P.b_pt = d2;
     P.b_uv = d4;
+    // per-device restart: the inter-device pairs of this rank (camera side with a halo point: sign +1; point
+    // side with a halo camera: sign -1)
+    if (P.restart_scope == 1) {
+      std::vector<int32_t> ic, ip, is;
+      std::vector<double2> iu;
+      for (size_t q = 0; q < kc; ++q)
+        if (S.c_pt[q] >= S.n_own_pts) {
+          ic.push_back(S.c_cam[q]);
+          ip.push_back(S.c_pt[q]);
+          iu.push_back(make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]));
+          is.push_back(1);
+        }
+      for (size_t b = 0; b < bcam.size(); ++b) {
+        ic.push_back(bcam[b]);
+        ip.push_back(bpt[b]);
+        iu.push_back(buv[b]);
+        is.push_back(-1);
+      }
+      P.n_inter = (int64_t)ic.size();
+      P.n_inter_blocks = (int32_t)((P.n_inter + kInterThreads - 1) / kInterThreads);
+      const int32_t *e0, *e1, *e2;
+      const double2* e3;
+      if ((rc = upload(C, const_cast<int32_t**>(&e0), ic)) || (rc = upload(C, const_cast<int32_t**>(&e1), ip)) ||
+          (rc = upload(C, const_cast<int32_t**>(&e2), is)) || (rc = upload(C, const_cast<double2**>(&e3), iu)) ||
+          (rc = dalloc(C, &P.inter_part, 2 * (size_t)std::max(P.n_inter_blocks, 1))))
+        return bail(rc);
+      P.i_cam = e0;
+      P.i_pt = e1;
+      P.i_sign = e2;
+      P.i_uv = e3;
+    }
     P.n_pt_blocks = std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, 148 * 8));
   }
   // scratch
@@ -588,6 +628,17 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
   double F0 = 0, nd = 0;
   if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
+  if (P.restart_scope == 1) {
+    // eq. Fainit per device: F-bar^{a(-1)} = F^{a(-1)} = E^a(x^{a(0)} | x^{(0)}) = F_kappa(x^0): the rank's
+    // camera-side F with its inter-device pairs at weight 1/2 (k_inter at x^{-1} = x^0); D^{a(-1)} = 0
+    launch_inter(P, C->stream);
+    launch_reduce_inter(P, C->stream);
+    double loc[kGlobalCols];
+    if (cudaMemcpyAsync(loc, P.local, sizeof loc, cudaMemcpyDeviceToHost, C->stream) != cudaSuccess ||
+        cudaStreamSynchronize(C->stream) != cudaSuccess)
+      return bail(DABA_E_CUDA);
+    F0 = loc[0] + loc[10];
+  }
   {
     const double sched[8] = {1.0, F0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (cudaMemcpyAsync(P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, C->stream) != cudaSuccess)
@@ -596,7 +647,8 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (cudaStreamSynchronize(C->stream) != cudaSuccess) return bail(DABA_E_CUDA);
   }
   // launches per iteration (for bookkeeping)
-  C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) + (C->comm ? 1 : 0);
+  C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) + (C->comm ? 1 : 0) +
+                         (P.n_inter_blocks > 0);
   C->launches_per_iter += (C->n_send_cam + C->n_send_pt > 0) + (C->n_recv_cam + C->n_recv_pt > 0);
   *out = c.release();
   return DABA_OK;
@@ -746,6 +798,8 @@ extern "C" int daba_set_state_native(daba_ctx* ctx, const double* cams_k, const 
                                      const double* cams_km1, const double* pts_km1, double s, double Fbar) {
   if (!ctx || (ctx->plan.M > 0 && (!cams_k || !cams_km1)) || (ctx->plan.N > 0 && (!pts_k || !pts_km1)) || !(s >= 1))
     return DABA_E_INVALID_ARG;
+  if (ctx->P.restart_scope == 1)
+    return fail(ctx, DABA_E_STATE, "daba_set_state_native: the per-device restart metrics cannot be restored");
   cudaSetDevice(ctx->device);
   int rc = upload_states(ctx, cams_k, pts_k, cams_km1, pts_km1, 1, 0);
   if (rc) return rc;

@@ -532,6 +532,10 @@ __device__ void final_reduce(const IterParams& p) {
     v[5] += __ldcg(q + 2);
     v[6] += __ldcg(q + 3);
   }
+  for (int b = threadIdx.x; b < p.n_inter_blocks; b += nt) {
+    v[10] += __ldcg(p.inter_part + 2 * (size_t)b);
+    v[11] += __ldcg(p.inter_part + 2 * (size_t)b + 1);
+  }
   for (int c = 0; c < kGlobalCols; ++c) s[c][threadIdx.x] = v[c];
   __syncthreads();
   for (int st = nt / 2; st > 0; st >>= 1) {
@@ -557,7 +561,7 @@ __device__ void finish_block(const IterParams& p) {
   if (threadIdx.x == 0) {
     *p.counter = 0;
     __threadfence();
-    if (!p.has_comm) do_select(p);
+    if (!p.has_comm || p.restart_scope == 1) do_select(p);  // a per-device decision needs no collective
   }
 }
 
@@ -898,17 +902,22 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
 
 // ------------------------------------------------------------------ a9 + a10: restart test and selection
 __device__ void do_select(const IterParams& p) {
-  const double* G = p.global;
   double s_next;
   const double gamma = sched_gamma(p.sched[0], p.accelerate, &s_next);
-  const double F = G[0];
-  const double Fbar = (1.0 - p.eta) * p.sched[1] + p.eta * F;  // eq. lFak (global form)
+  const bool dev = p.restart_scope == 1;
+  // Global test (D2): the allreduced sums.  Per device (eqs. Fak, lFak, Eak; reading DN1): this rank's sums,
+  //   F^{a(k)} = F_kappa(x^k) + D^{a(k)},  D^{a(k)} = D^{a(k-1)} + (1/2) sum_inter sign (dP_ij - dQ_ij),
+  // F_kappa = the rank's camera-side F with inter-device pairs at weight 1/2 (local[0] + local[10]).
+  const double* G = dev ? p.local : p.global;
+  const double D = dev ? p.sched[3] + G[11] : 0.0;
+  const double F = dev ? (G[0] + G[10]) + D : G[0];
+  const double Fbar = (1.0 - p.eta) * p.sched[1] + p.eta * F;  // eq. lFak
   const double Eacc = F + (G[1] + G[2]);                        // eq. Eak: E(x_acc | x^k)
   const double Emm = F + (G[3] + G[4]);
   const bool restart = p.accelerate ? (Eacc > Fbar) : true;     // Alg. 1, strict ">"
   const int64_t k = (int64_t)p.sched[2];
   double* tr = p.trace + (size_t)(k % p.trace_cap) * kTraceCols;
-  tr[0] = F;
+  tr[0] = dev ? G[0] + G[10] : F;  // per device with a communicator: replaced by the global F in k_trace_post
   tr[1] = Fbar;
   tr[2] = Eacc;
   tr[3] = (p.accelerate && restart) ? 1.0 : 0.0;
@@ -918,6 +927,8 @@ __device__ void do_select(const IterParams& p) {
   tr[7] = G[7];
   tr[8] = G[8];
   tr[9] = G[9];
+  tr[10] = F;
+  if (dev) p.sched[3] = D;
   const int r0 = p.roles[0], r1 = p.roles[1], r2 = p.roles[2], r3 = p.roles[3];
   p.roles[0] = r1;                 // x^{k}   -> x^{k-1}
   p.roles[1] = restart ? r3 : r2;  // x^{k+1} = x_mm (restart, Alg. 1) or x_acc (L414)
@@ -931,6 +942,113 @@ __device__ void do_select(const IterParams& p) {
 
 __global__ void k_select(IterParams p) {
   if (threadIdx.x == 0 && blockIdx.x == 0) do_select(p);
+}
+
+// Per-device restart with a communicator: the decision was local; the allreduce then supplies the global
+// columns of the trace row just written (F, degenerate pairs, cameras without an accepted trial).
+__global__ void k_trace_post(IterParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t k = (int64_t)p.sched[2] - 1;
+  double* tr = p.trace + (size_t)(k % p.trace_cap) * kTraceCols;
+  tr[0] = p.global[0];
+  tr[7] = p.global[7];
+  tr[8] = p.global[8];
+  tr[9] = p.global[9];
+}
+
+// Inter-device pair terms of the per-device metrics (eq. DEalpha at x = x^k, anchor x^{k-1}; DN1).
+// For a pair with sign s (+1: this rank owns the camera, -1: it owns the point):
+//   col 0: -s F_ij(x^k) / 2           (F_kappa counts an inter-device pair at weight 1/2 on each side)
+//   col 1:  s (dP_ij - dQ_ij) / 2      (dP_ij = P_ij(c^k|x^{k-1}) - P_ij(c^{k-1}|x^{k-1}), dQ_ij likewise: the
+//                                        anchor-relative forms w dr.(dr + R e), w (lam dl).(lam dl - R e))
+template <int LOSS>
+__global__ void __launch_bounds__(kInterThreads) k_inter(IterParams p) {
+  double v0 = 0.0, v1 = 0.0;
+  const int64_t b = blockIdx.x * (int64_t)kInterThreads + threadIdx.x;
+  if (b < p.n_inter) {
+    const int32_t i = p.i_cam[b], j = p.i_pt[b];
+    const double sg = (double)p.i_sign[b];
+    const double2 u = p.i_uv[b];
+    const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
+    const double* cp = p.cams[p.roles[0]] + (size_t)i * kCamStride;
+    const double4 lk = p.pts[p.roles[1]][j], lp = p.pts[p.roles[0]][j];
+    const double s = fma(u.x, u.x, u.y * u.y);
+    // anchor x^{k-1}: ray, lambda, R e, w (eqs. ray, gamma, error, w)
+    const double pzp = fma(s, fma(s, cp[14], cp[13]), cp[12]);
+    const double rpx = fma(cp[0], u.x, fma(cp[1], u.y, cp[2] * pzp));
+    const double rpy = fma(cp[3], u.x, fma(cp[4], u.y, cp[5] * pzp));
+    const double rpz = fma(cp[6], u.x, fma(cp[7], u.y, cp[8] * pzp));
+    const double vx = lp.x - cp[9], vy = lp.y - cp[10], vz = lp.z - cp[11];
+    const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
+    if (nv > p.eps2) {
+      const double lam = fma(vx, rpx, fma(vy, rpy, vz * rpz)) / nv;
+      const double ex = fma(-lam, vx, rpx), ey = fma(-lam, vy, rpy), ez = fma(-lam, vz, rpz);
+      const double w = loss_eval<LOSS, false>(fma(ex, ex, fma(ey, ey, ez * ez)), p.delta, p.delta2, p.idelta2,
+                                               nullptr);
+      // camera move: dr = R^k p(d^k) - R^{k-1} p(d^{k-1}) + lam (t^k - t^{k-1})
+      const double pzk = fma(s, fma(s, ck[14], ck[13]), ck[12]);
+      const double dx = fma(ck[0], u.x, fma(ck[1], u.y, ck[2] * pzk)) - rpx + lam * (ck[9] - cp[9]);
+      const double dy = fma(ck[3], u.x, fma(ck[4], u.y, ck[5] * pzk)) - rpy + lam * (ck[10] - cp[10]);
+      const double dz = fma(ck[6], u.x, fma(ck[7], u.y, ck[8] * pzk)) - rpz + lam * (ck[11] - cp[11]);
+      const double dP = w * fma(dx, dx + ex, fma(dy, dy + ey, dz * (dz + ez)));
+      const double mx = lam * (lk.x - lp.x), my = lam * (lk.y - lp.y), mz = lam * (lk.z - lp.z);
+      const double dQ = w * fma(mx, mx - ex, fma(my, my - ey, mz * (mz - ez)));
+      v1 = 0.5 * sg * (dP - dQ);
+    }
+    // F_ij(x^k) (eq. Fij)
+    const double pz = fma(s, fma(s, ck[14], ck[13]), ck[12]);
+    const double rx = fma(ck[0], u.x, fma(ck[1], u.y, ck[2] * pz));
+    const double ry = fma(ck[3], u.x, fma(ck[4], u.y, ck[5] * pz));
+    const double rz = fma(ck[6], u.x, fma(ck[7], u.y, ck[8] * pz));
+    const double wx = lk.x - ck[9], wy = lk.y - ck[10], wz = lk.z - ck[11];
+    const double nw = fma(wx, wx, fma(wy, wy, wz * wz));
+    if (nw > p.eps2) {
+      const double lam = fma(wx, rx, fma(wy, ry, wz * rz)) / nw;
+      const double ex = fma(-lam, wx, rx), ey = fma(-lam, wy, ry), ez = fma(-lam, wz, rz);
+      double rho;
+      loss_eval<LOSS, true>(fma(ex, ex, fma(ey, ey, ez * ez)), p.delta, p.delta2, p.idelta2, &rho);
+      v0 = -0.25 * sg * rho;  // -s F_ij / 2, F_ij = rho / 2
+    }
+  }
+  __shared__ double s0[kInterThreads], s1[kInterThreads];
+  s0[threadIdx.x] = v0;
+  s1[threadIdx.x] = v1;
+  __syncthreads();
+  for (int st = kInterThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      s0[threadIdx.x] += s0[threadIdx.x + st];
+      s1[threadIdx.x] += s1[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.inter_part[2 * (size_t)blockIdx.x] = s0[0];
+    p.inter_part[2 * (size_t)blockIdx.x + 1] = s1[0];
+  }
+}
+
+// Create time: sum the k_inter partials into local[10], local[11] (fixed order).
+__global__ void k_reduce_inter(IterParams p) {
+  __shared__ double s0[256], s1[256];
+  double a = 0, b = 0;
+  for (int q = threadIdx.x; q < p.n_inter_blocks; q += 256) {
+    a += p.inter_part[2 * (size_t)q];
+    b += p.inter_part[2 * (size_t)q + 1];
+  }
+  s0[threadIdx.x] = a;
+  s1[threadIdx.x] = b;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      s0[threadIdx.x] += s0[threadIdx.x + st];
+      s1[threadIdx.x] += s1[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.local[10] = s0[0];
+    p.local[11] = s1[0];
+  }
 }
 
 // x-bar^k of every local camera and point from x^k, x^{k-1} (create / set_state); writes the role-selected
@@ -952,17 +1070,19 @@ __global__ void k_lbar_all(IterParams p) {
 // Both candidates of each boundary variable (before the restart decision): camera [acc 15 | mm 15],
 // point [acc 3 | mm 3].
 __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                       const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf) {
+                       const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // before the decision: [acc | mm] candidates; after a local decision (selected): [x^{k+1} | x^{k+1}]
+  const int ra = selected ? p.roles[1] : p.roles[2], rm = selected ? p.roles[1] : p.roles[3];
   if (t < n_cam) {
-    const double* ca = p.cams[p.roles[2]] + (size_t)cam_idx[t] * kCamStride;
-    const double* cm = p.cams[p.roles[3]] + (size_t)cam_idx[t] * kCamStride;
+    const double* ca = p.cams[ra] + (size_t)cam_idx[t] * kCamStride;
+    const double* cm = p.cams[rm] + (size_t)cam_idx[t] * kCamStride;
     double* b = buf + cam_off[t];
     for (int k = 0; k < 15; ++k) b[k] = ca[k];
     for (int k = 0; k < 15; ++k) b[15 + k] = cm[k];
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
-    const double4 la = p.pts[p.roles[2]][pt_idx[q]], lm = p.pts[p.roles[3]][pt_idx[q]];
+    const double4 la = p.pts[ra][pt_idx[q]], lm = p.pts[rm][pt_idx[q]];
     double* b = buf + pt_off[q];
     b[0] = la.x;
     b[1] = la.y;
@@ -1074,9 +1194,31 @@ int launch_objective(const IterParams& p, cudaStream_t st) {
 }
 
 int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, cudaStream_t st) {
+                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected,
+                cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf);
+  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
+                                                    selected);
+  return 1;
+}
+
+int launch_inter(const IterParams& p, cudaStream_t st) {
+  if (p.n_inter_blocks == 0) return 0;
+  switch (p.loss) {
+    case kHuber: k_inter<kHuber><<<p.n_inter_blocks, kInterThreads, 0, st>>>(p); break;
+    case kCauchy: k_inter<kCauchy><<<p.n_inter_blocks, kInterThreads, 0, st>>>(p); break;
+    default: k_inter<kTrivial><<<p.n_inter_blocks, kInterThreads, 0, st>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_reduce_inter(const IterParams& p, cudaStream_t st) {
+  k_reduce_inter<<<1, 256, 0, st>>>(p);
+  return 1;
+}
+
+int launch_trace_post(const IterParams& p, cudaStream_t st) {
+  k_trace_post<<<1, 32, 0, st>>>(p);
   return 1;
 }
 

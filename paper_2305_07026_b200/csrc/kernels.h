@@ -22,8 +22,10 @@ constexpr int kCamChunkObs = DABA_CHUNK;  // max observations per camera-pass ch
 constexpr int kPtPassThreads = 256;     // point solve: threads (points) per CTA
 constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
-constexpr int kGlobalCols = 10;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
-constexpr int kTraceCols = 10;    // = DABA_TRACE_COLS
+constexpr int kGlobalCols = 12;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm,
+                                  // F_kappa correction, D increment (per-device restart, k_inter)
+constexpr int kTraceCols = 11;    // = DABA_TRACE_COLS
+constexpr int kInterThreads = 256;
 
 struct CamChunk {
   int32_t cam;    // local camera index (owned)
@@ -84,6 +86,16 @@ struct IterParams {
   double* global;         // kGlobalCols (allreduced)
   double* trace;          // trace ring, trace_cap x kTraceCols
   int32_t trace_cap;
+  // decentralized (per-device) restart, DABA_RESTART_DEVICE: the inter-device pairs this rank touches —
+  // camera-side pairs with a halo point (sign +1) and point-side boundary pairs with a halo camera (sign -1)
+  int32_t restart_scope;  // 0 global, 1 per device
+  int64_t n_inter;
+  const int32_t* i_cam;   // local camera
+  const int32_t* i_pt;    // local point
+  const double2* i_uv;
+  const int32_t* i_sign;
+  double* inter_part;     // k_inter blocks x 2
+  int32_t n_inter_blocks;
 };
 
 // Launchers (all asynchronous on `st`).  They return the number of kernels launched.
@@ -93,11 +105,18 @@ int launch_pt_pass(const IterParams& p, cudaStream_t st);
 int launch_cam_solve(const IterParams& p, cudaStream_t st);
 int launch_pt_sum(const IterParams& p, cudaStream_t st);  // + rank-local sums (+ select without comm)
 int launch_select(const IterParams& p, cudaStream_t st);
+// per-device restart: the inter-device pair terms of F^{a(k)} (before k_cam_solve); rank-local sums of them
+// into local[10..11] (create time); the allreduced trace columns after a local decision
+int launch_inter(const IterParams& p, cudaStream_t st);
+int launch_reduce_inter(const IterParams& p, cudaStream_t st);
+int launch_trace_post(const IterParams& p, cudaStream_t st);
 // F(x^k) only (create-time F-bar^{(-1)} and daba_objective): writes local[0] (and local[7] = degenerate count)
 int launch_objective(const IterParams& p, cudaStream_t st);
 // halo exchange helpers: gather owned boundary entries of x^k into a send buffer / scatter received entries
+// (selected = 1: after a local decision both slots carry x^{k+1})
 int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, cudaStream_t st);
+                const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected,
+                cudaStream_t st);
 // also writes x-bar of the received halo entries (gamma of the next iteration)
 int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                   const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, cudaStream_t st);

@@ -14,8 +14,9 @@ _lib = None
 
 LOSS_TRIVIAL, LOSS_HUBER, LOSS_CAUCHY = 0, 1, 2
 COMM_NCCL, COMM_LOCAL = 0, 1
-(TR_F, TR_FBAR, TR_EACC, TR_RESTART, TR_EMM, TR_STEP2, TR_GAMMA, TR_NDEGEN, TR_NOACC_ACC, TR_NOACC_MM,
- TRACE_COLS) = range(11)
+(TR_F, TR_FBAR, TR_EACC, TR_RESTART, TR_EMM, TR_STEP2, TR_GAMMA, TR_NDEGEN, TR_NOACC_ACC, TR_NOACC_MM, TR_FDEV,
+ TRACE_COLS) = range(12)
+RESTART_GLOBAL, RESTART_DEVICE = 0, 1
 ERRORS = {0: "DABA_OK", -1: "DABA_E_INVALID_ARG", -2: "DABA_E_DEGENERATE", -3: "DABA_E_CUDA", -4: "DABA_E_NCCL",
           -5: "DABA_E_OOM", -6: "DABA_E_STATE"}
 
@@ -34,7 +35,7 @@ class Options(ctypes.Structure):
     _fields_ = [("xi", ctypes.c_double), ("eta", ctypes.c_double), ("lm_mu0", ctypes.c_double),
                 ("lm_mu_up", ctypes.c_double), ("eps", ctypes.c_double), ("lm_max_trials", ctypes.c_int),
                 ("accelerate", ctypes.c_int), ("comm", ctypes.c_int), ("use_graph", ctypes.c_int),
-                ("profile", ctypes.c_int), ("stream", ctypes.c_void_p)]
+                ("profile", ctypes.c_int), ("stream", ctypes.c_void_p), ("restart_scope", ctypes.c_int)]
 
 
 EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate", "daba_iterate_trace",

@@ -292,6 +292,17 @@ def test_nccl_transport_single_rank():
         np.testing.assert_array_equal(a.state_native(0)[0], b.state_native(0)[0])
 
 
+def test_nccl_transport_single_rank_device_restart():
+    """Per-device restart through NCCL (local decision in the graph, allreduce feeding the trace only)."""
+    p = gen.generate("small_huber")
+    key = D.comm_id()
+    with solver(p, eta=1.0) as a, solver(p, nranks=1, rank=0, comm_key=key, comm=D.COMM_NCCL, eta=1.0,
+                                           restart_scope=D.RESTART_DEVICE) as b:
+        ta, tb = a.iterate_trace(12), b.iterate_trace(12)
+        np.testing.assert_array_equal(ta, tb)
+        assert ta[:, D.daba.TR_RESTART].sum() > 0
+
+
 def test_random_ownership_four_ranks():
     """Irregular partition (random camera and point owners over 4 ranks: every rank talks to every other, many
     boundary observations recomputed from halo cameras) gives the 1-rank iterates (reading D1)."""
@@ -354,3 +365,85 @@ def test_acceleration_beats_plain_mm(name):
     ka = int(np.argmax(Fa <= F_delta)) if (Fa <= F_delta).any() else 10**9
     kb = int(np.argmax(Fb <= F_delta)) if (Fb <= F_delta).any() else 10**9
     assert ka < kb, (ka, kb)
+
+
+# ---------------------------------------------------------------- decentralized (per-device) restart, NEXT-1
+def run_ranks_all(p, nranks, n_iter, **kw):
+    """Every rank's trace and the assembled owned states (LOCAL transport, ranks = threads)."""
+    key = np.random.default_rng(100 + nranks).bytes(128)
+    out = [None] * nranks
+    err = []
+
+    def work(r):
+        try:
+            s = solver(p, rank=r, nranks=nranks, comm_key=key, comm=D.COMM_LOCAL, **kw)
+            tr = s.iterate_trace(n_iter)
+            c, l, mask = s.state_native(0)
+            out[r] = (tr, c, l, mask)
+            s.close()
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    if err:
+        raise err[0]
+    cams, pts = np.full((p.M, 15), np.nan), np.full((p.N, 3), np.nan)
+    for tr, c, l, mask in out:
+        cams[mask[:p.M] == 1] = c[mask[:p.M] == 1]
+        pts[mask[p.M:] == 1] = l[mask[p.M:] == 1]
+    return [o[0] for o in out], cams, pts
+
+
+def test_device_restart_single_rank_is_global():
+    p = gen.generate("small_huber")
+    with solver(p, eta=1.0) as a, solver(p, eta=1.0, restart_scope=D.RESTART_DEVICE) as b:
+        ta, tb = a.iterate_trace(20), b.iterate_trace(20)
+        np.testing.assert_array_equal(ta, tb)
+        np.testing.assert_array_equal(tb[:, D.daba.TR_FDEV], tb[:, D.daba.TR_F])
+        ck, lk, _ = b.state_native(0)
+        cp, lp, _ = b.state_native(1)
+        with pytest.raises(D.DabaError) as e:  # per-device metrics are not part of the resume point
+            b.set_state_native(ck, lk, cp, lp, 2.0, 1.0)
+        assert e.value.code == -6
+
+
+@pytest.mark.parametrize("name,nranks,eta", [("small_huber", 2, 1.0), ("small_cauchy", 3, 0.1),
+                                              ("small_seq_huber", 3, 1.0), ("tiny_seq", 2, 1.0)])
+def test_device_restart_parity(name, nranks, eta):
+    # each rank = one device of eqs. DEalpha-Eak; the oracle simulates the same devices
+    p = gen.generate(name)
+    r = np.random.default_rng(3)
+    cd = r.integers(0, nranks, p.M).astype(np.int32)
+    pd = r.integers(0, nranks, p.N).astype(np.int32)
+    cd[:nranks] = np.arange(nranks)
+    pd[:nranks] = np.arange(nranks)
+    n_iter = 30
+    o = oracle_for(p, eta=eta)
+    o.set_devices(cd, pd)
+    otr, om = [], []
+    for k in range(n_iter):
+        otr.append(o.iterate(1)[0])
+        om.append(o.device_metrics())
+    otr, om = np.array(otr), np.array(om)
+    trs, cams, pts = run_ranks_all(p, nranks, n_iter, cam_owner=cd, pt_owner=pd, eta=eta,
+                                   restart_scope=D.RESTART_DEVICE)
+    F = otr[:, oracle.TR_F]
+    fired = 0
+    for a in range(nranks):
+        tr = trs[a]
+        np.testing.assert_allclose(tr[:, D.daba.TR_F], F, rtol=F_TOL)
+        tol = F_TOL * F
+        assert np.all(np.abs(tr[:, D.daba.TR_FDEV] - om[:, a, oracle.DEV_F]) <= tol)
+        assert np.all(np.abs(tr[:, D.daba.TR_FBAR] - om[:, a, oracle.DEV_FBAR]) <= tol)
+        assert np.all(np.abs(tr[:, D.daba.TR_EACC] - om[:, a, oracle.DEV_EACC]) <= tol)
+        assert np.all(np.abs(tr[:, D.daba.TR_EMM] - om[:, a, oracle.DEV_EMM]) <= tol)
+        np.testing.assert_array_equal(tr[:, D.daba.TR_RESTART], om[:, a, oracle.DEV_RESTART])
+        fired += int(tr[:, D.daba.TR_RESTART].sum())
+    # the devices' objectives add up to F (reading DN1)
+    fsum = sum(t[:, D.daba.TR_FDEV] for t in trs)
+    np.testing.assert_allclose(fsum, F, rtol=1e-10)
+    co, lo = o.state(0)
+    assert max(state_errors(cams, pts, co, lo)) <= X_TOL
+    if eta == 1.0:
+        assert fired > 0
