@@ -190,6 +190,11 @@ int timed(daba_ctx* c, const char* name, F&& fn) {
   cudaEventRecord(a, c->stream);
   const int n = fn();
   cudaEventRecord(b, c->stream);
+  if (n == 0) {  // nothing launched: no entry
+    c->event_pool.push_back(a);
+    c->event_pool.push_back(b);
+    return 0;
+  }
   c->pending.push_back({id, a, b});
   c->klaunches[(size_t)id] += n;
   return n;
@@ -499,23 +504,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
     P.n_cam_side = (int64_t)kc;
     P.n_boundary = (int64_t)bcam.size();
-#ifdef DABA_PTMAJOR
-    {  // records at their point-major position
-      std::vector<int32_t> pos_of_obs((size_t)K, -1), crec(kc), brec;
-      for (size_t q = 0; q < kp; ++q) pos_of_obs[(size_t)S.p_obs[q]] = (int32_t)q;
-      for (size_t q = 0; q < kc; ++q) crec[q] = pos_of_obs[(size_t)S.c_obs[q]];
-      for (size_t q = 0; q < kp; ++q)
-        if (src[q] >= (int32_t)kc) brec.push_back((int32_t)q);
-      const int32_t *dc, *db;
-      if ((rc = upload(C, const_cast<int32_t**>(&dc), crec)) || (rc = upload(C, const_cast<int32_t**>(&db), brec)))
-        return bail(rc);
-      P.c_rec = dc;
-      P.b_rec = db;
-    }
-    P.n_records = std::max<int64_t>((int64_t)kp, 1);
-#else
     P.n_records = std::max<int64_t>(P.n_cam_side + P.n_boundary, 1);
-#endif
     if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
     const int32_t *d0, *d1, *d2;
     const double2* d4;

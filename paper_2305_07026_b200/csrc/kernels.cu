@@ -49,6 +49,17 @@ __device__ __forceinline__ void st256(double4* q, double4 v) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) DABA_ST_CLOBBER);
 }
 
+// Point-side record of observation r at anchor a (0: x-bar^k, 1: x^k), 32 B, in two separate arrays.
+// DABA_INTERLEAVE puts an observation's two records side by side (64 B): measured neutral on Final-13682
+// (k_pt_sum -0.04 ms, k_cam_pass +0.03 ms: the two anchors' CTAs then write half lines).
+__device__ __forceinline__ double4* rec_ptr(const IterParams& p, int64_t r, int a) {
+#ifdef DABA_INTERLEAVE
+  return reinterpret_cast<double4*>(p.staging) + 2 * r + a;
+#else
+  return reinterpret_cast<double4*>(p.staging + (a ? 4 * p.n_records : 0)) + r;
+#endif
+}
+
 // Point record: 32 bytes (x, y, z, pad) — one sector per gather.
 __device__ __forceinline__ void ld_point(const double4* base, int64_t j, double& x, double& y, double& z) {
   const double2* q = reinterpret_cast<const double2*>(base + j);
@@ -121,7 +132,7 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
     acc[40] += 1.0;
     if (rec >= 0)
-      st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec, make_double4(0.0, 0.0, 0.0, 0.0));
+      st256(rec_ptr(p, rec, ACC ? 0 : 1), make_double4(0.0, 0.0, 0.0, 0.0));
     return;
   }
   // camera-frame point R^T (l - t)
@@ -204,7 +215,7 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   const double gy = fma(c[3], ex, fma(c[4], ey, c[5] * ez));
   const double gz = fma(c[6], ex, fma(c[7], ey, c[8] * ez));
   if (rec >= 0)
-    st256(reinterpret_cast<double4*>(p.staging + (ACC ? 0 : 4 * p.n_records)) + rec,
+    st256(rec_ptr(p, rec, ACC ? 0 : 1),
           make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
 #ifdef DABA_NOEMIT
   }
@@ -246,13 +257,7 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
   // stage the chunk's point indices: every 4-byte copy in flight at once (cp.async), one wait
   for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(sidx + o, p.c_pt + ch.o0 + o);
-#ifdef DABA_PTMAJOR
-  int32_t* srec = sidx + kCamChunkObs;  // record (point-major position) of each observation
-  for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(srec + o, p.c_rec + ch.o0 + o);
-#define REC(kk) (int64_t) srec[tid + (kk) * kCamPassThreads]
-#else
 #define REC(kk) (ch.o0 + tid + (int64_t)(kk) * kCamPassThreads)
-#endif
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
@@ -339,11 +344,7 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, d
   }
 }
 
-#ifdef DABA_PTMAJOR
-constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs;  // ring + indices + records
-#else
 constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs / 2;  // ring + indices
-#endif
 constexpr int kCamSmemDoubles =
     kCamRingDoubles > kCamPassThreads * kPartialStride ? kCamRingDoubles : kCamPassThreads * kPartialStride;
 
@@ -496,13 +497,9 @@ __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
   double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   pt_terms<LOSS>(p.cbarb[p.roles[4]] + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
   pt_terms<LOSS>(p.cams[p.roles[1]] + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
-#ifdef DABA_PTMAJOR
-  const int64_t r = p.b_rec[b];
-#else
   const int64_t r = p.n_cam_side + b;
-#endif
-  reinterpret_cast<double4*>(p.staging)[r] = make_double4(a[0], a[1], a[2], a[3]);
-  reinterpret_cast<double4*>(p.staging + 4 * p.n_records)[r] = make_double4(a[4], a[5], a[6], a[7]);
+  *rec_ptr(p, r, 0) = make_double4(a[0], a[1], a[2], a[3]);
+  *rec_ptr(p, r, 1) = make_double4(a[4], a[5], a[6], a[7]);
 }
 
 __device__ void do_select(const IterParams& p);
@@ -570,8 +567,6 @@ __device__ void finish_block(const IterParams& p) {
 // rank-local sums (a9) and, without a communicator, takes the restart decision (a9 + a10).  Deterministic.
 __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   double qv[kPtCols] = {0, 0, 0, 0};
-  const double4* ra = reinterpret_cast<const double4*>(p.staging);
-  const double4* rm = reinterpret_cast<const double4*>(p.staging + 4 * p.n_records);
   for (int j = blockIdx.x * kPtPassThreads + threadIdx.x; j < p.n_own_pts; j += gridDim.x * kPtPassThreads) {
     const double4 k4 = p.pts[p.roles[1]][j], b4 = p.lbar[p.roles[4]][j];
     const double lk[3] = {k4.x, k4.y, k4.z};
@@ -581,17 +576,13 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
     for (int64_t o = p.p_ptr[j]; o < o1; o += 4) {  // up to 4 records (8 x 32 B) in flight per thread
       int32_t r[4];
 #pragma unroll
-#ifdef DABA_PTMAJOR
-      for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? (int32_t)(o + i) : -1;
-#else
       for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? p.p_src[o + i] : -1;
-#endif
       double4 A[4], B[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (r[i] >= 0) {
-          A[i] = ld256(ra + r[i]);
-          B[i] = ld256(rm + r[i]);
+          A[i] = ld256(rec_ptr(p, r[i], 0));
+          B[i] = ld256(rec_ptr(p, r[i], 1));
         }
 #pragma unroll
       for (int i = 0; i < 4; ++i)

@@ -65,8 +65,6 @@ struct IterParams {
   // get records n_cam_side + b.  p_src lists each owned point's records in (point, camera) order.
   const int64_t* p_ptr;          // n_own_pts + 1
   const int32_t* p_src;          // record of each point-side observation
-  const int32_t* c_rec;          // (point-major records) record of each camera-side observation, -1: not owned
-  const int32_t* b_rec;          // (point-major records) record of each boundary observation
   double* staging;               // 2 x n_records x 4
   int64_t n_cam_side, n_records;
   // boundary observations (point owned here, camera owned elsewhere): recomputed from halo cameras
