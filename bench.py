@@ -4,9 +4,12 @@
 One step = one DABA iteration (Algorithm 1) over the whole synthetic BAL Final-13682-shaped problem
 (BASELINE.json configs[3]: 13,682 cameras, 4,456,117 points, 28,987,644 observations, Huber loss), fp64.
 N = 1: one B200.  N > 1 (torchrun, one rank per GPU): the same problem partitioned across the ranks (strong
-scaling; NCCL halo exchange + one allreduce per iteration).
+scaling; NCCL halo exchange + one allreduce per iteration).  --config weak_slab (configs[4], Cauchy): N slabs of
+31.25M observations at N GPUs (weak scaling).  --restart device: the paper's decentralized per-device restart
+(reading DN1) instead of the global test.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config final13682] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config final13682] [--restart global|device]
+                  [--impl reference]
 
 Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
 """
@@ -45,6 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="final13682")
+    ap.add_argument("--restart", default="global", choices=["global", "device"])
     ap.add_argument("--impl", default="daba", choices=["daba", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -103,6 +107,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+WEAK = {"weak_slab"}  # BASELINE.json configs[4]: per-GPU slab fixed, N slabs at N GPUs (weak scaling)
+
+
+def make_problem(config, world):
+    import gen
+    if config in WEAK:
+        cM, cN, cK = gen.CONFIGS[config][:3]
+        return gen.generate(config, M=cM * world, N=cN * world, K=cK * world), "weak"
+    return gen.generate(config), "strong"
+
+
 def sample_problem(p, max_obs):
     """Induced sub-problem on the first cameras whose observations total <= max_obs (for the CPU oracle)."""
     import numpy as np
@@ -144,7 +159,7 @@ def main():
         # The reference arm is the CPU oracle, as it stands, on the box's host cores (rank 0 only).
         if rank != 0:
             return
-        p = gen.generate(a.config)
+        p, _ = make_problem(a.config, 1)
         sp = sample_problem(p, 60_000)
         import oracle
         o = oracle.Oracle(sp)
@@ -171,7 +186,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo", init_method="env://")
-    p = gen.generate(a.config)
+    p, scaling = make_problem(a.config, world)
 
     def fresh_key():
         # every context gets its own NCCL communicator, hence its own unique id (rank 0 draws, all receive)
@@ -182,7 +197,8 @@ def main():
         return obj[0]
 
     stream = torch.cuda.Stream(device=local)
-    kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, device=local)
+    kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, device=local,
+              restart_scope=1 if a.restart == "device" else 0)
 
     # ---------------- device-resident timed region (production path: one CUDA graph per iteration)
     s = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, comm_key=fresh_key(),
@@ -273,6 +289,7 @@ def main():
     dom = max(kt.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / max(dl, 1)
+    kt = {k: v for k, v in kt.items() if v[1] > 0}
     kshare = {k: round(v[0] / prof_ms, 4) for k, v in kt.items()}
     roof = None
     kbytes = {k: f(info["cam_side_obs"] if k == "k_cam_pass" else info["pt_side_obs"],
@@ -298,9 +315,10 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": a.config, "cameras": p.M, "points": p.N, "observations": int(p.K),
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": a.config if scaling == "strong" else f"{a.config} x{world}", "cameras": p.M, "points": p.N, "observations": int(p.K),
                    "loss": ["trivial", "huber", "cauchy"][p.loss], "parallelism": f"camera-partitioned x{world}",
+                   "restart": a.restart,
                    "l2": "inputs larger than L2 (observation streams 1.2 GB, point states 4 x 143 MB)",
                    "F_end": F_end},
         "roofline": roof,

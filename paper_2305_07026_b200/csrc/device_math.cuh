@@ -24,7 +24,7 @@ __device__ __forceinline__ double loss_eval(double s, double delta, double delta
   } else if (LOSS == kCauchy) {
     const double q = s * idelta2;
     if (WANT_RHO) *rho = delta2 * log1p(q);
-    return 1.0 / (1.0 + q);
+    return __drcp_rn(1.0 + q);  // = 1.0 / (1 + q), correctly rounded, without the division's slow-path call
   } else {
     if (WANT_RHO) *rho = s;
     return 1.0;
