@@ -56,7 +56,7 @@ typedef struct {
   double scale;
 } daba_loss;
 
-enum { DABA_COMM_NCCL = 0, DABA_COMM_LOCAL = 1 };
+enum { DABA_COMM_NCCL = 0, DABA_COMM_LOCAL = 1, DABA_COMM_NONE = 2 };
 
 typedef struct {
   double xi;          /* proximal weight xi > 0 of eq. Ealpha; default 1e-4 */
@@ -67,7 +67,10 @@ typedef struct {
   int lm_max_trials;  /* LM trials per camera per anchor, 1..8; default 5 */
   int accelerate;     /* 1: DABA (Nesterov + restart); 0: DUBA ablation, plain MM; default 1 */
   int comm;           /* DABA_COMM_NCCL (one process per GPU) or DABA_COMM_LOCAL (ranks = host threads of one
-                         process sharing a hub; used by tests to run several ranks on one GPU); default NCCL */
+                         process sharing a hub; used by tests to run several ranks on one GPU); default NCCL.
+                         DABA_COMM_NONE is a MEASUREMENT mode: one rank's shard runs alone, the allreduce becomes a
+                         local copy and the halo exchange is skipped — the iterates are NOT the method's; it
+                         times a rank's device work at nranks > 1 on one GPU (tools/shard_scaling.py). */
   int use_graph;      /* 1: capture one iteration as a CUDA graph and replay it; default 1 */
   int profile;        /* 1: record CUDA events around every kernel (see daba_kernel_times); default 0 */
   void* stream;       /* cudaStream_t to launch on (NULL: a stream owned by the context) */

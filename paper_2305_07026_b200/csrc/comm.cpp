@@ -134,6 +134,19 @@ struct Hub {
   }
 };
 
+// NONE (measurement only): one rank's shard without peers.  The allreduce is a local copy (so the iteration's
+// kernels run unchanged), the exchange moves nothing.
+class NoneComm : public Comm {
+ public:
+  std::string allreduce(const double* d_in, double* d_out, int n, cudaStream_t st) override {
+    return cudaMemcpyAsync(d_out, d_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st) == cudaSuccess
+               ? ""
+               : "NONE allreduce: copy failed";
+  }
+  std::string exchange(const double*, double*, const std::vector<PeerSeg>&, cudaStream_t) override { return ""; }
+  bool capturable() const override { return true; }
+};
+
 std::mutex g_hub_mu;
 std::map<std::string, std::weak_ptr<Hub>> g_hubs;
 
@@ -205,6 +218,7 @@ std::string nccl_unique_id(void* id_out) {
 }
 
 Comm* make_comm(int kind, const void* id, int rank, int nranks, std::string* err) {
+  if (kind == 2) return new NoneComm();
   if (kind == 1) {
     std::string key(static_cast<const char*>(id), 128);
     std::shared_ptr<Hub> hub;

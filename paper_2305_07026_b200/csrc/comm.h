@@ -37,7 +37,8 @@ class Comm {
   virtual bool capturable() const = 0;
 };
 
-// Create a communicator.  kind: 0 NCCL, 1 LOCAL.  id: 128 bytes.  Returns nullptr and sets *err on failure.
+// Create a communicator.  kind: 0 NCCL, 1 LOCAL, 2 NONE (measurement only: no peers; see include/daba.h).
+// id: 128 bytes.  Returns nullptr and sets *err on failure.
 Comm* make_comm(int kind, const void* id, int rank, int nranks, std::string* err);
 // ncclGetUniqueId through the dynamically loaded library.
 std::string nccl_unique_id(void* id_out);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,7 +27,7 @@ struct daba_ctx {
   std::string err;
   int device = 0, rank = 0, nranks = 1;
   cudaStream_t stream = nullptr, side = nullptr;  // side: the k_cam_solve branch of an iteration
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork0 = nullptr, ev_join0 = nullptr;
   int num_sms = 148;
   bool own_stream = false;
   daba_options opt{};
@@ -47,6 +48,10 @@ struct daba_ctx {
   cudaGraphExec_t graph = nullptr;
   bool graph_failed = false;
   int launches_per_iter = 0;
+  // parallel graph branches (A/B switches, environment at create): boundary records beside the camera pass
+  // (DABA_FORK0=1; measured slower at 8 ranks: 0.272 vs 0.258 ms), the solve beside the point pass when small
+  // (DABA_FORK1=0 disables)
+  bool fork0 = false, fork1 = true;
   // profiling
   std::vector<std::string> knames;
   std::vector<double> kms;
@@ -72,6 +77,13 @@ void parallel_for(int64_t n, F&& f) {
   std::vector<std::thread> th;
   for (unsigned t = 0; t < hw; ++t) th.emplace_back([&, t] { f(n * t / hw, n * (t + 1) / hw); });
   for (auto& x : th) x.join();
+}
+
+// Integer tuning knob from the environment (create time only), else the default.
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return (int64_t)std::atoll(v);
 }
 
 int fail(daba_ctx* c, int code, const std::string& m) {
@@ -218,13 +230,25 @@ void collect_times(daba_ctx* c) {
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
-  n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
-  n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
-  n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
+  if (!c->opt.profile && c->fork0 && (P.n_boundary > 0 || P.n_inter_blocks > 0)) {
+    // the boundary records and the inter-device terms only read x^k, x-bar^k and the halo: a parallel branch
+    // beside the camera pass
+    CUDA_OR(c, cudaEventRecord(c->ev_fork0, c->stream));
+    CUDA_OR(c, cudaStreamWaitEvent(c->side, c->ev_fork0, 0));
+    n += launch_pt_pass(P, c->side);
+    n += launch_inter(P, c->side);
+    CUDA_OR(c, cudaEventRecord(c->ev_join0, c->side));
+    n += launch_cam_pass(P, c->stream);
+    CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join0, 0));
+  } else {
+    n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
+    n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
+    n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
+  }
   // k_cam_solve and k_pt_sum are independent.  Run them as parallel branches when the solve is small (it then
   // hides behind the point pass); a large solve would crowd the point pass off the SMs (measured: +30 us at
   // 13.7K cameras), so it runs serialised.  Profiling always serialises so events bracket one kernel.
-  if (c->opt.profile || P.n_cam_eval_blocks >= c->num_sms / 2) {
+  if (c->opt.profile || !c->fork1 || P.n_cam_eval_blocks >= c->num_sms / 2) {
     n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
     n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
   } else {
@@ -354,11 +378,15 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   if (!(o.xi > 0) || !(o.eta > 0 && o.eta <= 1) || !(o.lm_mu0 > 0) || !(o.lm_mu_up >= 1) || !(o.eps >= 0) ||
       o.lm_max_trials < 1 || o.lm_max_trials > 8 || o.restart_scope < 0 || o.restart_scope > 1)
     return DABA_E_INVALID_ARG;
-  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm_id)) return DABA_E_INVALID_ARG;
+  if (o.comm < DABA_COMM_NCCL || o.comm > DABA_COMM_NONE) return DABA_E_INVALID_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm_id && o.comm != DABA_COMM_NONE))
+    return DABA_E_INVALID_ARG;
   C->loss = loss;
   C->rank = rank;
   C->nranks = nranks;
   C->device = cuda_device;
+  C->fork0 = env_int("DABA_FORK0", 0) == 1;
+  C->fork1 = std::getenv("DABA_FORK1") == nullptr || std::atoi(std::getenv("DABA_FORK1")) != 0;
   std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan);
   if (!e.empty()) {
     *out = nullptr;
@@ -392,11 +420,14 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   cudaDeviceGetAttribute(&C->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   if (cudaStreamCreateWithFlags(&C->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_fork0, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_join0, cudaEventDisableTiming) != cudaSuccess) {
     daba_destroy(c.release());
     return DABA_E_CUDA;
   }
-  if (nranks > 1 || comm_id) {  // a single rank with a comm id still routes its sums through the communicator
+  if (nranks > 1 || comm_id || o.comm == DABA_COMM_NONE) {  // a single rank with a comm id still routes its
+                                                            // sums through the communicator
     std::string ce;
     C->comm.reset(make_comm(o.comm, comm_id, rank, nranks, &ce));
     if (!C->comm) {
@@ -887,5 +918,7 @@ extern "C" void daba_destroy(daba_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_fork0) cudaEventDestroy(ctx->ev_fork0);
+  if (ctx->ev_join0) cudaEventDestroy(ctx->ev_join0);
   delete ctx;
 }

@@ -487,16 +487,34 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
 
 // Boundary observations (their camera is owned by another rank, N > 1 only): recompute the point-side
 // contribution from the halo camera and write it into the staging record, like the camera pass does.
+// A 128-byte camera record into registers: four 256-bit loads, all in flight together.
+__device__ __forceinline__ void load_cam16(const double* c, double* out) {
+  const double4* q = reinterpret_cast<const double4*>(c);
+  double4 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = ld256(q + k);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    out[4 * k] = v[k].x;
+    out[4 * k + 1] = v[k].y;
+    out[4 * k + 2] = v[k].z;
+    out[4 * k + 3] = v[k].w;
+  }
+}
+
 template <int LOSS>
 __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= p.n_boundary) return;
   const int32_t i = p.b_cam[b], j = p.b_pt[b];
   const double2 u = p.b_uv[b];
-  const double4 lk = p.pts[p.roles[1]][j], lb = p.lbar[p.roles[4]][j];
+  const double4 lk = ld256(p.pts[p.roles[1]] + j), lb = ld256(p.lbar[p.roles[4]] + j);
+  double cb[16], ck[16];
+  load_cam16(p.cbarb[p.roles[4]] + (size_t)i * kCamStride, cb);
+  load_cam16(p.cams[p.roles[1]] + (size_t)i * kCamStride, ck);
   double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  pt_terms<LOSS>(p.cbarb[p.roles[4]] + (size_t)i * kCamStride, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
-  pt_terms<LOSS>(p.cams[p.roles[1]] + (size_t)i * kCamStride, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
+  pt_terms<LOSS>(cb, lb.x, lb.y, lb.z, u, p, a[0], a[1], a[2], a[3]);
+  pt_terms<LOSS>(ck, lk.x, lk.y, lk.z, u, p, a[4], a[5], a[6], a[7]);
   const int64_t r = p.n_cam_side + b;
   *rec_ptr(p, r, 0) = make_double4(a[0], a[1], a[2], a[3]);
   *rec_ptr(p, r, 1) = make_double4(a[4], a[5], a[6], a[7]);
@@ -1063,16 +1081,18 @@ __global__ void k_lbar_all(IterParams p) {
 __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                        const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  // before the decision: [acc | mm] candidates; after a local decision (selected): [x^{k+1} | x^{k+1}]
+  // before the decision: [acc | mm] candidates; after a local decision (selected): [x^{k+1} | x^{k+1}].
+  // Cameras: one warp per camera, one double per lane; points: one thread per point.
   const int ra = selected ? p.roles[1] : p.roles[2], rm = selected ? p.roles[1] : p.roles[3];
-  if (t < n_cam) {
-    const double* ca = p.cams[ra] + (size_t)cam_idx[t] * kCamStride;
-    const double* cm = p.cams[rm] + (size_t)cam_idx[t] * kCamStride;
-    double* b = buf + cam_off[t];
-    for (int k = 0; k < 15; ++k) b[k] = ca[k];
-    for (int k = 0; k < 15; ++k) b[15 + k] = cm[k];
-  } else if (t < n_cam + n_pt) {
-    const int q = t - n_cam;
+  const int n_cam_threads = 32 * n_cam;
+  if (t < n_cam_threads) {
+    const int e = t >> 5, c = t & 31;
+    if (c < 30) {
+      const double v = (c < 15 ? p.cams[ra] : p.cams[rm])[(size_t)cam_idx[e] * kCamStride + (c < 15 ? c : c - 15)];
+      buf[cam_off[e] + c] = v;
+    }
+  } else if (t < n_cam_threads + n_pt) {
+    const int q = t - n_cam_threads;
     const double4 la = p.pts[ra][pt_idx[q]], lm = p.pts[rm][pt_idx[q]];
     double* b = buf + pt_off[q];
     b[0] = la.x;
@@ -1095,9 +1115,14 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
     const size_t i = (size_t)cam_idx[t] * kCamStride;
     double* c = p.cams[p.roles[1]] + i;
     const double* src = buf + cam_off[t] + 15 * sel;
-    for (int k = 0; k < 15; ++k) c[k] = src[k];
-    c[15] = 0.0;
-    extrapolate_camera(c, p.cams[p.roles[0]] + i, gamma, p.cbarb[p.roles[4]] + i);
+    double v[16], prev[16];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) v[k] = src[k];  // all loads in flight before any store
+    v[15] = 0.0;
+    load_cam16(p.cams[p.roles[0]] + i, prev);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = v[k];
+    extrapolate_camera(v, prev, gamma, p.cbarb[p.roles[4]] + i);
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
     const double* b = buf + pt_off[q] + 3 * sel;
@@ -1188,8 +1213,8 @@ int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_
                 const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected,
                 cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_pack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
-                                                    selected);
+  k_pack<<<blocks(32 * (int64_t)n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt,
+                                                                  buf, selected);
   return 1;
 }
 

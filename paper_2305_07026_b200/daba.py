@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("DABA_LIB", os.path.join(_HERE, "libdaba.so"))
 _lib = None
 
 LOSS_TRIVIAL, LOSS_HUBER, LOSS_CAUCHY = 0, 1, 2
-COMM_NCCL, COMM_LOCAL = 0, 1
+COMM_NCCL, COMM_LOCAL, COMM_NONE = 0, 1, 2
 (TR_F, TR_FBAR, TR_EACC, TR_RESTART, TR_EMM, TR_STEP2, TR_GAMMA, TR_NDEGEN, TR_NOACC_ACC, TR_NOACC_MM, TR_FDEV,
  TRACE_COLS) = range(12)
 RESTART_GLOBAL, RESTART_DEVICE = 0, 1
