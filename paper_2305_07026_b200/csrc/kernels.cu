@@ -524,7 +524,13 @@ __device__ void do_select(const IterParams& p);
 
 // Rank-local sums of the camera partials (k_cam_solve blocks, 8 columns) and point partials (k_pt_sum blocks,
 // 4 columns) in a fixed order by one block (any power-of-two size <= 256) -> p.local (a9).
-__device__ void final_reduce(const IterParams& p) {
+// (noinline, arguments by value: its registers stay out of the kernels' allocation and no parameter copy)
+struct FinalArgs {
+  const double *cam_part, *pt_part, *inter_part;
+  int32_t n_cam_eval_blocks, n_pt_blocks, n_inter_blocks;
+  double* local;
+};
+__device__ __noinline__ void final_reduce(const FinalArgs p) {
   __shared__ double s[8][kGlobalCols];  // one row per warp (blockDim.x <= 256)
   const int nt = blockDim.x;
   double v[kGlobalCols];
@@ -578,7 +584,8 @@ __device__ void finish_block(const IterParams& p) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  final_reduce(p);
+  final_reduce(FinalArgs{p.cam_part, p.pt_part, p.inter_part, p.n_cam_eval_blocks, p.n_pt_blocks, p.n_inter_blocks,
+                         p.local});
   if (threadIdx.x == 0) {
     *p.counter = 0;
     __threadfence();
