@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -86,6 +87,18 @@ int64_t env_int(const char* name, int64_t dflt) {
   return (int64_t)std::atoll(v);
 }
 
+// Create-time phase timer (DABA_TIMING=1 prints the host cost of each phase of daba_create to stderr).
+struct PhaseTimer {
+  bool on = std::getenv("DABA_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "daba_create %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 int fail(daba_ctx* c, int code, const std::string& m) {
   if (c) c->err = m;
   return code;
@@ -109,8 +122,8 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
   return DABA_OK;
 }
 
-template <class T>
-int upload(daba_ctx* c, T** p, const std::vector<T>& h) {
+template <class T, class A>
+int upload(daba_ctx* c, T** p, const std::vector<T, A>& h) {
   int rc = dalloc(c, p, h.size());
   if (rc) return rc;
   if (!h.empty()) CUDA_OR(c, cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
@@ -307,29 +320,33 @@ int compute_objective(daba_ctx* c, double* F, double* ndeg) {
 int upload_states(daba_ctx* c, const double* cams_k, const double* pts_k, const double* cams_km1,
                   const double* pts_km1, int rk, int rkm1) {
   const ShardPlan& S = c->plan;
-  std::vector<double> hc(S.cam_g.size() * kCamStride), hp(S.pt_g.size() * 4);
+  int h_roles[4];
+  CUDA_OR(c, cudaMemcpyAsync(h_roles, c->P.roles, sizeof h_roles, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR(c, cudaStreamSynchronize(c->stream));
+  hvec<double> hc(S.cam_g.size() * kCamStride), hp(S.pt_g.size() * 4);
   for (int pass = 0; pass < 2; ++pass) {
     const double* gc = pass ? cams_km1 : cams_k;
     const double* gp = pass ? pts_km1 : pts_k;
-    for (size_t li = 0; li < S.cam_g.size(); ++li) {
-      std::memcpy(&hc[li * kCamStride], gc + 15 * (size_t)S.cam_g[li], 15 * sizeof(double));
-      hc[li * kCamStride + 15] = 0.0;
-    }
-    for (size_t lj = 0; lj < S.pt_g.size(); ++lj) {
-      for (int k = 0; k < 3; ++k) hp[lj * 4 + k] = gp[3 * (size_t)S.pt_g[lj] + k];
-      hp[lj * 4 + 3] = 0.0;
-    }
+    parallel_for((int64_t)S.cam_g.size(), [&](int64_t a, int64_t b) {
+      for (int64_t li = a; li < b; ++li) {
+        std::memcpy(&hc[(size_t)li * kCamStride], gc + 15 * (size_t)S.cam_g[(size_t)li], 15 * sizeof(double));
+        hc[(size_t)li * kCamStride + 15] = 0.0;
+      }
+    });
+    parallel_for((int64_t)S.pt_g.size(), [&](int64_t a, int64_t b) {
+      for (int64_t lj = a; lj < b; ++lj) {
+        for (int k = 0; k < 3; ++k) hp[(size_t)lj * 4 + k] = gp[3 * (size_t)S.pt_g[(size_t)lj] + k];
+        hp[(size_t)lj * 4 + 3] = 0.0;
+      }
+    });
     const int role = pass ? rkm1 : rk;
-    int h_roles[4];
-    CUDA_OR(c, cudaMemcpyAsync(h_roles, c->P.roles, sizeof h_roles, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OR(c, cudaStreamSynchronize(c->stream));
     if (!hc.empty())
       CUDA_OR(c, cudaMemcpyAsync(c->P.cams[h_roles[role]], hc.data(), hc.size() * sizeof(double),
                                  cudaMemcpyHostToDevice, c->stream));
     if (!hp.empty())
       CUDA_OR(c, cudaMemcpyAsync(c->P.pts[h_roles[role]], hp.data(), hp.size() * sizeof(double),
                                  cudaMemcpyHostToDevice, c->stream));
-    CUDA_OR(c, cudaStreamSynchronize(c->stream));
+    CUDA_OR(c, cudaStreamSynchronize(c->stream));  // the host buffers are refilled by the next pass
   }
   return DABA_OK;
 }
@@ -387,11 +404,13 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   C->device = cuda_device;
   C->fork0 = env_int("DABA_FORK0", 0) == 1;
   C->fork1 = std::getenv("DABA_FORK1") == nullptr || std::atoi(std::getenv("DABA_FORK1")) != 0;
+  PhaseTimer timer;
   std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan);
   if (!e.empty()) {
     *out = nullptr;
     return DABA_E_INVALID_ARG;
   }
+  timer.mark("plan_shard");
   // native cameras and Assumption 2 at x^0
   std::vector<double> nat((size_t)M * 15);
   for (int64_t i = 0; i < M; ++i) {
@@ -409,6 +428,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
   });
   if (degenerate) return DABA_E_DEGENERATE;
+  timer.mark("native + Assumption 2");
   // device and stream
   if (cudaSetDevice(cuda_device) != cudaSuccess) return DABA_E_CUDA;
   if (o.stream) {
@@ -474,18 +494,31 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     std::vector<int32_t> roles = {0, 1, 2, 3, 0};
     if ((rc = upload(C, &P.roles, roles))) return bail(rc);
   }
+  timer.mark("device, stream, comm");
   // camera side + chunks
   {
     const size_t kc = S.c_obs.size();
-    std::vector<double2> uv(kc);
-    parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
-      for (int64_t q = a; q < b; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
-    });
-    const double2* duv;
-    if ((rc = upload(C, const_cast<double2**>(&duv), uv))) return bail(rc);
+    double2* duv;
+    int32_t* dpt;
+    if ((rc = dalloc(C, &duv, kc)) || (rc = dalloc(C, &dpt, kc))) return bail(rc);
+    if (S.cam_side_identity) {
+      // one rank, input sorted by (camera, point): the camera side is the input itself (no host copies)
+      if (kc) {
+        CUDA_OR(C, cudaMemcpyAsync(duv, obs_uv, kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
+        CUDA_OR(C, cudaMemcpyAsync(dpt, obs_pt, kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
+      }
+    } else {
+      hvec<double2> uv(kc);
+      parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
+      });
+      if (kc) {
+        CUDA_OR(C, cudaMemcpyAsync(duv, uv.data(), kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
+        CUDA_OR(C, cudaMemcpyAsync(dpt, S.c_pt.data(), kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
+      }
+      CUDA_OR(C, cudaStreamSynchronize(C->stream));  // uv is freed at the end of this scope
+    }
     P.c_uv = duv;
-    const int32_t* dpt;
-    if ((rc = upload(C, const_cast<int32_t**>(&dpt), S.c_pt))) return bail(rc);
     P.c_pt = dpt;
     std::vector<CamChunk> chunks;
     std::vector<int32_t> cptr(1, 0);
@@ -510,6 +543,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return bail(rc);
     P.cam_chunk_ptr = dcp;
   }
+  timer.mark("camera side");
   // point side: records written by the camera pass at its observation index; boundary observations (camera
   // owned elsewhere) are recomputed into records n_cam_side + b
   {
@@ -517,16 +551,26 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     const int64_t* dptr;
     if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
     P.p_ptr = dptr;
-    std::vector<int32_t> cam_side_of((size_t)K, -1);
-    parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
-      for (int64_t q = a; q < b; ++q) cam_side_of[(size_t)S.c_obs[q]] = (int32_t)q;
-    });
-    std::vector<int32_t> src(kp), bcam, bpt;
+    hvec<int32_t> src(kp);
+    std::vector<int32_t> bcam, bpt;
     std::vector<double2> buv;
-    parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
-      for (int64_t q = a; q < b; ++q) src[q] = cam_side_of[(size_t)S.p_obs[q]];
-    });
-    for (size_t q = 0; q < kp; ++q) {
+    if (S.cam_side_identity) {  // the camera-side index of observation o is o
+      parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) src[q] = S.p_obs[q];
+      });
+    } else {
+      hvec<int32_t> cam_side_of((size_t)K);
+      parallel_for(K, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) cam_side_of[(size_t)q] = -1;
+      });
+      parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) cam_side_of[(size_t)S.c_obs[q]] = (int32_t)q;
+      });
+      parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) src[q] = cam_side_of[(size_t)S.p_obs[q]];
+      });
+    }
+    for (size_t q = 0; q < (S.cam_side_identity ? 0 : kp); ++q) {
       if (src[q] >= 0) continue;  // written by this rank's camera pass
       src[q] = (int32_t)(kc + bcam.size());
       bcam.push_back(S.p_cam[q]);
@@ -579,6 +623,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
     P.n_pt_blocks = std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, 148 * 8));
   }
+  timer.mark("point side");
   // scratch
   P.n_cam_eval_blocks = (2 * P.n_own_cams + 127) / 128;  // k_cam_solve blocks
   P.trace_cap = 1024;
@@ -594,6 +639,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   if ((rc = dalloc(C, &P.sched, 8))) return bail(rc);
   if (!C->comm) P.global = P.local;
   cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
+  timer.mark("scratch");
   // halo plan: per peer a segment [cameras x 15 | points x 3] of the send / receive buffers; the pack and unpack
   // items of all peers are flattened so that one kernel does each
   if (nranks > 1) {
@@ -640,11 +686,13 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
         (rc = dalloc(C, &C->d_recvbuf, (size_t)std::max<int64_t>(roff, 1))))
       return bail(rc);
   }
+  timer.mark("halo plan");
   // state: x^{-1} = x^0 (Alg. 1)
   {
     rc = upload_states(C, nat.data(), points, nat.data(), points, 1, 0);
     if (rc) return bail(rc);
   }
+  timer.mark("states");
   // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
   double F0 = 0, nd = 0;
   if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
@@ -666,6 +714,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     launch_lbar_all(P, C->stream);  // x-bar^0 = x^0 (gamma^{(0)} = 0)
     if (cudaStreamSynchronize(C->stream) != cudaSuccess) return bail(DABA_E_CUDA);
   }
+  timer.mark("objective, x-bar");
   // launches per iteration (for bookkeeping)
   C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) + (C->comm ? 1 : 0) +
                          (P.n_inter_blocks > 0);

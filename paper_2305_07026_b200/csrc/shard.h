@@ -11,10 +11,35 @@
 #pragma once
 #include <stdint.h>
 
+#include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace daba {
+
+// Allocator whose value-less construct default-initialises (no zero fill): large host arrays are first touched
+// by the parallel loops that fill them instead of by a serial memset.
+template <class T>
+struct NoInit : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInit<U>;
+  };
+  NoInit() = default;
+  template <class U>
+  NoInit(const NoInit<U>&) {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using hvec = std::vector<T, NoInit<T>>;
 
 struct Peer {
   int rank;
@@ -29,12 +54,13 @@ struct ShardPlan {
   std::vector<int32_t> cam_g, pt_g;             // local -> global ids: owned (ascending) then halo (ascending)
   int32_t n_own_cams = 0, n_own_pts = 0;
   // camera side (sorted by camera, then point): local camera, local point, global observation id
-  std::vector<int32_t> c_cam, c_pt;
-  std::vector<int32_t> c_obs;
+  hvec<int32_t> c_cam, c_pt;
+  hvec<int32_t> c_obs;
+  bool cam_side_identity = false;               // c_obs[q] = q, c_pt = obs_pt, c_cam = obs_cam (1 rank, sorted)
   std::vector<int64_t> cam_ptr;                 // n_own_cams + 1 offsets into the camera side
   // point side (sorted by point, then camera)
-  std::vector<int32_t> p_cam, p_pt;
-  std::vector<int32_t> p_obs;
+  hvec<int32_t> p_cam, p_pt;
+  hvec<int32_t> p_obs;
   std::vector<int64_t> pt_ptr;                  // n_own_pts + 1
   std::vector<Peer> peers;
   int64_t send_doubles = 0, recv_doubles = 0;   // per iteration
