@@ -411,6 +411,11 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     return DABA_E_INVALID_ARG;
   }
   timer.mark("plan_shard");
+  {  // point numbering for locality (shard.h); DABA_POINT_ORDER = 0 off, 1 automatic (default), 2 always
+    const int64_t po = env_int("DABA_POINT_ORDER", 1);
+    if (po != 0) order_owned_points(&C->plan, obs_cam, po == 2);
+  }
+  timer.mark("point order");
   // native cameras and Assumption 2 at x^0
   std::vector<double> nat((size_t)M * 15);
   for (int64_t i = 0; i < M; ++i) {
@@ -501,21 +506,16 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     double2* duv;
     int32_t* dpt;
     if ((rc = dalloc(C, &duv, kc)) || (rc = dalloc(C, &dpt, kc))) return bail(rc);
+    if (kc) CUDA_OR(C, cudaMemcpyAsync(dpt, S.c_pt.data(), kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
     if (S.cam_side_identity) {
-      // one rank, input sorted by (camera, point): the camera side is the input itself (no host copies)
-      if (kc) {
-        CUDA_OR(C, cudaMemcpyAsync(duv, obs_uv, kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
-        CUDA_OR(C, cudaMemcpyAsync(dpt, obs_pt, kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
-      }
+      // one rank, input sorted by (camera, point): the camera-side pixels are the input itself (no host copy)
+      if (kc) CUDA_OR(C, cudaMemcpyAsync(duv, obs_uv, kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
     } else {
       hvec<double2> uv(kc);
       parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
         for (int64_t q = a; q < b; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
       });
-      if (kc) {
-        CUDA_OR(C, cudaMemcpyAsync(duv, uv.data(), kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
-        CUDA_OR(C, cudaMemcpyAsync(dpt, S.c_pt.data(), kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
-      }
+      if (kc) CUDA_OR(C, cudaMemcpyAsync(duv, uv.data(), kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
       CUDA_OR(C, cudaStreamSynchronize(C->stream));  // uv is freed at the end of this scope
     }
     P.c_uv = duv;

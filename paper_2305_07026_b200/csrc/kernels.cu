@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterPar
     cam_pass_body<LOSS, true>(p, ch, acc, ring, sidx);
   else
     cam_pass_body<LOSS, false>(p, ch, acc, ring, sidx);
+
   __syncthreads();  // the ring is reused as the reduction buffer
   block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride, smem);
 }

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <thread>
@@ -344,6 +345,88 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
     }
   }
   return "";
+}
+
+bool order_owned_points(ShardPlan* S, const int32_t* obs_cam, bool force) {
+  const int32_t np = S->n_own_pts;
+  if (np < 2) return false;
+  // key: smallest global camera observing the point (M if none)
+  std::vector<int32_t> key((size_t)np);
+  pfor(np, [&](int64_t a, int64_t b, int) {
+    for (int64_t j = a; j < b; ++j) {
+      int32_t m = (int32_t)S->M;
+      for (int64_t q = S->pt_ptr[(size_t)j]; q < S->pt_ptr[(size_t)j + 1]; ++q)
+        m = std::min(m, obs_cam[S->p_obs[(size_t)q]]);
+      key[(size_t)j] = m;
+    }
+  });
+  // keep a numbering that already follows the cameras: consecutive points whose smallest cameras lie far apart
+  // (> 1024 camera ids) are rare in it (cluster changes), common in a scattered one
+  std::atomic<int64_t> jumps(0);
+  pfor(np - 1, [&](int64_t a, int64_t b, int) {
+    int64_t d = 0;
+    for (int64_t j = a; j < b; ++j) d += std::abs(key[(size_t)j + 1] - key[(size_t)j]) > 1024;
+    jumps += d;
+  });
+  if (!force && jumps.load() * 4 < (int64_t)np) return false;
+  // stable counting sort by key (owned points ascend by global id already)
+  std::vector<int64_t> start((size_t)S->M + 2, 0);
+  for (int32_t j = 0; j < np; ++j) ++start[(size_t)key[(size_t)j] + 1];
+  for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+  std::vector<int32_t> order((size_t)np), inv((size_t)np);
+  for (int32_t j = 0; j < np; ++j) order[(size_t)start[(size_t)key[(size_t)j]]++] = j;
+  pfor(np, [&](int64_t a, int64_t b, int) {
+    for (int64_t q = a; q < b; ++q) inv[(size_t)order[(size_t)q]] = (int32_t)q;
+  });
+  {
+    std::vector<int32_t> g((size_t)np);
+    for (int32_t q = 0; q < np; ++q) g[(size_t)q] = S->pt_g[(size_t)order[(size_t)q]];
+    std::copy(g.begin(), g.end(), S->pt_g.begin());
+  }
+  // camera side: new point ids, each camera's observations re-sorted by them (records of points with
+  // neighbouring ids become neighbours)
+  pfor(S->n_own_cams, [&](int64_t a, int64_t b, int) {
+    std::vector<std::pair<int32_t, int32_t>> seg;
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t lo = S->cam_ptr[(size_t)i], hi = S->cam_ptr[(size_t)i + 1];
+      seg.clear();
+      for (int64_t q = lo; q < hi; ++q) {
+        const int32_t j = S->c_pt[(size_t)q];
+        seg.emplace_back(j < np ? inv[(size_t)j] : j, S->c_obs[(size_t)q]);
+      }
+      std::sort(seg.begin(), seg.end());
+      for (int64_t q = lo; q < hi; ++q) {
+        S->c_pt[(size_t)q] = seg[(size_t)(q - lo)].first;
+        S->c_obs[(size_t)q] = seg[(size_t)(q - lo)].second;
+      }
+    }
+  }, (int64_t)S->c_obs.size());
+  S->cam_side_identity = false;
+  // point-side rows in the new order
+  std::vector<int64_t> ptr((size_t)np + 1, 0);
+  for (int32_t q = 0; q < np; ++q) {
+    const int32_t j = order[(size_t)q];
+    ptr[(size_t)q + 1] = ptr[(size_t)q] + (S->pt_ptr[(size_t)j + 1] - S->pt_ptr[(size_t)j]);
+  }
+  hvec<int32_t> pc(S->p_cam.size()), pp(S->p_pt.size()), po(S->p_obs.size());
+  pfor(np, [&](int64_t a, int64_t b, int) {
+    for (int64_t q = a; q < b; ++q) {
+      const int32_t j = order[(size_t)q];
+      int64_t d = ptr[(size_t)q];
+      for (int64_t r = S->pt_ptr[(size_t)j]; r < S->pt_ptr[(size_t)j + 1]; ++r, ++d) {
+        pc[(size_t)d] = S->p_cam[(size_t)r];
+        pp[(size_t)d] = (int32_t)q;
+        po[(size_t)d] = S->p_obs[(size_t)r];
+      }
+    }
+  }, (int64_t)S->p_obs.size());
+  S->pt_ptr.swap(ptr);
+  S->p_cam.swap(pc);
+  S->p_pt.swap(pp);
+  S->p_obs.swap(po);
+  for (Peer& pe : S->peers)
+    for (int32_t& j : pe.send_pts) j = inv[(size_t)j];
+  return true;
 }
 
 }  // namespace daba

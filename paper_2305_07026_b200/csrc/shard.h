@@ -56,7 +56,7 @@ struct ShardPlan {
   // camera side (sorted by camera, then point): local camera, local point, global observation id
   hvec<int32_t> c_cam, c_pt;
   hvec<int32_t> c_obs;
-  bool cam_side_identity = false;               // c_obs[q] = q, c_pt = obs_pt, c_cam = obs_cam (1 rank, sorted)
+  bool cam_side_identity = false;               // c_obs[q] = q (1 rank, input sorted by (camera, point))
   std::vector<int64_t> cam_ptr;                 // n_own_cams + 1 offsets into the camera side
   // point side (sorted by point, then camera)
   hvec<int32_t> p_cam, p_pt;
@@ -65,6 +65,15 @@ struct ShardPlan {
   std::vector<Peer> peers;
   int64_t send_doubles = 0, recv_doubles = 0;   // per iteration
 };
+
+// Renumber the owned points by (smallest observing camera id, global id) when the input numbering does not
+// follow the cameras (a quarter or more of consecutive points have smallest cameras > 1024 ids apart), and
+// re-sort each camera's observations by the new ids: points seen by the same cameras get neighbouring ids and
+// their records neighbouring slots.  Measured on Final-13682 with randomly numbered points: point pass 1.17 ->
+// 0.58 ms, camera pass 0.88 -> 0.76 ms, for ≈ 0.4 s more in daba_create.  The generator's host-camera numbering
+// is kept (renumbering it would save 0.04 ms per iteration for the same create cost).  Returns whether it
+// renumbered.
+bool order_owned_points(ShardPlan* plan, const int32_t* obs_cam, bool force = false);
 
 // Build rank `rank`'s shard.  cam_owner/pt_owner may be null (defaults above).  Returns "" or an error message
 // (index out of range, duplicate (i,j), owner out of range).

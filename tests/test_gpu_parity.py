@@ -447,3 +447,19 @@ def test_device_restart_parity(name, nranks, eta):
     assert max(state_errors(cams, pts, co, lo)) <= X_TOL
     if eta == 1.0:
         assert fired > 0
+
+
+def test_point_renumbering_path(monkeypatch):
+    """The engine's locality renumbering of owned points (shard.h order_owned_points), forced on a shuffled
+    problem, at 1 and 3 ranks: the iterates are the oracle's."""
+    monkeypatch.setenv("DABA_POINT_ORDER", "2")
+    p = gen.generate("small_cauchy", shuffle_points=True)
+    o = oracle_for(p)
+    tro = o.iterate(20)
+    co, lo = o.state(0)
+    with solver(p) as s:
+        trg = s.iterate_trace(20)
+        assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
+        assert max(state_errors(*s.state_native(0)[:2], co, lo)) <= X_TOL
+    _, cams, pts, _ = run_ranks(p, 3, 20)
+    assert max(state_errors(cams, pts, co, lo)) <= X_TOL
