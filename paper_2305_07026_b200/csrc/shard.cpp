@@ -34,7 +34,7 @@ unsigned nthreads(int64_t n) {
 }
 
 // Stable sort of observation ids by key (0..nkeys-1); ptr gets nkeys+1 offsets.  Parallel LSD radix sort on
-// (key, id) pairs, 11 bits per pass: per-thread digit histograms over contiguous input slices, then a stable
+// (key, id) pairs, <= 13 bits per pass (two passes up to 2^26 keys): per-thread digit histograms over contiguous input slices, then a stable
 // scatter (thread t writes its slice's elements in order after threads < t) — sequential streams, no atomics.
 void bucket(int64_t nkeys, const hvec<int32_t>& ids, const int32_t* key, std::vector<int64_t>& ptr,
             hvec<int32_t>& out) {
@@ -48,7 +48,8 @@ void bucket(int64_t nkeys, const hvec<int32_t>& ids, const int32_t* key, std::ve
   });
   int bits = 1;
   while ((int64_t(1) << bits) < nkeys) ++bits;
-  constexpr int R = 11, B = 1 << R;
+  const int passes = (bits + 12) / 13;               // <= 13 bits per pass (8192 buckets per thread)
+  const int R = (bits + passes - 1) / passes, B = 1 << R;
   const unsigned T = nthreads(n);
   std::vector<int64_t> hist((size_t)T * B);
   for (int shift = 0; shift < bits; shift += R) {
