@@ -279,7 +279,7 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
     // k_select decides on the allreduced sums; per device: the rank has decided already (last block of
     // k_cam_solve) and sends x^{k+1}; the allreduce only feeds the trace
     const bool dev = P.restart_scope == 1;
-    if (halo)
+    if (halo && !P.sendbuf)  // (global test: the solves already wrote the send buffer)
       n += timed(c, "k_pack", [&] {
         return launch_pack(P, c->d_send_cam, c->d_send_cam_off, c->n_send_cam, c->d_send_pt, c->d_send_pt_off,
                            c->n_send_pt, c->d_sendbuf, dev ? 1 : 0, c->stream);
@@ -287,14 +287,16 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
     std::string e = c->comm->allreduce_exchange(P.local, P.global, kGlobalCols, c->d_sendbuf, c->d_recvbuf,
                                                 halo ? c->segs : std::vector<PeerSeg>(), c->stream);
     if (!e.empty()) return fail(c, DABA_E_NCCL, e);
+    // the global decision is taken inside k_unpack when there is one; otherwise by k_select
+    const bool unpack = c->n_recv_cam + c->n_recv_pt > 0;
     if (dev)
       n += timed(c, "k_trace_post", [&] { return launch_trace_post(P, c->stream); });
-    else
+    else if (!unpack)
       n += timed(c, "k_select", [&] { return launch_select(P, c->stream); });
-    if (halo)
+    if (unpack)
       n += timed(c, "k_unpack", [&] {
         return launch_unpack(P, c->d_recv_cam, c->d_recv_cam_off, c->n_recv_cam, c->d_recv_pt, c->d_recv_pt_off,
-                             c->n_recv_pt, c->d_recvbuf, c->stream);
+                             c->n_recv_pt, c->d_recvbuf, dev ? 0 : 1, c->stream);
       });
   }
   *launches += n;
@@ -685,6 +687,33 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = dalloc(C, &C->d_sendbuf, (size_t)std::max<int64_t>(soff, 1))) ||
         (rc = dalloc(C, &C->d_recvbuf, (size_t)std::max<int64_t>(roff, 1))))
       return bail(rc);
+    // global test: the solves write both candidates into the send slots themselves (no k_pack); per owned
+    // variable the list of its slots
+    if (P.restart_scope == 0 && !C->segs.empty()) {
+      auto csr = [](int32_t n, const std::vector<int32_t>& idx, const std::vector<int64_t>& off,
+                    std::vector<int32_t>& ptr, std::vector<int64_t>& o) {
+        ptr.assign((size_t)n + 1, 0);
+        for (int32_t v : idx) ++ptr[(size_t)v + 1];
+        for (int32_t v = 0; v < n; ++v) ptr[(size_t)v + 1] += ptr[(size_t)v];
+        o.resize(idx.size());
+        std::vector<int32_t> pos(ptr.begin(), ptr.end() - 1);
+        for (size_t q = 0; q < idx.size(); ++q) o[(size_t)pos[(size_t)idx[q]]++] = off[q];
+      };
+      std::vector<int32_t> cptr_s, pptr_s;
+      std::vector<int64_t> coff_s, poff_s;
+      csr(P.n_own_cams, sc, sco, cptr_s, coff_s);
+      csr(P.n_own_pts, sp, spo, pptr_s, poff_s);
+      const int32_t *a0, *a2;
+      const int64_t *a1, *a3;
+      if ((rc = upload(C, const_cast<int32_t**>(&a0), cptr_s)) || (rc = upload(C, const_cast<int64_t**>(&a1), coff_s)) ||
+          (rc = upload(C, const_cast<int32_t**>(&a2), pptr_s)) || (rc = upload(C, const_cast<int64_t**>(&a3), poff_s)))
+        return bail(rc);
+      P.cam_send_ptr = a0;
+      P.cam_send_off = a1;
+      P.pt_send_ptr = a2;
+      P.pt_send_off = a3;
+      P.sendbuf = C->d_sendbuf;
+    }
   }
   timer.mark("halo plan");
   // state: x^{-1} = x^0 (Alg. 1)
@@ -716,9 +745,12 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   }
   timer.mark("objective, x-bar");
   // launches per iteration (for bookkeeping)
-  C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) + (C->comm ? 1 : 0) +
-                         (P.n_inter_blocks > 0);
-  C->launches_per_iter += (C->n_send_cam + C->n_send_pt > 0) + (C->n_recv_cam + C->n_recv_pt > 0);
+  {
+    const bool unpack = C->n_recv_cam + C->n_recv_pt > 0, dev = P.restart_scope == 1;
+    C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) +
+                           (P.n_inter_blocks > 0) + (C->comm && (dev || !unpack) ? 1 : 0) +
+                           (C->n_send_cam + C->n_send_pt > 0 && !P.sendbuf) + unpack;
+  }
   *out = c.release();
   return DABA_OK;
 }

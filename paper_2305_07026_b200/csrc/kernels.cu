@@ -472,6 +472,16 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
   const double nx = lk[0] + mx, ny = lk[1] + my, nz = lk[2] + mz;
   p.pts[p.roles[3]][j] = make_double4(nx, ny, nz, 0.0);
   // x-bar^{k+1} for either outcome of the restart test (eq. nesterov_l with gamma^{(k+1)}); k_select keeps one
+  if (p.sendbuf)  // boundary point: both candidates straight into its halo send slots
+    for (int s = p.pt_send_ptr[j]; s < p.pt_send_ptr[j + 1]; ++s) {
+      double* b = p.sendbuf + p.pt_send_off[s];
+      b[0] = ax;
+      b[1] = ay;
+      b[2] = az;
+      b[3] = nx;
+      b[4] = ny;
+      b[5] = nz;
+    }
   const double g1 = sched_gamma_next(p.sched[0], p.accelerate);
   p.lbar[0][j] = make_double4(fma(g1, ax - lk[0], ax), fma(g1, ay - lk[1], ay), fma(g1, az - lk[2], az), 0.0);
   p.lbar[1][j] = make_double4(fma(g1, nx - lk[0], nx), fma(g1, ny - lk[1], ny), fma(g1, nz - lk[2], nz), 0.0);
@@ -878,6 +888,9 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
     double* dst = p.cams[p.roles[2 + a]] + (size_t)i * kCamStride;
     for (int k = 0; k < 15; ++k) dst[k] = out[k];
     dst[15] = 0.0;
+    if (p.sendbuf)  // boundary camera: this anchor's candidate straight into its halo send slots
+      for (int s = p.cam_send_ptr[i]; s < p.cam_send_ptr[i + 1]; ++s)
+        for (int k = 0; k < 15; ++k) p.sendbuf[p.cam_send_off[s] + 15 * a + k] = out[k];
     p.decisions[2 * i + a] = accepted;
     // x-bar^{k+1} of this candidate (used if the restart test selects it): eqs. nesterov_x with gamma^{(k+1)}
     double cb[16];
@@ -925,6 +938,15 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
 }
 
 // ------------------------------------------------------------------ a9 + a10: restart test and selection
+// The global test alone (D2), on the allreduced sums — the same arithmetic as do_select.
+__device__ __forceinline__ bool restart_decision(const IterParams& p) {
+  const double* G = p.global;
+  const double F = G[0];
+  const double Fbar = (1.0 - p.eta) * p.sched[1] + p.eta * F;
+  const double Eacc = F + (G[1] + G[2]);
+  return p.accelerate ? (Eacc > Fbar) : true;
+}
+
 __device__ void do_select(const IterParams& p) {
   double s_next;
   const double gamma = sched_gamma(p.sched[0], p.accelerate, &s_next);
@@ -938,7 +960,8 @@ __device__ void do_select(const IterParams& p) {
   const double Fbar = (1.0 - p.eta) * p.sched[1] + p.eta * F;  // eq. lFak
   const double Eacc = F + (G[1] + G[2]);                        // eq. Eak: E(x_acc | x^k)
   const double Emm = F + (G[3] + G[4]);
-  const bool restart = p.accelerate ? (Eacc > Fbar) : true;     // Alg. 1, strict ">"
+  // Alg. 1, strict ">"; the global test through restart_decision so that k_unpack's copy agrees bitwise
+  const bool restart = dev ? (p.accelerate ? (Eacc > Fbar) : true) : restart_decision(p);
   const int64_t k = (int64_t)p.sched[2];
   double* tr = p.trace + (size_t)(k % p.trace_cap) * kTraceCols;
   tr[0] = dev ? G[0] + G[10] : F;  // per device with a communicator: replaced by the global F in k_trace_post
@@ -1122,29 +1145,56 @@ __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_
 // After the restart decision (roles rotated, roles[4] = 1 iff the MM candidate was kept): the selected candidate
 // becomes the halo entry of x^{k+1}, and its x-bar^{k+1} is formed from the cached x^k (eqs. nesterov_x).
 __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                         const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf) {
+                         const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf,
+                         int select_inside) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const double gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
-  const int sel = p.roles[4];
+  // after the decision: x^{k+1} = roles[1], x^k = roles[0], x-bar buffer roles[4], gamma^{(k+1)} from s^{(k+1)};
+  // with select_inside the decision is still to be committed: every thread derives the same outcome
+  int sel, r_new, r_old;
+  double gamma;
+  if (select_inside) {
+    const bool restart = restart_decision(p);
+    sel = restart ? 1 : 0;
+    r_new = restart ? p.roles[3] : p.roles[2];
+    r_old = p.roles[1];
+    gamma = sched_gamma_next(p.sched[0], p.accelerate);
+  } else {
+    sel = p.roles[4];
+    r_new = p.roles[1];
+    r_old = p.roles[0];
+    gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
+  }
   if (t < n_cam) {
     const size_t i = (size_t)cam_idx[t] * kCamStride;
-    double* c = p.cams[p.roles[1]] + i;
+    double* c = p.cams[r_new] + i;
     const double* src = buf + cam_off[t] + 15 * sel;
     double v[16], prev[16];
 #pragma unroll
     for (int k = 0; k < 15; ++k) v[k] = src[k];  // all loads in flight before any store
     v[15] = 0.0;
-    load_cam16(p.cams[p.roles[0]] + i, prev);
+    load_cam16(p.cams[r_old] + i, prev);
 #pragma unroll
     for (int k = 0; k < 16; ++k) c[k] = v[k];
-    extrapolate_camera(v, prev, gamma, p.cbarb[p.roles[4]] + i);
+    extrapolate_camera(v, prev, gamma, p.cbarb[sel] + i);
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
     const double* b = buf + pt_off[q] + 3 * sel;
-    const double4 lp = p.pts[p.roles[0]][pt_idx[q]];
-    p.pts[p.roles[1]][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);
-    p.lbar[p.roles[4]][pt_idx[q]] = make_double4(fma(gamma, b[0] - lp.x, b[0]), fma(gamma, b[1] - lp.y, b[1]),
-                                                 fma(gamma, b[2] - lp.z, b[2]), 0.0);
+    const double4 lp = p.pts[r_old][pt_idx[q]];
+    p.pts[r_new][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);
+    p.lbar[sel][pt_idx[q]] = make_double4(fma(gamma, b[0] - lp.x, b[0]), fma(gamma, b[1] - lp.y, b[1]),
+                                          fma(gamma, b[2] - lp.z, b[2]), 0.0);
+  }
+  if (select_inside) {  // the last block commits the decision (roles, schedule, trace) once every block is done
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      *p.counter = 0;
+      __threadfence();
+      do_select(p);
+    }
   }
 }
 
@@ -1254,9 +1304,11 @@ int launch_trace_post(const IterParams& p, cudaStream_t st) {
 }
 
 int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, cudaStream_t st) {
+                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, int select_inside,
+                  cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf);
+  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
+                                                      select_inside);
   return 1;
 }
 

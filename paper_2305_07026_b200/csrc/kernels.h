@@ -94,6 +94,13 @@ struct IterParams {
   const int32_t* i_sign;
   double* inter_part;     // k_inter blocks x 2
   int32_t n_inter_blocks;
+  // halo send slots written by the solves themselves (global restart test with a communicator; no k_pack):
+  // owned camera i / point j goes to send slots [ptr[i], ptr[i+1]), each at buffer offset off[s]
+  double* sendbuf;        // null: a separate k_pack
+  const int32_t* cam_send_ptr;
+  const int64_t* cam_send_off;
+  const int32_t* pt_send_ptr;
+  const int64_t* pt_send_off;
 };
 
 // Launchers (all asynchronous on `st`).  They return the number of kernels launched.
@@ -115,8 +122,11 @@ int launch_objective(const IterParams& p, cudaStream_t st);
 int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                 const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected,
                 cudaStream_t st);
-// also writes x-bar of the received halo entries (gamma of the next iteration)
+// also writes x-bar of the received halo entries (gamma of the next iteration).  select_inside = 1: the
+// restart decision is taken inside (every thread from the allreduced sums; the last block commits it), no
+// separate k_select
 int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
-                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, cudaStream_t st);
+                  const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, int select_inside,
+                  cudaStream_t st);
 
 }  // namespace daba
