@@ -652,24 +652,24 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       PeerSeg sg;
       sg.rank = pe.rank;
       sg.send_off = soff;
-      sg.send_cnt = 30 * (int64_t)pe.send_cams.size() + 6 * (int64_t)pe.send_pts.size();  // both candidates
+      sg.send_cnt = kHaloCam * (int64_t)pe.send_cams.size() + 6 * (int64_t)pe.send_pts.size();  // both candidates
       sg.recv_off = roff;
-      sg.recv_cnt = 30 * (int64_t)pe.recv_cams.size() + 6 * (int64_t)pe.recv_pts.size();
+      sg.recv_cnt = kHaloCam * (int64_t)pe.recv_cams.size() + 6 * (int64_t)pe.recv_pts.size();
       for (size_t q = 0; q < pe.send_cams.size(); ++q) {
         sc.push_back(pe.send_cams[q]);
-        sco.push_back(soff + 30 * (int64_t)q);
+        sco.push_back(soff + kHaloCam * (int64_t)q);
       }
       for (size_t q = 0; q < pe.send_pts.size(); ++q) {
         sp.push_back(pe.send_pts[q]);
-        spo.push_back(soff + 30 * (int64_t)pe.send_cams.size() + 6 * (int64_t)q);
+        spo.push_back(soff + kHaloCam * (int64_t)pe.send_cams.size() + 6 * (int64_t)q);
       }
       for (size_t q = 0; q < pe.recv_cams.size(); ++q) {
         rcm.push_back(pe.recv_cams[q]);
-        rco.push_back(roff + 30 * (int64_t)q);
+        rco.push_back(roff + kHaloCam * (int64_t)q);
       }
       for (size_t q = 0; q < pe.recv_pts.size(); ++q) {
         rpt.push_back(pe.recv_pts[q]);
-        rpo.push_back(roff + 30 * (int64_t)pe.recv_cams.size() + 6 * (int64_t)q);
+        rpo.push_back(roff + kHaloCam * (int64_t)pe.recv_cams.size() + 6 * (int64_t)q);
       }
       soff += sg.send_cnt;
       roff += sg.recv_cnt;

@@ -888,15 +888,18 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
     double* dst = p.cams[p.roles[2 + a]] + (size_t)i * kCamStride;
     for (int k = 0; k < 15; ++k) dst[k] = out[k];
     dst[15] = 0.0;
-    if (p.sendbuf)  // boundary camera: this anchor's candidate straight into its halo send slots
-      for (int s = p.cam_send_ptr[i]; s < p.cam_send_ptr[i + 1]; ++s)
-        for (int k = 0; k < 15; ++k) p.sendbuf[p.cam_send_off[s] + 15 * a + k] = out[k];
     p.decisions[2 * i + a] = accepted;
     // x-bar^{k+1} of this candidate (used if the restart test selects it): eqs. nesterov_x with gamma^{(k+1)}
     double cb[16];
     extrapolate_camera(out, ck, sched_gamma_next(p.sched[0], p.accelerate), cb);
     double* cdst = p.cbarb[a] + (size_t)i * kCamStride;
     for (int k = 0; k < 16; ++k) cdst[k] = cb[k];
+    if (p.sendbuf)  // boundary camera: this anchor's candidate and its x-bar straight into its halo send slots
+      for (int s = p.cam_send_ptr[i]; s < p.cam_send_ptr[i + 1]; ++s) {
+        double* b = p.sendbuf + p.cam_send_off[s];
+        for (int k = 0; k < 15; ++k) b[15 * a + k] = out[k];
+        for (int k = 0; k < 16; ++k) b[30 + 16 * a + k] = cb[k];
+      }
   }
   // camera part of E(x_acc|x^k) on the MM lane: the accelerated candidate comes from the partner lane
   double ca[15];
@@ -1122,13 +1125,20 @@ __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_
   // before the decision: [acc | mm] candidates; after a local decision (selected): [x^{k+1} | x^{k+1}].
   // Cameras: one warp per camera, one double per lane; points: one thread per point.
   const int ra = selected ? p.roles[1] : p.roles[2], rm = selected ? p.roles[1] : p.roles[3];
-  const int n_cam_threads = 32 * n_cam;
-  if (t < n_cam_threads) {
-    const int e = t >> 5, c = t & 31;
-    if (c < 30) {
-      const double v = (c < 15 ? p.cams[ra] : p.cams[rm])[(size_t)cam_idx[e] * kCamStride + (c < 15 ? c : c - 15)];
-      buf[cam_off[e] + c] = v;
-    }
+  const int n_cam_threads = 64 * n_cam;
+  if (t < n_cam_threads) {  // two warps per camera: lanes 0..61 copy one double each
+    const int e = t >> 6, c = t & 63;
+    const size_t i = (size_t)cam_idx[e] * kCamStride;
+    double v = 0.0;
+    if (c < 15)
+      v = p.cams[ra][i + c];
+    else if (c < 30)
+      v = p.cams[rm][i + c - 15];
+    else if (c < 46)  // x-bar of either outcome (before the decision) or of the selected one (after)
+      v = p.cbarb[selected ? p.roles[4] : 0][i + c - 30];
+    else if (c < 62)
+      v = p.cbarb[selected ? p.roles[4] : 1][i + c - 46];
+    if (c < kHaloCam) buf[cam_off[e] + c] = v;
   } else if (t < n_cam_threads + n_pt) {
     const int q = t - n_cam_threads;
     const double4 la = p.pts[ra][pt_idx[q]], lm = p.pts[rm][pt_idx[q]];
@@ -1164,18 +1174,21 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
     r_old = p.roles[0];
     gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
   }
-  if (t < n_cam) {
+  if (t < n_cam) {  // x^{k+1} and its x-bar^{k+1} as the owner computed them
     const size_t i = (size_t)cam_idx[t] * kCamStride;
+    const double* src = buf + cam_off[t];
+    double v[15], xb[16];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) v[k] = src[15 * sel + k];  // all loads in flight before any store
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xb[k] = src[30 + 16 * sel + k];
     double* c = p.cams[r_new] + i;
-    const double* src = buf + cam_off[t] + 15 * sel;
-    double v[16], prev[16];
+    double* cb = p.cbarb[sel] + i;
 #pragma unroll
-    for (int k = 0; k < 15; ++k) v[k] = src[k];  // all loads in flight before any store
-    v[15] = 0.0;
-    load_cam16(p.cams[r_old] + i, prev);
+    for (int k = 0; k < 15; ++k) c[k] = v[k];
+    c[15] = 0.0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) c[k] = v[k];
-    extrapolate_camera(v, prev, gamma, p.cbarb[sel] + i);
+    for (int k = 0; k < 16; ++k) cb[k] = xb[k];
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
     const double* b = buf + pt_off[q] + 3 * sel;
@@ -1278,7 +1291,7 @@ int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_
                 const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, double* buf, int selected,
                 cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_pack<<<blocks(32 * (int64_t)n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt,
+  k_pack<<<blocks(64 * (int64_t)n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt,
                                                                   buf, selected);
   return 1;
 }

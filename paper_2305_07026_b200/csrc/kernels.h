@@ -26,6 +26,9 @@ constexpr int kGlobalCols = 12;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc,
                                   // F_kappa correction, D increment (per-device restart, k_inter)
 constexpr int kTraceCols = 11;    // = DABA_TRACE_COLS
 constexpr int kInterThreads = 256;
+// halo record of a camera: [acc 15 | mm 15 | acc x-bar 16 | mm x-bar 16] — the next iteration's x-bar travels
+// with the state (the receiver would recompute the same ProjRot3D); of a point: [acc 3 | mm 3]
+constexpr int kHaloCam = 62;
 
 struct CamChunk {
   int32_t cam;    // local camera index (owned)
