@@ -589,7 +589,7 @@ __device__ __noinline__ void final_reduce(const FinalArgs p) {
 // communicator, takes the restart decision.
 __device__ void finish_block(const IterParams& p) {
   __shared__ bool last;
-  __threadfence();
+  if (threadIdx.x < kCamEvalCols) __threadfence();  // the threads that wrote this block's partial
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == p.n_cam_eval_blocks + p.n_pt_blocks - 1;
   __syncthreads();
@@ -1199,9 +1199,11 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
   }
   if (select_inside) {  // the last block commits the decision (roles, schedule, trace) once every block is done
     __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(p.counter, 1) == (int)gridDim.x - 1;
+    __syncthreads();  // (do_select reads only the allreduced sums and the roles every block has read by now)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(p.counter, 1) == (int)gridDim.x - 1;
+    }
     __syncthreads();
     if (last && threadIdx.x == 0) {
       *p.counter = 0;
