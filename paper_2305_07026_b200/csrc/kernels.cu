@@ -30,34 +30,23 @@ __device__ __forceinline__ double sched_gamma(double s, int accelerate, double* 
   return accelerate ? (s - 1.0) / s_next : 0.0;
 }
 
-// 256-bit global access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): one instruction per 32-byte record.
-#ifdef DABA_STRICT_ASM
-#define DABA_LD_ASM asm volatile
-#define DABA_ST_CLOBBER : "memory"
-#else
-#define DABA_LD_ASM asm
-#define DABA_ST_CLOBBER
-#endif
+// 256-bit global access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): one instruction per 32-byte record.  The
+// load is not volatile (it may be scheduled freely); the store has no memory clobber: nobody reads a record in
+// the kernel that writes it, so loads may move across it.
 __device__ __forceinline__ double4 ld256(const double4* q) {
   double4 v;
-  DABA_LD_ASM("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
   return v;
 }
-// plain store of a record nobody reads in the same kernel: no memory clobber, so the scheduler may move loads
-// across it
 __device__ __forceinline__ void st256(double4* q, double4 v) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) DABA_ST_CLOBBER);
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w));
 }
 
-// Point-side record of observation r at anchor a (0: x-bar^k, 1: x^k), 32 B, in two separate arrays.
-// DABA_INTERLEAVE puts an observation's two records side by side (64 B): measured neutral on Final-13682
-// (k_pt_sum -0.04 ms, k_cam_pass +0.03 ms: the two anchors' CTAs then write half lines).
+// Point-side record of observation r at anchor a (0: x-bar^k, 1: x^k), 32 B, in two separate arrays.  (The two
+// anchors' records side by side, 64 B, measured neutral on Final-13682: k_pt_sum -0.04 ms, k_cam_pass +0.03 ms,
+// the two anchors' CTAs then writing half lines.)
 __device__ __forceinline__ double4* rec_ptr(const IterParams& p, int64_t r, int a) {
-#ifdef DABA_INTERLEAVE
-  return reinterpret_cast<double4*>(p.staging) + 2 * r + a;
-#else
   return reinterpret_cast<double4*>(p.staging + (a ? 4 * p.n_records : 0)) + r;
-#endif
 }
 
 // Point record: 32 bytes (x, y, z, pad) — one sector per gather.
@@ -94,13 +83,8 @@ __device__ __forceinline__ void extrapolate_camera(const double* ck, const doubl
 //  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e
 //  38 w |e|^2   39 a   [40 degenerate pairs]
 // Camera record kept in shared memory and re-read at every use (volatile shared loads are not hoisted into
-// registers): frees ~30 registers per thread in the camera pass, i.e. one more resident CTA per SM.
-#ifdef DABA_CAM_REGS
-struct CamRegs {
-  double v[15];
-  __device__ __forceinline__ double operator[](int k) const { return v[k]; }
-};
-#else
+// registers): frees ~30 registers per thread in the camera pass, i.e. more resident CTAs per SM (a copy in
+// registers measured 0.80 ms with spills at 6 CTAs/SM, 0.86 ms at 4).
 struct CamRegs {
   const double* sm;  // shared-memory camera record (16 doubles)
   __device__ __forceinline__ double operator[](int k) const {
@@ -109,10 +93,6 @@ struct CamRegs {
     return v;
   }
 };
-#endif
-#ifndef DABA_SINGLE
-#define DABA_DUAL  // two observations per step (measured: 0.97 vs 1.02 ms on Final-13682)
-#endif
 #ifndef DABA_RING
 #define DABA_RING 8
 #endif
@@ -139,26 +119,12 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   const double cx = fma(c[0], vx, fma(c[3], vy, c[6] * vz));
   const double cy = fma(c[1], vx, fma(c[4], vy, c[7] * vz));
   const double cz = fma(c[2], vx, fma(c[5], vy, c[8] * vz));
-#ifdef DABA_FASTRCP
-  double rn = (double)__frcp_rn((float)nv);
-  rn = rn * fma(-nv, rn, 2.0);
-  rn = rn * fma(-nv, rn, 2.0);
-  rn = fma(rn, fma(-nv, rn, 1.0), rn);
-  const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * rn;
-#else
   const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
-#endif
   const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
   const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
   double rho = 0;
   const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
   const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
-#ifdef DABA_NOMOM
-  acc[0] += w; acc[1] += wx * lam; acc[2] += wy * ex; acc[3] += ws * ey + ez;
-  if (!ACC) { acc[38] = fma(w, sh, acc[38]); acc[39] += 0.5 * fma(-w, sh, rho); }
-  const double wl = w * lam;
-  if (false) {
-#endif
   acc[0] = fma(wx, u.x, acc[0]);
   acc[1] = fma(wx, u.y, acc[1]);
   acc[2] = fma(wy, u.y, acc[2]);
@@ -203,12 +169,6 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
     acc[38] = fma(w, sh, acc[38]);
     acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
   }
-#ifdef DABA_NOMOM
-  }
-#endif
-#ifdef DABA_NOEMIT
-  if (rec < 0) {
-#endif
   // point side of the same pair: (w lam^2, w lam R e) with the world-frame error R e (eq. Q's sums), written
   // coalesced at the camera-side index (one 32-byte record per anchor)
   const double gx = fma(c[0], ex, fma(c[1], ey, c[2] * ez));
@@ -217,9 +177,6 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   if (rec >= 0)
     st256(rec_ptr(p, rec, ACC ? 0 : 1),
           make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
-#ifdef DABA_NOEMIT
-  }
-#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -243,15 +200,9 @@ template <int LOSS, bool ACC>
 __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc,
                                               double2* ring, int32_t* sidx) {
   const double* cam = (ACC ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
-#ifdef DABA_CAM_REGS
-  CamRegs c;
-#pragma unroll
-  for (int k = 0; k < 15; ++k) c.v[k] = cam[k];
-#else
   __shared__ double scam[kCamStride];
   if (threadIdx.x < kCamStride) scam[threadIdx.x] = cam[threadIdx.x];
   CamRegs c{scam};
-#endif
   const double4* __restrict__ L = ACC ? p.lbar[p.roles[4]] : p.pts[p.roles[1]];
   const int tid = threadIdx.x;
   const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
@@ -268,50 +219,25 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   };
 #pragma unroll
   for (int k = 0; k < kRing - 1; ++k) issue(k);
-#ifdef DABA_DUAL
-  // two observations per step: two independent dependency chains feed the same accumulators; the point
-  // records of the next DABA_PFS steps are in flight (registers)
-#ifndef DABA_PFS
-#define DABA_PFS 1
-#endif
-  constexpr int PS = DABA_PFS;
-  double4 lq[2 * PS];
-#pragma unroll
-  for (int r = 0; r < 2 * PS; ++r) lq[r] = r < n ? ld256(L + sidx[tid + r * kCamPassThreads]) : make_double4(0, 0, 0, 0);
+  // two observations per step: two independent dependency chains feed the same accumulators; the next step's
+  // point records are in flight (registers).  (Measured: one observation per step 0.90 ms vs 0.76 ms; a deeper
+  // record prefetch was slower.)
+  double4 lq0 = 0 < n ? ld256(L + sidx[tid]) : make_double4(0, 0, 0, 0);
+  double4 lq1 = 1 < n ? ld256(L + sidx[tid + kCamPassThreads]) : make_double4(0, 0, 0, 0);
   issue(kRing - 1);
 #pragma unroll 1
-  for (int k0 = 0; k0 < n; k0 += 2 * PS) {
-#pragma unroll
-    for (int h = 0; h < PS; ++h) {
-      const int k = k0 + 2 * h;
-      if (k < n) {
-        const double4 l0 = lq[2 * h], l1 = lq[2 * h + 1];
-        if (k + 2 * PS < n) lq[2 * h] = ld256(L + sidx[tid + (k + 2 * PS) * kCamPassThreads]);
-        if (k + 2 * PS + 1 < n) lq[2 * h + 1] = ld256(L + sidx[tid + (k + 2 * PS + 1) * kCamPassThreads]);
-        cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
-        const double2 u0 = *uslot(k);
-        const double2 u1 = *uslot(k + 1);
-        issue(k + kRing);  // refills the two slots just read
-        issue(k + kRing + 1);
-        cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, REC(k));
-        if (k + 1 < n)
-          cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, REC(k + 1));
-      }
-    }
+  for (int k = 0; k < n; k += 2) {
+    const double4 l0 = lq0, l1 = lq1;
+    if (k + 2 < n) lq0 = ld256(L + sidx[tid + (k + 2) * kCamPassThreads]);
+    if (k + 3 < n) lq1 = ld256(L + sidx[tid + (k + 3) * kCamPassThreads]);
+    cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
+    const double2 u0 = *uslot(k);
+    const double2 u1 = *uslot(k + 1);
+    issue(k + kRing);  // refills the two slots just read
+    issue(k + kRing + 1);
+    cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, REC(k));
+    if (k + 1 < n) cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, REC(k + 1));
   }
-#else
-  double4 lnext = make_double4(0, 0, 0, 0);
-  if (n > 0) lnext = ld256(L + sidx[tid]);
-#pragma unroll 1
-  for (int k = 0; k < n; ++k) {
-    const double4 l = lnext;
-    if (k + 1 < n) lnext = ld256(L + sidx[tid + (k + 1) * kCamPassThreads]);
-    issue(k + kRing - 1);
-    cp_async_wait<kRing - 1>();
-    const double2 u = *uslot(k);
-    cam_obs<LOSS, ACC>(p, c, u, l.x, l.y, l.z, acc, REC(k));
-  }
-#endif
   cp_async_wait<0>();
 }
 
