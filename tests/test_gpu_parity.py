@@ -252,7 +252,7 @@ def test_rank_count_invariance(nranks):
 
 # ---------------------------------------------------------------- full-size sampled parity
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["trafalgar", "final13682"])
+@pytest.mark.parametrize("name", ["trafalgar", "venice1778", "final13682", "weak_slab"])
 def test_full_size_sampled(name):
     """At the benchmark's full size: F(x^k) over all observations, and the next iterate of sampled cameras and
     points computed one by one by the oracle from the GPU's (x^k, x^{k-1}, s)."""
