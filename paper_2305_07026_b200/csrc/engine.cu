@@ -237,9 +237,11 @@ void collect_times(daba_ctx* c) {
   c->pending.clear();
 }
 
-// Enqueue one iteration of Algorithm 1.  With a communicator, both candidates of every boundary variable are
-// packed as soon as they exist and exchanged in the same NCCL group as the allreduce of the restart sums (the two
-// transfers overlap); after the restart decision the unpack keeps the selected candidate.
+// Enqueue one iteration of Algorithm 1.  With a communicator and the global restart test, the solves write both
+// candidates of every boundary variable into the send buffer, which is exchanged in the same NCCL group as the
+// allreduce of the restart sums (the two transfers overlap); k_unpack then takes the decision from the
+// allreduced sums, keeps the selected candidate and commits the decision.  With the per-device test the rank
+// decides in the solves' last block and sends x^{k+1} (k_pack); the allreduce only feeds the trace.
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
@@ -275,9 +277,6 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
   }
   if (c->comm) {
     const bool halo = !c->segs.empty();
-    // global test: both candidates are sent before the decision (the exchange overlaps the allreduce) and
-    // k_select decides on the allreduced sums; per device: the rank has decided already (last block of
-    // k_cam_solve) and sends x^{k+1}; the allreduce only feeds the trace
     const bool dev = P.restart_scope == 1;
     if (halo && !P.sendbuf)  // (global test: the solves already wrote the send buffer)
       n += timed(c, "k_pack", [&] {
