@@ -33,11 +33,11 @@ FP64_FMA_PEAK = 17.06e12  # measured DFMA/s, profiles/r01_day0_micro.log (148 SM
 # Algorithmic bytes per launch: what each kernel must read or write at least once.
 #   k_cam_pass (both anchors): per observation u (16 B) + point index (4 B) read, the point-side record of both
 #     anchors written (2 x 32 B); per point the two anchor states read once (2 x 32 B); cameras 2 x 128 B.
-#   k_pt_pass (= k_pt_sum): per observation both records (64 B) + record index (4 B); per point read x^k and
+#   k_pt_sum: per observation both records (64 B) + record index (4 B); per point read x^k and
 #     x-bar^k (64 B), write both candidates and both next x-bar (4 x 32 B), offsets (8 B).
 BYTES = {
     "k_cam_pass": lambda K, N, M: 84 * K + 64 * N + 2 * 128 * M,
-    "k_pt_pass": lambda K, N, M: 68 * K + 200 * N,
+    "k_pt_sum": lambda K, N, M: 68 * K + 200 * N,
 }
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
@@ -285,8 +285,9 @@ def main():
 
     value = a.steps * p.K / (ms * 1e-3)
     hbm, hbm_src = peaks()
-    # dominant kernel and its roofline
-    dom = max(kt.items(), key=lambda kv: kv[1][0])
+    # dominant kernel (of those with a byte model) and its roofline
+    dom = max(((k, v) for k, v in kt.items() if k in BYTES), key=lambda kv: kv[1][0], default=None) or \
+        max(kt.items(), key=lambda kv: kv[1][0])
     dname, (dms, dl) = dom
     per_launch_ms = dms / max(dl, 1)
     kt = {k: v for k, v in kt.items() if v[1] > 0}
@@ -319,7 +320,9 @@ def main():
         "config": {"workload": a.config if scaling == "strong" else f"{a.config} x{world}", "cameras": p.M, "points": p.N, "observations": int(p.K),
                    "loss": ["trivial", "huber", "cauchy"][p.loss], "parallelism": f"camera-partitioned x{world}",
                    "restart": a.restart,
-                   "l2": "inputs larger than L2 (observation streams 1.2 GB, point states 4 x 143 MB)",
+                   "l2": (f"inputs larger than L2 (observation streams {20 * p.K / 1e9:.2f} GB, point states "
+                          f"4 x {32 * p.N / 1e6:.0f} MB)") if 20 * p.K > 126e6 else
+                         "small config: inputs fit in L2 (not a benchmark workload)",
                    "F_end": F_end},
         "roofline": roof,
         "kernel_share": kshare,
