@@ -533,7 +533,8 @@ __device__ void finish_block(const IterParams& p) {
 // Point solve (a7) over a grid-stride set of owned points: each point adds its observations' records in
 // ascending (camera) order and takes the exact minimiser for both anchors.  The last block to finish forms the
 // rank-local sums (a9) and, without a communicator, takes the restart decision (a9 + a10).  Deterministic.
-// (measured: 3 CTAs/SM spill and take 1.14 ms; a max-L1 carve-out 0.69 ms; 2 CTAs with the default 0.61 ms)
+// (measured at 2 CTAs/SM and 4 records per batch: 0.588 ms; 3 records 0.612, 6 records 0.652, 2 records at 3 or 4
+// CTAs/SM 0.607 / 0.717, 4 records at 3 CTAs/SM spill: 1.14, a max-L1 carve-out 0.69)
 __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   double qv[kPtCols] = {0, 0, 0, 0};
   for (int j = blockIdx.x * kPtPassThreads + threadIdx.x; j < p.n_own_pts; j += gridDim.x * kPtPassThreads) {
