@@ -463,3 +463,16 @@ def test_point_renumbering_path(monkeypatch):
         assert max(state_errors(*s.state_native(0)[:2], co, lo)) <= X_TOL
     _, cams, pts, _ = run_ranks(p, 3, 20)
     assert max(state_errors(cams, pts, co, lo)) <= X_TOL
+
+
+def test_long_trace_spans_the_device_ring():
+    """More iterations in one call than the device trace ring holds (1024): the trace is drained in batches and
+    matches the oracle's F(x^k) all the way."""
+    p = gen.generate("tiny_seq")
+    o = oracle_for(p, eta=1.0)
+    tro = o.iterate(1300)
+    with solver(p, eta=1.0) as s:
+        trg = s.iterate_trace(1300)
+    rel = np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])
+    assert rel.max() <= 1e-9, (rel.max(), int(rel.argmax()))
+    np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART][:200], tro[:, oracle.TR_RESTART][:200])
