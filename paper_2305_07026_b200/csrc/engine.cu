@@ -539,6 +539,8 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       cptr.push_back((int32_t)chunks.size());
     }
     P.n_chunks = (int32_t)chunks.size();
+    // one CTA per chunk for both anchors once the chunks fill the GPU four times over (6 CTAs per SM)
+    P.cam_shared_ctas = (int32_t)env_int("DABA_CAM_SHARED", P.n_chunks >= 4 * 6 * C->num_sms ? 1 : 0);
     const CamChunk* dch;
     if ((rc = upload(C, const_cast<CamChunk**>(&dch), chunks))) return bail(rc);
     P.chunks = dch;

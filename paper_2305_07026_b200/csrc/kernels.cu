@@ -196,25 +196,26 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // prefetched one observation ahead in registers.  The chunk's point indices are staged in shared memory.
 constexpr int kRing = DABA_RING;
 
-template <int LOSS, bool ACC>
+// The chunk's point indices staged in shared memory (every 4-byte copy in flight at once, one wait) and the
+// anchor camera's record; the caller synchronises the CTA afterwards.
+__device__ __forceinline__ void stage_chunk(const IterParams& p, const CamChunk ch, int32_t* sidx) {
+  for (int o = threadIdx.x; o < ch.n; o += kCamPassThreads) cp_async4(sidx + o, p.c_pt + ch.o0 + o);
+  cp_async_commit();
+  cp_async_wait<0>();
+}
+
+// One anchor's pass over a chunk by a group of G threads (lane = rank in the group): observation lane + G k.
+template <int LOSS, bool ACC, int G>
 __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc,
-                                              double2* ring, int32_t* sidx) {
-  const double* cam = (ACC ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]]) + (size_t)ch.cam * kCamStride;
-  __shared__ double scam[kCamStride];
-  if (threadIdx.x < kCamStride) scam[threadIdx.x] = cam[threadIdx.x];
+                                              double2* ring, const int32_t* sidx, int lane, const double* scam) {
   CamRegs c{scam};
   const double4* __restrict__ L = ACC ? p.lbar[p.roles[4]] : p.pts[p.roles[1]];
   const int tid = threadIdx.x;
-  const int n = (ch.n - tid + kCamPassThreads - 1) / kCamPassThreads;  // observations of this thread
-  // stage the chunk's point indices: every 4-byte copy in flight at once (cp.async), one wait
-  for (int o = tid; o < ch.n; o += kCamPassThreads) cp_async4(sidx + o, p.c_pt + ch.o0 + o);
-#define REC(kk) (ch.o0 + tid + (int64_t)(kk) * kCamPassThreads)
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
+  const int n = (ch.n - lane + G - 1) / G;  // observations of this thread
+#define REC(kk) (ch.o0 + lane + (int64_t)(kk) * G)
   auto uslot = [&](int k) { return ring + (k & (kRing - 1)) * kCamPassThreads + tid; };
   auto issue = [&](int k) {
-    if (k < n) cp_async16(uslot(k), p.c_uv + ch.o0 + tid + (int64_t)k * kCamPassThreads);
+    if (k < n) cp_async16(uslot(k), p.c_uv + ch.o0 + lane + (int64_t)k * G);
     cp_async_commit();
   };
 #pragma unroll
@@ -222,14 +223,14 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   // two observations per step: two independent dependency chains feed the same accumulators; the next step's
   // point records are in flight (registers).  (Measured: one observation per step 0.90 ms vs 0.76 ms; a deeper
   // record prefetch was slower.)
-  double4 lq0 = 0 < n ? ld256(L + sidx[tid]) : make_double4(0, 0, 0, 0);
-  double4 lq1 = 1 < n ? ld256(L + sidx[tid + kCamPassThreads]) : make_double4(0, 0, 0, 0);
+  double4 lq0 = 0 < n ? ld256(L + sidx[lane]) : make_double4(0, 0, 0, 0);
+  double4 lq1 = 1 < n ? ld256(L + sidx[lane + G]) : make_double4(0, 0, 0, 0);
   issue(kRing - 1);
 #pragma unroll 1
   for (int k = 0; k < n; k += 2) {
     const double4 l0 = lq0, l1 = lq1;
-    if (k + 2 < n) lq0 = ld256(L + sidx[tid + (k + 2) * kCamPassThreads]);
-    if (k + 3 < n) lq1 = ld256(L + sidx[tid + (k + 3) * kCamPassThreads]);
+    if (k + 2 < n) lq0 = ld256(L + sidx[lane + (k + 2) * G]);
+    if (k + 3 < n) lq1 = ld256(L + sidx[lane + (k + 3) * G]);
     cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
     const double2 u0 = *uslot(k);
     const double2 u1 = *uslot(k + 1);
@@ -239,10 +240,13 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
     if (k + 1 < n) cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, REC(k + 1));
   }
   cp_async_wait<0>();
+#undef REC
 }
 
-// Deterministic block reduction of kPartialStride doubles per thread (128 threads) via shared-memory transposes.
-__device__ __forceinline__ void block_reduce_moments(double* acc, double* out, double* smem) {
+// The moments of each group of G threads (the anchors of a CTA) summed in a fixed order via a shared-memory
+// transpose; group g's sums go to out + g * kPartialStride.
+template <int G>
+__device__ __forceinline__ void group_reduce_moments(double* acc, double* out, double* smem) {
   double(*red)[32][kPartialStride] = reinterpret_cast<double(*)[32][kPartialStride]>(smem);
   __shared__ double wsum[kCamWarps][kPartialStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -258,15 +262,17 @@ __device__ __forceinline__ void block_reduce_moments(double* acc, double* out, d
     }
     wsum[warp][k] = s0 + s1;
   }
+  constexpr int WG = G / 32, NG = kCamPassThreads / G;  // warps per group, groups
+  if (WG == 1) {
+    for (int k = lane; k < kPartialStride; k += 32) out[(size_t)warp * kPartialStride + k] = wsum[warp][k];
+    return;
+  }
   __syncthreads();
-  if (threadIdx.x < kPartialStride) {
-    const int k = threadIdx.x;
-    if (kCamWarps == 4)
-      out[k] = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
-    else if (kCamWarps == 2)
-      out[k] = wsum[0][k] + wsum[1][k];
-    else
-      out[k] = wsum[0][k];
+  if (threadIdx.x < NG * kPartialStride) {
+    const int g = threadIdx.x / kPartialStride, k = threadIdx.x % kPartialStride;
+    double v = 0.0;
+    for (int w = 0; w < WG; ++w) v += wsum[g * WG + w][k];
+    out[(size_t)g * kPartialStride + k] = v;
   }
 }
 
@@ -274,24 +280,33 @@ constexpr int kCamRingDoubles = kRing * 2 * kCamPassThreads + kCamChunkObs / 2; 
 constexpr int kCamSmemDoubles =
     kCamRingDoubles > kCamPassThreads * kPartialStride ? kCamRingDoubles : kCamPassThreads * kPartialStride;
 
-template <int LOSS>
+// SHARED: one CTA per chunk, the first half of the threads the accelerated anchor and the second half the MM
+// anchor, sharing the staged indices (large shards).  Otherwise one CTA per chunk and anchor, all threads on
+// one anchor: twice the CTAs, for shards too small to fill the GPU a few times over (measured: Final-13682 at
+// one rank 0.741 vs 0.764 ms; one rank of eight 0.247 vs 0.251 ms per iteration).
+template <int LOSS, bool SHARED>
 __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterParams p) {
   extern __shared__ __align__(16) double smem[];  // kCamSmemDoubles
-  const int chunk = blockIdx.x >> 1;
-  const bool acc_anchor = (blockIdx.x & 1) == 0;
+  constexpr int G = SHARED ? kCamPassThreads / 2 : kCamPassThreads;
+  const int chunk = SHARED ? blockIdx.x : blockIdx.x >> 1;
+  const int grp = SHARED ? threadIdx.x / G : (blockIdx.x & 1), lane = threadIdx.x % G;
   const CamChunk ch = p.chunks[chunk];
   double acc[kPartialStride];
 #pragma unroll
   for (int k = 0; k < kPartialStride; ++k) acc[k] = 0.0;
   double2* ring = reinterpret_cast<double2*>(smem);
   int32_t* sidx = reinterpret_cast<int32_t*>(smem + kRing * 2 * kCamPassThreads);
-  if (acc_anchor)
-    cam_pass_body<LOSS, true>(p, ch, acc, ring, sidx);
+  __shared__ double scam[2][kCamStride];
+  if (lane < kCamStride)
+    scam[grp][lane] = (grp == 0 ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]])[(size_t)ch.cam * kCamStride + lane];
+  stage_chunk(p, ch, sidx);
+  __syncthreads();
+  if (grp == 0)
+    cam_pass_body<LOSS, true, G>(p, ch, acc, ring, sidx, lane, scam[0]);
   else
-    cam_pass_body<LOSS, false>(p, ch, acc, ring, sidx);
-
+    cam_pass_body<LOSS, false, G>(p, ch, acc, ring, sidx, lane, scam[1]);
   __syncthreads();  // the ring is reused as the reduction buffer
-  block_reduce_moments(acc, p.partial + (size_t)blockIdx.x * kPartialStride, smem);
+  group_reduce_moments<G>(acc, p.partial + (size_t)(SHARED ? 2 * blockIdx.x : blockIdx.x) * kPartialStride, smem);
 }
 
 // ------------------------------------------------------------------ objective F(x^k) only
@@ -1155,10 +1170,14 @@ static void cam_launch(const IterParams& p, cudaStream_t st) {
   constexpr size_t sm = sizeof(double) * kCamSmemDoubles;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_cam_pass<LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_cam_pass<LOSS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_cam_pass<LOSS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  k_cam_pass<LOSS><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
+  if (p.cam_shared_ctas)
+    k_cam_pass<LOSS, true><<<p.n_chunks, kCamPassThreads, sm, st>>>(p);
+  else
+    k_cam_pass<LOSS, false><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
 }
 
 int launch_cam_pass(const IterParams& p, cudaStream_t st) {

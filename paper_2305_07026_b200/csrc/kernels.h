@@ -11,9 +11,9 @@ constexpr int kCamStride = 16;
 constexpr int kNumMoments = 40;   // per camera and anchor, see DESIGN.md "camera moments"
 constexpr int kPartialStride = 41;  // 40 moments + degenerate-pair count
 #ifndef DABA_CPT
-#define DABA_CPT 64  // measured on Final-13682: 64 -> 0.758 ms, 128 -> 0.843 ms, 32 -> 1.18 ms (k_cam_pass)
+#define DABA_CPT 64  // one warp per anchor (k_cam_pass 0.741 ms on Final-13682)
 #endif
-constexpr int kCamPassThreads = DABA_CPT;  // 32, 64 or 128 threads per camera-pass CTA
+constexpr int kCamPassThreads = DABA_CPT;  // threads per camera-pass CTA: half per anchor
 constexpr int kCamWarps = kCamPassThreads / 32;
 #ifndef DABA_CHUNK
 #define DABA_CHUNK 4096
@@ -45,6 +45,7 @@ struct IterParams {
   int32_t n_pts;         // local points (owned first, then halo)
   int32_t n_own_pts;
   int32_t n_chunks;      // camera-pass chunks
+  int32_t cam_shared_ctas;  // 1: one camera-pass CTA per chunk (both anchors), 0: one per chunk and anchor
   int32_t loss;
   double delta, delta2, idelta2;
   double xi, eta, mu0, mu_up, eps2;

@@ -476,3 +476,18 @@ def test_long_trace_spans_the_device_ring():
     rel = np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])
     assert rel.max() <= 1e-9, (rel.max(), int(rel.argmax()))
     np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART][:200], tro[:, oracle.TR_RESTART][:200])
+
+
+@pytest.mark.parametrize("name", ["small_cauchy", "small_seq_huber"])
+def test_shared_anchor_camera_ctas(name, monkeypatch):
+    """The camera pass with one CTA per chunk for both anchors (the large-shard layout) forced on small problems:
+    the oracle's trajectory."""
+    monkeypatch.setenv("DABA_CAM_SHARED", "1")
+    p = gen.generate(name)
+    o = oracle_for(p, eta=1.0)
+    tro = o.iterate(30)
+    with solver(p, eta=1.0) as s:
+        trg = s.iterate_trace(30)
+        assert (np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])).max() <= F_TOL
+        np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
