@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <atomic>
 #include <thread>
@@ -122,11 +123,51 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
   return DABA_OK;
 }
 
+// Host -> device copy on the context's stream.  Small or page-locked sources go directly; large pageable ones
+// through a process-wide page-locked staging buffer (two 32 MB halves: the host threads fill one half while
+// the copy engine drains the other).  Returns once the source may be reused.
+cudaError_t h2d(daba_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer may leave an error behind on some drivers
+  if (pinned || bytes < (8u << 20)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+  static std::mutex mu;
+  static char* stage = nullptr;
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  constexpr size_t kHalf = 32u << 20;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!stage) {
+    if (cudaMallocHost(&stage, 2 * kHalf) != cudaSuccess) {
+      stage = nullptr;
+      cudaGetLastError();
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+    }
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+  }
+  bool used[2] = {false, false};
+  for (size_t off = 0, h = 0; off < bytes; off += kHalf, h ^= 1) {
+    const size_t n = std::min(kHalf, bytes - off);
+    if (used[h]) cudaEventSynchronize(ev[h]);
+    char* buf = stage + h * kHalf;
+    const char* s = static_cast<const char*>(src) + off;
+    parallel_for((int64_t)n, [&](int64_t a, int64_t b) { std::memcpy(buf + a, s + a, (size_t)(b - a)); });
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, buf, n, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(ev[h], c->stream);
+    used[h] = true;
+  }
+  for (int h = 0; h < 2; ++h)
+    if (used[h]) cudaEventSynchronize(ev[h]);  // the staging buffer is free for the next caller
+  return cudaSuccess;
+}
+
 template <class T, class A>
 int upload(daba_ctx* c, T** p, const std::vector<T, A>& h) {
   int rc = dalloc(c, p, h.size());
   if (rc) return rc;
-  if (!h.empty()) CUDA_OR(c, cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OR(c, h2d(c, *p, h.data(), h.size() * sizeof(T)));
   return DABA_OK;
 }
 
@@ -341,12 +382,8 @@ int upload_states(daba_ctx* c, const double* cams_k, const double* pts_k, const 
       }
     });
     const int role = pass ? rkm1 : rk;
-    if (!hc.empty())
-      CUDA_OR(c, cudaMemcpyAsync(c->P.cams[h_roles[role]], hc.data(), hc.size() * sizeof(double),
-                                 cudaMemcpyHostToDevice, c->stream));
-    if (!hp.empty())
-      CUDA_OR(c, cudaMemcpyAsync(c->P.pts[h_roles[role]], hp.data(), hp.size() * sizeof(double),
-                                 cudaMemcpyHostToDevice, c->stream));
+    CUDA_OR(c, h2d(c, c->P.cams[h_roles[role]], hc.data(), hc.size() * sizeof(double)));
+    CUDA_OR(c, h2d(c, c->P.pts[h_roles[role]], hp.data(), hp.size() * sizeof(double)));
     CUDA_OR(c, cudaStreamSynchronize(c->stream));  // the host buffers are refilled by the next pass
   }
   return DABA_OK;
@@ -509,16 +546,16 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     double2* duv;
     int32_t* dpt;
     if ((rc = dalloc(C, &duv, kc)) || (rc = dalloc(C, &dpt, kc))) return bail(rc);
-    if (kc) CUDA_OR(C, cudaMemcpyAsync(dpt, S.c_pt.data(), kc * sizeof(int32_t), cudaMemcpyHostToDevice, C->stream));
+    CUDA_OR(C, h2d(C, dpt, S.c_pt.data(), kc * sizeof(int32_t)));
     if (S.cam_side_identity) {
       // one rank, input sorted by (camera, point): the camera-side pixels are the input itself (no host copy)
-      if (kc) CUDA_OR(C, cudaMemcpyAsync(duv, obs_uv, kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
+      CUDA_OR(C, h2d(C, duv, obs_uv, kc * sizeof(double2)));
     } else {
       hvec<double2> uv(kc);
       parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
         for (int64_t q = a; q < b; ++q) uv[q] = make_double2(obs_uv[2 * S.c_obs[q]], obs_uv[2 * S.c_obs[q] + 1]);
       });
-      if (kc) CUDA_OR(C, cudaMemcpyAsync(duv, uv.data(), kc * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
+      CUDA_OR(C, h2d(C, duv, uv.data(), kc * sizeof(double2)));
       CUDA_OR(C, cudaStreamSynchronize(C->stream));  // uv is freed at the end of this scope
     }
     P.c_uv = duv;

@@ -237,11 +237,25 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
       g2l_cam[(size_t)i] = (int32_t)P.cam_g.size();
       P.cam_g.push_back((int32_t)i);
     }
-  for (int64_t j = 0; j < N; ++j)
-    if (P.pt_owner[(size_t)j] == rank) {
-      g2l_pt[(size_t)j] = (int32_t)P.pt_g.size();
-      P.pt_g.push_back((int32_t)j);
-    }
+  {  // owned points in ascending id: per-thread counts, offsets, fills
+    const unsigned T = nthreads(N);
+    std::vector<int64_t> cnt((size_t)T + 1, 0);
+    pfor(N, [&](int64_t a, int64_t b, int t) {
+      int64_t c = 0;
+      for (int64_t j = a; j < b; ++j) c += P.pt_owner[(size_t)j] == rank;
+      cnt[(size_t)t + 1] = c;
+    });
+    for (unsigned t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+    P.pt_g.resize((size_t)cnt[T]);
+    pfor(N, [&](int64_t a, int64_t b, int t) {
+      int64_t w = cnt[(size_t)t];
+      for (int64_t j = a; j < b; ++j)
+        if (P.pt_owner[(size_t)j] == rank) {
+          g2l_pt[(size_t)j] = (int32_t)w;
+          P.pt_g[(size_t)w++] = (int32_t)j;
+        }
+    });
+  }
   P.n_own_cams = (int32_t)P.cam_g.size();
   P.n_own_pts = (int32_t)P.pt_g.size();
   if (nranks > 1) {
