@@ -879,7 +879,7 @@ extern "C" int daba_objective(daba_ctx* ctx, double* F_out) {
   return compute_objective(ctx, F_out, nullptr);
 }
 
-static int get_native(daba_ctx* c, int which, std::vector<double>& hc, std::vector<double>& hp) {
+static int get_native(daba_ctx* c, int which, hvec<double>& hc, hvec<double>& hp) {
   int roles[4];
   CUDA_OR(c, cudaMemcpyAsync(roles, c->P.roles, sizeof roles, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR(c, cudaStreamSynchronize(c->stream));
@@ -898,7 +898,7 @@ extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_o
                                      uint8_t* owned_mask_out) {
   if (!ctx || which < 0 || which > 1) return DABA_E_INVALID_ARG;
   cudaSetDevice(ctx->device);
-  std::vector<double> hc, hp;
+  hvec<double> hc, hp;
   int rc = get_native(ctx, which, hc, hp);
   if (rc) return rc;
   const ShardPlan& S = ctx->plan;
@@ -908,19 +908,21 @@ extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_o
     if (cameras_out) std::memcpy(cameras_out + 15 * g, &hc[(size_t)li * kCamStride], 15 * sizeof(double));
     if (owned_mask_out) owned_mask_out[g] = 1;
   }
-  for (int32_t lj = 0; lj < S.n_own_pts; ++lj) {
-    const int64_t g = S.pt_g[(size_t)lj];
-    if (points_out)
-      for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
-    if (owned_mask_out) owned_mask_out[S.M + g] = 1;
-  }
+  parallel_for(S.n_own_pts, [&](int64_t a, int64_t b) {
+    for (int64_t lj = a; lj < b; ++lj) {
+      const int64_t g = S.pt_g[(size_t)lj];
+      if (points_out)
+        for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
+      if (owned_mask_out) owned_mask_out[S.M + g] = 1;
+    }
+  });
   return DABA_OK;
 }
 
 extern "C" int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points_out, uint8_t* owned_mask_out) {
   if (!ctx) return DABA_E_INVALID_ARG;
   cudaSetDevice(ctx->device);
-  std::vector<double> hc, hp;
+  hvec<double> hc, hp;
   int rc = get_native(ctx, 0, hc, hp);
   if (rc) return rc;
   const ShardPlan& S = ctx->plan;
@@ -930,12 +932,14 @@ extern "C" int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points
     if (cameras_out) native_to_bal(&hc[(size_t)li * kCamStride], cameras_out + 9 * g);
     if (owned_mask_out) owned_mask_out[g] = 1;
   }
-  for (int32_t lj = 0; lj < S.n_own_pts; ++lj) {
-    const int64_t g = S.pt_g[(size_t)lj];
-    if (points_out)
-      for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
-    if (owned_mask_out) owned_mask_out[S.M + g] = 1;
-  }
+  parallel_for(S.n_own_pts, [&](int64_t a, int64_t b) {
+    for (int64_t lj = a; lj < b; ++lj) {
+      const int64_t g = S.pt_g[(size_t)lj];
+      if (points_out)
+        for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
+      if (owned_mask_out) owned_mask_out[S.M + g] = 1;
+    }
+  });
   return DABA_OK;
 }
 

@@ -199,14 +199,18 @@ class Solver:
         self._check(lib().daba_objective(self.h, ctypes.byref(F)), "daba_objective")
         return F.value
 
+    def _out(self, shape):
+        # entries this rank does not own stay NaN; one rank owns everything (no fill needed)
+        return np.empty(shape) if self.nranks == 1 else np.full(shape, np.nan)
+
     def state(self):
-        cams, pts = np.full((self.M, 9), np.nan), np.full((self.N, 3), np.nan)
+        cams, pts = self._out((self.M, 9)), self._out((self.N, 3))
         mask = np.zeros(self.M + self.N, np.uint8)
         self._check(lib().daba_get_state(self.h, cams.ctypes.data, pts.ctypes.data, mask.ctypes.data), "get_state")
         return cams, pts, mask
 
     def state_native(self, which: int = 0):
-        cams, pts = np.full((self.M, 15), np.nan), np.full((self.N, 3), np.nan)
+        cams, pts = self._out((self.M, 15)), self._out((self.N, 3))
         mask = np.zeros(self.M + self.N, np.uint8)
         self._check(lib().daba_get_state_native(self.h, which, cams.ctypes.data, pts.ctypes.data, mask.ctypes.data),
                     "get_state_native")
