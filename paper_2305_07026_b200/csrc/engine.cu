@@ -51,9 +51,9 @@ struct daba_ctx {
   bool graph_failed = false;
   int launches_per_iter = 0;
   // parallel graph branches (A/B switches, environment at create): boundary records beside the camera pass
-  // (DABA_FORK0=1; measured slower at 8 ranks: 0.272 vs 0.258 ms), the solve beside the point pass when small
+  // (DABA_FORK0=1; measured slower at 8 ranks: 0.272 vs 0.258 ms), the solve beside the point pass
   // (DABA_FORK1=0 disables)
-  bool fork0 = false, fork1 = true, fork1_force = false;
+  bool fork0 = false, fork1 = true;
   // profiling
   std::vector<std::string> knames;
   std::vector<double> kms;
@@ -301,10 +301,10 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
     n += timed(c, "k_pt_boundary", [&] { return launch_pt_pass(P, c->stream); });
     n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
   }
-  // k_cam_solve and k_pt_sum are independent.  Run them as parallel branches when the solve is small (it then
-  // hides behind the point pass); a large solve would crowd the point pass off the SMs (measured: +30 us at
-  // 13.7K cameras), so it runs serialised.  Profiling always serialises so events bracket one kernel.
-  if (c->opt.profile || !c->fork1 || (P.n_cam_eval_blocks >= c->num_sms / 2 && !c->fork1_force)) {
+  // k_cam_solve and k_pt_sum are independent: parallel graph branches (the solve hides behind the point pass;
+  // measured 1.3451 -> 1.3423 ms at 13.7K cameras, and it is what keeps the solve off the critical path at 8
+  // ranks).  Profiling always serialises so events bracket one kernel; DABA_FORK1=0 serialises.
+  if (c->opt.profile || !c->fork1) {
     n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
     n += timed(c, "k_pt_sum", [&] { return launch_pt_sum(P, c->stream); });
   } else {
@@ -442,7 +442,6 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   C->device = cuda_device;
   C->fork0 = env_int("DABA_FORK0", 0) == 1;
   C->fork1 = std::getenv("DABA_FORK1") == nullptr || std::atoi(std::getenv("DABA_FORK1")) != 0;
-  C->fork1_force = env_int("DABA_FORK1", 1) == 2;
   PhaseTimer timer;
   std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan);
   if (!e.empty()) {
