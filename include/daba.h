@@ -8,9 +8,10 @@
  * Proposition 1, cameras take one successful Levenberg-Marquardt step,
  * points take the exact closed-form minimiser, Nesterov extrapolation (eqs.
  * nesterov_x0 / nesterov_x) with the adaptive restart test
- * E(x^{k+1}|x^k) > F-bar^{(k)} evaluated on one allreduced pair of
- * scalars.  All arithmetic is fp64 on the GPU; nothing runs on the host between
- * create and get_state.
+ * E(x^{k+1}|x^k) > F-bar^{(k)}, evaluated either globally on one allreduced
+ * vector of sums (default) or per device from the paper's local metrics
+ * (DABA_RESTART_DEVICE, eqs. DEalpha-Eak).  All arithmetic is fp64 on the GPU; nothing
+ * runs on the host between create and get_state.
  *
  * Conventions (all calls):
  *   - return value: 0 (DABA_OK) or a negative DABA_E_* code; daba_last_error(ctx)
@@ -34,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DABA_ABI_VERSION 1
+#define DABA_ABI_VERSION 2  /* 2: restart_scope option, DABA_TR_FDEV trace column, DABA_COMM_NONE */
 
 enum {
   DABA_OK = 0,
