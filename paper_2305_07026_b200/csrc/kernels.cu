@@ -43,8 +43,8 @@ __device__ __forceinline__ void st256(double4* q, double4 v) {
 }
 
 // Point-side record of observation r at anchor a (0: x-bar^k, 1: x^k), 32 B, in two separate arrays.  (The two
-// anchors' records side by side, 64 B, measured neutral on Final-13682: k_pt_sum -0.04 ms, k_cam_pass +0.03 ms,
-// the two anchors' CTAs then writing half lines.)
+// anchors' records side by side, 64 B: with one CTA per chunk and anchor k_pt_sum -0.04 / k_cam_pass +0.03 ms;
+// with both anchors in one CTA k_pt_sum +0.025 / k_cam_pass +0.033 ms.)
 __device__ __forceinline__ double4* rec_ptr(const IterParams& p, int64_t r, int a) {
   return reinterpret_cast<double4*>(p.staging + (a ? 4 * p.n_records : 0)) + r;
 }
