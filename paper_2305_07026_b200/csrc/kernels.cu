@@ -13,9 +13,13 @@
 //                           successful Levenberg-Marquardt step by Jacobi-scaled 9x9 Cholesky, the
 //                           candidates' x-bar^{k+1} (eqs. nesterov_R/t/d, ProjRot3D eq. proj_rot3d
 //                           P:L332-337), and the camera part of E(x_acc|x^k) and F(x^k)
-//   a9     k_reduce         deterministic sums (-> allreduce when nranks > 1)
-//   a9+a10 k_select         F-bar (eq. lFak), restart test (Alg. 1), role rotation;
-//                           folded into k_reduce when the rank has no communicator
+//   a9     final_reduce     deterministic rank sums, in the last block of k_cam_solve / k_pt_sum (-> allreduce
+//                           when nranks > 1)
+//   a9+a10 do_select        F-bar (eq. lFak), restart test (Alg. 1), role rotation: in
+//                           that last block without a communicator (or with the per-device test, k_inter adding
+//                           the inter-device terms of eq. DEalpha), else after the allreduce in k_unpack (which
+//                           also writes the received halo) or k_select
+//          k_pack / k_unpack halo send / receive buffers (N > 1); k_lbar_all, k_objective at create / resume
 #include <cstdio>
 
 #include "kernels.h"
