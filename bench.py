@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="final13682")
     ap.add_argument("--restart", default="global", choices=["global", "device"])
+    # test plumbing: "none" runs every rank's shard alone (DABA_COMM_NONE: no collectives, NOT the method's
+    # iterates) so that the multi-rank driver logic can be exercised on a one-GPU box
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "none"])
     ap.add_argument("--impl", default="daba", choices=["daba", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -183,6 +186,7 @@ def main():
 
     import paper_2305_07026_b200 as daba
 
+    local = local % max(torch.cuda.device_count(), 1) if a.comm == "none" else local
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo", init_method="env://")
@@ -190,7 +194,7 @@ def main():
 
     def fresh_key():
         # every context gets its own NCCL communicator, hence its own unique id (rank 0 draws, all receive)
-        if world == 1:
+        if world == 1 or a.comm == "none":
             return None
         obj = [daba.comm_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -198,6 +202,7 @@ def main():
 
     stream = torch.cuda.Stream(device=local)
     kw = dict(loss=p.loss, loss_scale=p.loss_scale, rank=rank, nranks=world, device=local,
+              comm=daba.COMM_NONE if a.comm == "none" else daba.COMM_NCCL,
               restart_scope=1 if a.restart == "device" else 0)
 
     # ---------------- device-resident timed region (production path: one CUDA graph per iteration)

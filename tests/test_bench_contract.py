@@ -42,3 +42,22 @@ def test_device_arm_contract():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 3 * 5
     assert "workload" in d["config"] and d["config"]["workload"] == "small_huber"
+
+
+@pytest.mark.gpu
+def test_multi_rank_driver_flow_one_gpu():
+    """torchrun with 2 ranks on one GPU and the measurement-only transport (no collectives): bench.py's
+    multi-rank plumbing (rendezvous, barriers, max-over-ranks timing, rank-0 output) end to end."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "4", "--warmup", "3", "--config", "small_huber", "--comm", "none",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "camera-partitioned x2"
