@@ -491,3 +491,20 @@ def test_shared_anchor_camera_ctas(name, monkeypatch):
         assert (np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])).max() <= F_TOL
         np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
         assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
+
+
+@pytest.mark.parametrize("shared", ["0", "1"])
+def test_cameras_split_into_many_chunks(shared, monkeypatch):
+    """Every camera split into chunks of at most 64 observations (partial moments summed per camera by the
+    solve), in both camera-pass CTA layouts: the oracle's trajectory."""
+    monkeypatch.setenv("DABA_CHUNK_OBS", "64")
+    monkeypatch.setenv("DABA_CAM_SHARED", shared)
+    p = gen.generate("small_huber")
+    o = oracle_for(p, eta=1.0)
+    tro = o.iterate(20)
+    with solver(p, eta=1.0) as s:
+        assert s.shard_info()["cam_side_obs"] == p.K
+        trg = s.iterate_trace(20)
+        assert (np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])).max() <= F_TOL
+        np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
