@@ -84,7 +84,8 @@ __device__ __forceinline__ void extrapolate_camera(const double* ck, const doubl
 // Moment slots (anchor camera frame; e = camera-frame reprojection error, s = |u|^2):
 //  0 w ux^2   1 w ux uy  2 w uy^2   3-5 w ux s^m  6-8 w uy s^m  9-13 w s^m (m=0..4)
 //  14 w lam ux  15 w lam uy  16-18 w lam s^m  19 w lam^2
-//  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e
+//  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e   (e = R e, world frame;
+//        k_cam_solve rotates them into the anchor camera frame: the camera pass never applies R^T)
 //  38 w |e|^2   39 a   [40 degenerate pairs]
 // Camera record kept in shared memory and re-read at every use (volatile shared loads are not hoisted into
 // registers): frees ~30 registers per thread in the camera pass, i.e. more resident CTAs per SM (a copy in
@@ -119,12 +120,14 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
       st256(rec_ptr(p, rec, ACC ? 0 : 1), make_double4(0.0, 0.0, 0.0, 0.0));
     return;
   }
-  // camera-frame point R^T (l - t)
-  const double cx = fma(c[0], vx, fma(c[3], vy, c[6] * vz));
-  const double cy = fma(c[1], vx, fma(c[4], vy, c[7] * vz));
-  const double cz = fma(c[2], vx, fma(c[5], vy, c[8] * vz));
-  const double lam = fma(cx, u.x, fma(cy, u.y, cz * pz)) * __drcp_rn(nv);  // eq. gamma
-  const double ex = fma(-lam, cx, u.x), ey = fma(-lam, cy, u.y), ez = fma(-lam, cz, pz);  // eq. error
+  // world-frame ray R p, lambda = (l - t).R p / |l - t|^2 (eq. gamma), world-frame error R e = R p - lambda (l - t)
+  // (eq. error): the moments of e are accumulated in the world frame and rotated by R_hat^T once per camera in
+  // k_cam_solve (they are linear in e), and R e is also the point-side record's vector
+  const double rx = fma(c[0], u.x, fma(c[1], u.y, c[2] * pz));
+  const double ry = fma(c[3], u.x, fma(c[4], u.y, c[5] * pz));
+  const double rz = fma(c[6], u.x, fma(c[7], u.y, c[8] * pz));
+  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * __drcp_rn(nv);  // eq. gamma
+  const double ex = fma(-lam, vx, rx), ey = fma(-lam, vy, ry), ez = fma(-lam, vz, rz);  // R e (eq. error)
   const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
   double rho = 0;
   const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
@@ -175,12 +178,8 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   }
   // point side of the same pair: (w lam^2, w lam R e) with the world-frame error R e (eq. Q's sums), written
   // coalesced at the camera-side index (one 32-byte record per anchor)
-  const double gx = fma(c[0], ex, fma(c[1], ey, c[2] * ez));
-  const double gy = fma(c[3], ex, fma(c[4], ey, c[5] * ez));
-  const double gz = fma(c[6], ex, fma(c[7], ey, c[8] * ez));
   if (rec >= 0)
-    st256(rec_ptr(p, rec, ACC ? 0 : 1),
-          make_double4(wl * lam, wl * gx, wl * gy, wl * gz));
+    st256(rec_ptr(p, rec, ACC ? 0 : 1), make_double4(wl * lam, wl * ex, wl * ey, wl * ez));
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -763,6 +762,15 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
     for (int k = 0; k < 9; ++k) Rh[k] = anchor[k];
     for (int k = 0; k < 3; ++k) th[k] = anchor[9 + k];
     for (int k = 0; k < 3; ++k) dh[k] = anchor[12 + k];
+    // the camera pass accumulated the error moments (slots 20..37: e times u_x, u_y, 1, s, s^2, lambda) in the
+    // world frame: rotate each 3-vector into the anchor camera frame, e = R_hat^T (R e)
+    for (int gq = 0; gq < 6; ++gq) {
+      double* v = m + 20 + 3 * gq;
+      const double a0 = v[0], a1 = v[1], a2 = v[2];
+      v[0] = fma(Rh[0], a0, fma(Rh[3], a1, Rh[6] * a2));
+      v[1] = fma(Rh[1], a0, fma(Rh[4], a1, Rh[7] * a2));
+      v[2] = fma(Rh[2], a0, fma(Rh[5], a1, Rh[8] * a2));
+    }
     derive_sums(m, dh, S);
     double H[81], g[9];
     normal_equations(Rh, S, p.xi, H, g);
