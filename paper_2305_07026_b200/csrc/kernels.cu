@@ -153,22 +153,22 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   acc[17] = fma(wl, s, acc[17]);
   acc[18] = fma(wl, s2, acc[18]);
   acc[19] = fma(wl, lam, acc[19]);
-  const double wex = w * ex, wey = w * ey, wez = w * ez;
-  acc[20] = fma(wex, u.x, acc[20]);
-  acc[21] = fma(wey, u.x, acc[21]);
-  acc[22] = fma(wez, u.x, acc[22]);
-  acc[23] = fma(wex, u.y, acc[23]);
-  acc[24] = fma(wey, u.y, acc[24]);
-  acc[25] = fma(wez, u.y, acc[25]);
-  acc[26] += wex;
-  acc[27] += wey;
-  acc[28] += wez;
-  acc[29] = fma(wex, s, acc[29]);
-  acc[30] = fma(wey, s, acc[30]);
-  acc[31] = fma(wez, s, acc[31]);
-  acc[32] = fma(wex, s2, acc[32]);
-  acc[33] = fma(wey, s2, acc[33]);
-  acc[34] = fma(wez, s2, acc[34]);
+  // error moments from the weighted factors already formed (w u_x, w u_y, w, w s, w s^2, w lam): one FMA each
+  acc[20] = fma(wx, ex, acc[20]);
+  acc[21] = fma(wx, ey, acc[21]);
+  acc[22] = fma(wx, ez, acc[22]);
+  acc[23] = fma(wy, ex, acc[23]);
+  acc[24] = fma(wy, ey, acc[24]);
+  acc[25] = fma(wy, ez, acc[25]);
+  acc[26] = fma(w, ex, acc[26]);
+  acc[27] = fma(w, ey, acc[27]);
+  acc[28] = fma(w, ez, acc[28]);
+  acc[29] = fma(ws, ex, acc[29]);
+  acc[30] = fma(ws, ey, acc[30]);
+  acc[31] = fma(ws, ez, acc[31]);
+  acc[32] = fma(ws2, ex, acc[32]);
+  acc[33] = fma(ws2, ey, acc[33]);
+  acc[34] = fma(ws2, ez, acc[34]);
   acc[35] = fma(wl, ex, acc[35]);
   acc[36] = fma(wl, ey, acc[36]);
   acc[37] = fma(wl, ez, acc[37]);
