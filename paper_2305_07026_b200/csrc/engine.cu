@@ -369,6 +369,13 @@ int upload_states(daba_ctx* c, const double* cams_k, const double* pts_k, const 
   for (int pass = 0; pass < 2; ++pass) {
     const double* gc = pass ? cams_km1 : cams_k;
     const double* gp = pass ? pts_km1 : pts_k;
+    if (pass == 1 && cams_km1 == cams_k && pts_km1 == pts_k) {  // x^{k-1} = x^k (create): a device copy
+      CUDA_OR(c, cudaMemcpyAsync(c->P.cams[h_roles[rkm1]], c->P.cams[h_roles[rk]], hc.size() * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OR(c, cudaMemcpyAsync(c->P.pts[h_roles[rkm1]], c->P.pts[h_roles[rk]], hp.size() * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+      break;
+    }
     parallel_for((int64_t)S.cam_g.size(), [&](int64_t a, int64_t b) {
       for (int64_t li = a; li < b; ++li) {
         std::memcpy(&hc[(size_t)li * kCamStride], gc + 15 * (size_t)S.cam_g[(size_t)li], 15 * sizeof(double));
@@ -443,35 +450,28 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   C->fork0 = env_int("DABA_FORK0", 0) == 1;
   C->fork1 = std::getenv("DABA_FORK1") == nullptr || std::atoi(std::getenv("DABA_FORK1")) != 0;
   PhaseTimer timer;
-  std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan);
+  // point numbering for locality (shard.h); DABA_POINT_ORDER = 0 off, 1 automatic (default), 2 always
+  const int64_t point_order = env_int("DABA_POINT_ORDER", 1);
+  const int32_t point_far = (int32_t)env_int("DABA_POINT_FAR", 1024);  // "far apart" in camera ids
+  // one rank with input sorted by (camera, point): a light host plan, the point side built on the device
+  const bool defer = nranks == 1 && point_order != 2 && env_int("DABA_DEVICE_PLAN", 1) != 0;
+  std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, defer);
   if (!e.empty()) {
     *out = nullptr;
     return DABA_E_INVALID_ARG;
   }
   timer.mark("plan_shard");
-  {  // point numbering for locality (shard.h); DABA_POINT_ORDER = 0 off, 1 automatic (default), 2 always
-    const int64_t po = env_int("DABA_POINT_ORDER", 1);
-    if (po != 0) order_owned_points(&C->plan, obs_cam, po == 2);
-  }
+  if (!C->plan.point_side_deferred && point_order != 0)
+    order_owned_points(&C->plan, obs_cam, point_order == 2, point_far);
   timer.mark("point order");
-  // native cameras and Assumption 2 at x^0
+  // native cameras (Assumption 2 at x^0, is checked on the device by the first objective evaluation)
   std::vector<double> nat((size_t)M * 15);
   for (int64_t i = 0; i < M; ++i) {
     double tmp[16];
     bal_to_native(cameras + 9 * i, tmp);
     std::memcpy(&nat[(size_t)i * 15], tmp, 15 * sizeof(double));
   }
-  std::atomic<bool> degenerate(false);
-  parallel_for(K, [&](int64_t k0, int64_t k1) {
-    for (int64_t k = k0; k < k1; ++k) {
-      const double* t = &nat[(size_t)obs_cam[k] * 15 + 9];
-      const double* l = points + 3 * (int64_t)obs_pt[k];
-      const double dx = l[0] - t[0], dy = l[1] - t[1], dz = l[2] - t[2];
-      if (!(dx * dx + dy * dy + dz * dz > o.eps * o.eps)) degenerate = true;
-    }
-  });
-  if (degenerate) return DABA_E_DEGENERATE;
-  timer.mark("native + Assumption 2");
+  timer.mark("native cameras");
   // device and stream
   if (cudaSetDevice(cuda_device) != cudaSuccess) return DABA_E_CUDA;
   if (o.stream) {
@@ -504,6 +504,35 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     daba_destroy(c.release());
     return code;
   };
+  // light plan: decide on the device whether the input point numbering follows the cameras; if not, fall back
+  // to the full host plan with the locality renumbering.  d_opt (the observations' points on the device)
+  // becomes the camera side's point index.
+  int32_t* d_opt = nullptr;
+  if (C->plan.point_side_deferred) {
+    int32_t* d_ocam = nullptr;
+    if (cudaMalloc(&d_opt, sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1)) != cudaSuccess ||
+        cudaMalloc(&d_ocam, sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1)) != cudaSuccess) {
+      cudaFree(d_opt);
+      cudaFree(d_ocam);
+      return bail(DABA_E_OOM);
+    }
+    C->allocs.push_back(d_opt);
+    C->dev_bytes += sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1);
+    if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
+        h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess) {
+      cudaFree(d_ocam);
+      return bail(DABA_E_CUDA);
+    }
+    const int64_t jumps = count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far, C->stream);
+    cudaFree(d_ocam);
+    if (jumps < 0) return bail(DABA_E_CUDA);
+    if (point_order != 0 && jumps * 4 >= N && N > 1) {  // scattered numbering: full plan, renumbered
+      std::string e2 = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, false);
+      if (!e2.empty()) return bail(DABA_E_INVALID_ARG);
+      order_owned_points(&C->plan, obs_cam, true);
+    }
+    timer.mark("device point-order check");
+  }
   const ShardPlan& S = C->plan;
   IterParams& P = C->P;
   P.n_cams = (int32_t)S.cam_g.size();
@@ -541,11 +570,15 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // camera side + chunks
   const int64_t chunk_obs = std::max<int64_t>(64, std::min<int64_t>(kCamChunkObs, env_int("DABA_CHUNK_OBS", kCamChunkObs)));
   {
-    const size_t kc = S.c_obs.size();
+    const bool light = S.point_side_deferred;
+    const size_t kc = light ? (size_t)K : S.c_obs.size();
     double2* duv;
-    int32_t* dpt;
-    if ((rc = dalloc(C, &duv, kc)) || (rc = dalloc(C, &dpt, kc))) return bail(rc);
-    CUDA_OR(C, h2d(C, dpt, S.c_pt.data(), kc * sizeof(int32_t)));
+    int32_t* dpt = d_opt;
+    if ((rc = dalloc(C, &duv, kc))) return bail(rc);
+    if (!light) {
+      if ((rc = dalloc(C, &dpt, kc))) return bail(rc);
+      CUDA_OR(C, h2d(C, dpt, S.c_pt.data(), kc * sizeof(int32_t)));
+    }
     if (S.cam_side_identity) {
       // one rank, input sorted by (camera, point): the camera-side pixels are the input itself (no host copy)
       CUDA_OR(C, h2d(C, duv, obs_uv, kc * sizeof(double2)));
@@ -587,14 +620,35 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   timer.mark("camera side");
   // point side: records written by the camera pass at its observation index; boundary observations (camera
   // owned elsewhere) are recomputed into records n_cam_side + b
+  std::vector<int32_t> bcam, bpt;
+  std::vector<double2> buv;
   {
+    if (S.point_side_deferred) {  // light plan: every point's records in camera order, sorted on the device
+      int64_t* dptr;
+      int32_t* dsrc;
+      if ((rc = dalloc(C, &dptr, (size_t)N + 1)) || (rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1))))
+        return bail(rc);
+      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, C->stream) != 0) return bail(DABA_E_CUDA);
+      P.p_ptr = dptr;
+      P.p_src = dsrc;
+      P.n_cam_side = K;
+      P.n_boundary = 0;
+      P.n_records = std::max<int64_t>(K, 1);
+      if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
+      const int32_t *d1, *d2;
+      const double2* d4;
+      if ((rc = upload(C, const_cast<int32_t**>(&d1), bcam)) || (rc = upload(C, const_cast<int32_t**>(&d2), bpt)) ||
+          (rc = upload(C, const_cast<double2**>(&d4), buv)))
+        return bail(rc);
+      P.b_cam = d1;
+      P.b_pt = d2;
+      P.b_uv = d4;
+    } else {
     const size_t kp = S.p_obs.size(), kc = S.c_obs.size();
     const int64_t* dptr;
     if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
     P.p_ptr = dptr;
     hvec<int32_t> src(kp);
-    std::vector<int32_t> bcam, bpt;
-    std::vector<double2> buv;
     if (S.cam_side_identity) {  // the camera-side index of observation o is o
       parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
         for (int64_t q = a; q < b; ++q) src[q] = S.p_obs[q];
@@ -631,12 +685,14 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.b_cam = d1;
     P.b_pt = d2;
     P.b_uv = d4;
+    }
+    const size_t kc = S.point_side_deferred ? (size_t)K : S.c_obs.size();  // camera-side observations
     // per-device restart: the inter-device pairs of this rank (camera side with a halo point: sign +1; point
     // side with a halo camera: sign -1)
     if (P.restart_scope == 1) {
       std::vector<int32_t> ic, ip, is;
       std::vector<double2> iu;
-      for (size_t q = 0; q < kc; ++q)
+      for (size_t q = 0; q < (S.point_side_deferred ? 0 : kc); ++q)  // (a light plan has no halo)
         if (S.c_pt[q] >= S.n_own_pts) {
           ic.push_back(S.c_cam[q]);
           ip.push_back(S.c_pt[q]);
@@ -768,6 +824,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
   double F0 = 0, nd = 0;
   if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
+  if (nd > 0) return bail(DABA_E_DEGENERATE);  // Assumption 2: ||l_j - t_i|| <= eps for some pair
   if (P.restart_scope == 1) {
     // eq. Fainit per device: F-bar^{a(-1)} = F^{a(-1)} = E^a(x^{a(0)} | x^{(0)}) = F_kappa(x^0): the rank's
     // camera-side F with its inter-device pairs at weight 1/2 (k_inter at x^{-1} = x^0); D^{a(-1)} = 0
@@ -994,8 +1051,8 @@ extern "C" int daba_shard_info(daba_ctx* ctx, int64_t info[8]) {
   info[1] = S.n_own_pts;
   info[2] = (int64_t)S.cam_g.size() - S.n_own_cams;
   info[3] = (int64_t)S.pt_g.size() - S.n_own_pts;
-  info[4] = (int64_t)S.c_obs.size();
-  info[5] = (int64_t)S.p_obs.size();
+  info[4] = S.point_side_deferred ? S.K : (int64_t)S.c_obs.size();
+  info[5] = S.point_side_deferred ? S.K : (int64_t)S.p_obs.size();
   info[6] = 16 * S.send_doubles;  // both candidates of each boundary variable, 8 B each
   info[7] = (int64_t)ctx->dev_bytes;
   return DABA_OK;

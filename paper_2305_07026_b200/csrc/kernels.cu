@@ -20,6 +20,7 @@
 //                           the inter-device terms of eq. DEalpha), else after the allreduce in k_unpack (which
 //                           also writes the received halo) or k_select
 //          k_pack / k_unpack halo send / receive buffers (N > 1); k_lbar_all, k_objective at create / resume
+#include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
 
 #include "kernels.h"
@@ -1283,6 +1284,83 @@ int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* ca
   k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
                                                       select_inside);
   return 1;
+}
+
+// ------------------------------------------------------------------ create-time point side on the device
+// (one rank, input sorted by (camera, point): the observation index is the camera-side record index)
+__global__ void k_iota(int32_t* v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+__global__ void k_fill_i32(int32_t* v, int64_t n, int32_t x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = x;
+}
+__global__ void k_min_camera(const int32_t* cam, const int32_t* pt, int64_t K, int32_t* key) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q < K) atomicMin(key + pt[q], cam[q]);
+}
+// consecutive points whose smallest cameras lie more than `far` ids apart (shard.h order_owned_points)
+__global__ void k_count_jumps(const int32_t* key, int64_t n, int32_t far, unsigned long long* out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool jump = j + 1 < n && abs(key[j + 1] - key[j]) > far;
+  const unsigned m = __ballot_sync(0xffffffffu, jump);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, (unsigned long long)__popc(m));
+}
+// CSR offsets from keys sorted ascending: ptr[j] = first position with key >= j, ptr[N] = K
+__global__ void k_ptr_from_sorted(const int32_t* keys, int64_t K, int32_t N, int64_t* ptr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int32_t k = keys[i], kp = i > 0 ? keys[i - 1] : -1;
+  for (int32_t j = kp + 1; j <= k; ++j) ptr[j] = i;
+  if (i == K - 1)
+    for (int32_t j = k + 1; j <= N; ++j) ptr[j] = K;
+}
+
+static inline unsigned grid(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+int64_t count_point_jumps_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int32_t N, int32_t far,
+                                 cudaStream_t st) {
+  int32_t* key = nullptr;
+  unsigned long long* cnt = nullptr;
+  if (cudaMalloc(&key, sizeof(int32_t) * (size_t)(N > 0 ? N : 1)) != cudaSuccess ||
+      cudaMalloc(&cnt, sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st);
+  if (N > 0) k_fill_i32<<<grid(N), 256, 0, st>>>(key, N, 0x7fffffff);
+  if (K > 0) k_min_camera<<<grid(K), 256, 0, st>>>(d_cam, d_pt, K, key);
+  if (N > 1) k_count_jumps<<<grid(N), 256, 0, st>>>(key, N, far, cnt);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(key);
+  cudaFree(cnt);
+  return e == cudaSuccess ? (int64_t)h : -1;
+}
+
+int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, cudaStream_t st) {
+  if (K == 0) {
+    cudaMemsetAsync(d_ptr, 0, sizeof(int64_t) * ((size_t)N + 1), st);
+    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : -1;
+  }
+  int32_t *vals = nullptr, *keys_out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int bits = 1;
+  while ((int64_t(1) << bits) < (int64_t)N) ++bits;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_pt, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)K, 0, bits, st);
+  if (cudaMalloc(&vals, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
+      cudaMalloc(&keys_out, sizeof(int32_t) * (size_t)K) != cudaSuccess || cudaMalloc(&tmp, tmp_bytes) != cudaSuccess)
+    return -1;
+  k_iota<<<grid(K), 256, 0, st>>>(vals, K);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, d_pt, keys_out, vals, d_src, (int)K, 0, bits, st);  // stable
+  k_ptr_from_sorted<<<grid(K), 256, 0, st>>>(keys_out, K, N, d_ptr);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(vals);
+  cudaFree(keys_out);
+  cudaFree(tmp);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace daba

@@ -112,7 +112,7 @@ struct Tm {
 
 std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, const int32_t* obs_pt,
                        const int32_t* cam_owner_in, const int32_t* pt_owner_in, int rank, int nranks,
-                       ShardPlan* out) {
+                       ShardPlan* out, bool defer_point_side) {
   char msg[256];
   Tm tm;
   if (M < 0 || N < 0 || K < 0 || nranks < 1 || rank < 0 || rank >= nranks) return "invalid sizes or rank";
@@ -150,7 +150,8 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
   }
   tm.mark("validate");
   // ---- observations in (camera, point) order; duplicate (i,j) check
-  hvec<int32_t> cam_sorted((size_t)K);
+  const bool light = defer_point_side && sorted && nranks == 1 && !cam_owner_in && !pt_owner_in;
+  hvec<int32_t> cam_sorted(light ? 0 : (size_t)K);
   std::vector<int64_t> cptr((size_t)M + 1, 0);
   if (sorted) {
     const unsigned T = nthreads(K);
@@ -158,13 +159,32 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
     pfor(K, [&](int64_t a, int64_t b, int t) {
       std::vector<int64_t>& c = part[(size_t)t];
       for (int64_t k = a; k < b; ++k) {
-        cam_sorted[(size_t)k] = (int32_t)k;
+        if (!light) cam_sorted[(size_t)k] = (int32_t)k;
         ++c[(size_t)obs_cam[k]];
       }
     });
     for (unsigned t = 0; t < T; ++t)
       for (int64_t i = 0; i < M; ++i) cptr[(size_t)i + 1] += part[t][(size_t)i];
     for (int64_t i = 0; i < M; ++i) cptr[(size_t)i + 1] += cptr[(size_t)i];
+    if (light) {  // one rank owns everything in input order; the point side is the engine's (on the device)
+      P.cam_owner.assign((size_t)M, 0);
+      P.pt_owner.assign((size_t)N, 0);
+      P.cam_g.resize((size_t)M);
+      P.pt_g.resize((size_t)N);
+      pfor(M, [&](int64_t a, int64_t b, int) {
+        for (int64_t i = a; i < b; ++i) P.cam_g[(size_t)i] = (int32_t)i;
+      });
+      pfor(N, [&](int64_t a, int64_t b, int) {
+        for (int64_t j = a; j < b; ++j) P.pt_g[(size_t)j] = (int32_t)j;
+      });
+      P.n_own_cams = (int32_t)M;
+      P.n_own_pts = (int32_t)N;
+      P.cam_ptr = cptr;
+      P.cam_side_identity = true;
+      P.point_side_deferred = true;
+      tm.mark("light plan");
+      return "";
+    }
   } else {
     hvec<int32_t> all((size_t)K);
     pfor(K, [&](int64_t a, int64_t b, int) {
@@ -362,7 +382,7 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
   return "";
 }
 
-bool order_owned_points(ShardPlan* S, const int32_t* obs_cam, bool force) {
+bool order_owned_points(ShardPlan* S, const int32_t* obs_cam, bool force, int32_t far) {
   const int32_t np = S->n_own_pts;
   if (np < 2) return false;
   // key: smallest global camera observing the point (M if none)
@@ -380,7 +400,7 @@ bool order_owned_points(ShardPlan* S, const int32_t* obs_cam, bool force) {
   std::atomic<int64_t> jumps(0);
   pfor(np - 1, [&](int64_t a, int64_t b, int) {
     int64_t d = 0;
-    for (int64_t j = a; j < b; ++j) d += std::abs(key[(size_t)j + 1] - key[(size_t)j]) > 1024;
+    for (int64_t j = a; j < b; ++j) d += std::abs(key[(size_t)j + 1] - key[(size_t)j]) > far;
     jumps += d;
   });
   if (!force && jumps.load() * 4 < (int64_t)np) return false;

@@ -57,6 +57,8 @@ struct ShardPlan {
   hvec<int32_t> c_cam, c_pt;
   hvec<int32_t> c_obs;
   bool cam_side_identity = false;               // c_obs[q] = q (1 rank, input sorted by (camera, point))
+  bool point_side_deferred = false;             // light plan: c_* and p_* not built (the engine builds the
+                                                // point side on the device; identity camera side)
   std::vector<int64_t> cam_ptr;                 // n_own_cams + 1 offsets into the camera side
   // point side (sorted by point, then camera)
   hvec<int32_t> p_cam, p_pt;
@@ -73,11 +75,14 @@ struct ShardPlan {
 // 0.58 ms, camera pass 0.88 -> 0.76 ms, for ≈ 0.4 s more in daba_create.  The generator's host-camera numbering
 // is kept (renumbering it would save 0.04 ms per iteration for the same create cost).  Returns whether it
 // renumbered.
-bool order_owned_points(ShardPlan* plan, const int32_t* obs_cam, bool force = false);
+bool order_owned_points(ShardPlan* plan, const int32_t* obs_cam, bool force = false, int32_t far = 1024);
 
 // Build rank `rank`'s shard.  cam_owner/pt_owner may be null (defaults above).  Returns "" or an error message
 // (index out of range, duplicate (i,j), owner out of range).
+// defer_point_side: with one rank and input sorted by (camera, point), stop after the camera offsets (a light
+// plan, point_side_deferred) — the engine derives the rest on the device.
 std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, const int32_t* obs_pt,
-                       const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks, ShardPlan* out);
+                       const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks, ShardPlan* out,
+                       bool defer_point_side = false);
 
 }  // namespace daba

@@ -508,3 +508,16 @@ def test_cameras_split_into_many_chunks(shared, monkeypatch):
         assert (np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])).max() <= F_TOL
         np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
         assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
+
+
+def test_device_plan_falls_back_to_renumbering(monkeypatch):
+    """One rank, sorted input with scattered point ids: the device-side check of the light plan (a jump
+    threshold of 1 camera id here) sends create to the full host plan with the locality renumbering."""
+    monkeypatch.setenv("DABA_POINT_FAR", "1")
+    p = gen.generate("small_cauchy", shuffle_points=True)
+    o = oracle_for(p)
+    tro = o.iterate(15)
+    with solver(p) as s:
+        trg = s.iterate_trace(15)
+        assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= X_TOL
