@@ -261,10 +261,13 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         se = daba.Solver(hc, hpnt, hoc, hop, huv, stream=stream.cuda_stream, comm_key=key, **kw)
+        t_c = time.perf_counter()
         Ftr, _ = se.iterate(a.steps, F_trace=True)
+        t_i = time.perf_counter()
         cams_out, pts_out, _ = se.state()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
+        phases = {"create_s": round(t_c - t0, 4), "iterate_s": round(t_i - t_c, 4), "state_s": round(te - (t_i - t0), 4)}
         se.close()
         if world > 1:
             t = torch.tensor([te], dtype=torch.float64)
@@ -274,7 +277,7 @@ def main():
         d2h = (8 * a.steps + 1 * a.steps + cams_out.nbytes + pts_out.nbytes) / a.steps
         e2e = {"value": a.steps * p.K / te, "unit": "obs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "includes": "daba_create (host shard plan + H2D) + iterations with "
-               "per-step F readback + daba_get_state"}
+               "per-step F readback + daba_get_state", "phases": phases}
 
     if rank != 0:
         if world > 1:

@@ -509,27 +509,24 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // becomes the camera side's point index.
   int32_t* d_opt = nullptr;
   if (C->plan.point_side_deferred) {
-    int32_t* d_ocam = nullptr;
-    if (cudaMalloc(&d_opt, sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1)) != cudaSuccess ||
-        cudaMalloc(&d_ocam, sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1)) != cudaSuccess) {
-      cudaFree(d_opt);
-      cudaFree(d_ocam);
-      return bail(DABA_E_OOM);
-    }
-    C->allocs.push_back(d_opt);
-    C->dev_bytes += sizeof(int32_t) * (size_t)std::max<int64_t>(K, 1);
+    // the record staging buffer (64 B per observation) is allocated now and lends its memory to the setup
+    // temporaries (no allocate / free churn at create)
+    IterParams& Q = C->P;
+    Q.n_records = std::max<int64_t>(K, 1);
+    if ((rc = dalloc(C, &Q.staging, 8 * (size_t)Q.n_records)) || (rc = dalloc(C, &d_opt, (size_t)Q.n_records)))
+      return bail(rc);
+    int32_t* d_ocam = reinterpret_cast<int32_t*>(Q.staging);
     if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
-        h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess) {
-      cudaFree(d_ocam);
+        h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess)
       return bail(DABA_E_CUDA);
-    }
-    const int64_t jumps = count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far, C->stream);
-    cudaFree(d_ocam);
+    const int64_t jumps = count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far,
+                                                   Q.staging + ((size_t)K + 7) / 2, C->stream);
     if (jumps < 0) return bail(DABA_E_CUDA);
     if (point_order != 0 && jumps * 4 >= N && N > 1) {  // scattered numbering: full plan, renumbered
       std::string e2 = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, false);
       if (!e2.empty()) return bail(DABA_E_INVALID_ARG);
       order_owned_points(&C->plan, obs_cam, true);
+      Q.staging = nullptr;  // (re-allocated at its final size by the full path; this one stays until destroy)
     }
     timer.mark("device point-order check");
   }
@@ -628,13 +625,13 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       int32_t* dsrc;
       if ((rc = dalloc(C, &dptr, (size_t)N + 1)) || (rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1))))
         return bail(rc);
-      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, C->stream) != 0) return bail(DABA_E_CUDA);
+      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, P.staging, 64 * (size_t)P.n_records,
+                                 C->stream) != 0)
+        return bail(DABA_E_CUDA);
       P.p_ptr = dptr;
       P.p_src = dsrc;
       P.n_cam_side = K;
       P.n_boundary = 0;
-      P.n_records = std::max<int64_t>(K, 1);
-      if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
       const int32_t *d1, *d2;
       const double2* d4;
       if ((rc = upload(C, const_cast<int32_t**>(&d1), bcam)) || (rc = upload(C, const_cast<int32_t**>(&d2), bpt)) ||
@@ -935,19 +932,53 @@ extern "C" int daba_objective(daba_ctx* ctx, double* F_out) {
   return compute_objective(ctx, F_out, nullptr);
 }
 
-static int get_native(daba_ctx* c, int which, hvec<double>& hc, hvec<double>& hp) {
+// Reads the owned cameras (native records) into hc and, unless the points go straight to the caller, the owned
+// points into hp.  With the light plan (one rank, identity numbering) the points are packed to xyz on the device
+// (in the record staging buffer, free between iterations) and copied once into points_out: *direct = true.
+static int get_native(daba_ctx* c, int which, hvec<double>& hc, hvec<double>& hp, double* points_out, bool* direct) {
   int roles[4];
   CUDA_OR(c, cudaMemcpyAsync(roles, c->P.roles, sizeof roles, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR(c, cudaStreamSynchronize(c->stream));
   const int r = roles[which ? 0 : 1];
+  const ShardPlan& S = c->plan;
+  const int32_t np = c->P.n_own_pts;
+  *direct = S.point_side_deferred && np == S.N && c->P.staging &&
+            3 * (size_t)np <= 8 * (size_t)c->P.n_records;
   hc.resize((size_t)c->P.n_own_cams * kCamStride);
-  hp.resize((size_t)c->P.n_own_pts * 4);
   if (!hc.empty())
     CUDA_OR(c, cudaMemcpyAsync(hc.data(), c->P.cams[r], hc.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  if (!hp.empty())
-    CUDA_OR(c, cudaMemcpyAsync(hp.data(), c->P.pts[r], hp.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (*direct) {
+    if (points_out && np > 0) {
+      launch_pts_xyz(c->P.pts[r], c->P.staging, np, c->stream);
+      CUDA_OR(c, cudaGetLastError());
+      CUDA_OR(c, cudaMemcpyAsync(points_out, c->P.staging, 3 * (size_t)np * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    }
+  } else {
+    hp.resize((size_t)np * 4);
+    if (!hp.empty())
+      CUDA_OR(c, cudaMemcpyAsync(hp.data(), c->P.pts[r], hp.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  }
   CUDA_OR(c, cudaStreamSynchronize(c->stream));
   return DABA_OK;
+}
+
+// points of the host copy (not direct) to their global slots, and the owned mask
+static void scatter_points(const ShardPlan& S, const hvec<double>& hp, bool direct, double* points_out,
+                           uint8_t* owned_mask_out) {
+  if (direct) {
+    if (owned_mask_out) std::memset(owned_mask_out + S.M, 1, (size_t)S.N);
+    return;
+  }
+  parallel_for(S.n_own_pts, [&](int64_t a, int64_t b) {
+    for (int64_t lj = a; lj < b; ++lj) {
+      const int64_t g = S.pt_g[(size_t)lj];
+      if (points_out)
+        for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
+      if (owned_mask_out) owned_mask_out[S.M + g] = 1;
+    }
+  });
 }
 
 extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_out, double* points_out,
@@ -955,7 +986,8 @@ extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_o
   if (!ctx || which < 0 || which > 1) return DABA_E_INVALID_ARG;
   cudaSetDevice(ctx->device);
   hvec<double> hc, hp;
-  int rc = get_native(ctx, which, hc, hp);
+  bool direct = false;
+  int rc = get_native(ctx, which, hc, hp, points_out, &direct);
   if (rc) return rc;
   const ShardPlan& S = ctx->plan;
   if (owned_mask_out) std::memset(owned_mask_out, 0, (size_t)(S.M + S.N));
@@ -964,14 +996,7 @@ extern "C" int daba_get_state_native(daba_ctx* ctx, int which, double* cameras_o
     if (cameras_out) std::memcpy(cameras_out + 15 * g, &hc[(size_t)li * kCamStride], 15 * sizeof(double));
     if (owned_mask_out) owned_mask_out[g] = 1;
   }
-  parallel_for(S.n_own_pts, [&](int64_t a, int64_t b) {
-    for (int64_t lj = a; lj < b; ++lj) {
-      const int64_t g = S.pt_g[(size_t)lj];
-      if (points_out)
-        for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
-      if (owned_mask_out) owned_mask_out[S.M + g] = 1;
-    }
-  });
+  scatter_points(S, hp, direct, points_out, owned_mask_out);
   return DABA_OK;
 }
 
@@ -979,7 +1004,8 @@ extern "C" int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points
   if (!ctx) return DABA_E_INVALID_ARG;
   cudaSetDevice(ctx->device);
   hvec<double> hc, hp;
-  int rc = get_native(ctx, 0, hc, hp);
+  bool direct = false;
+  int rc = get_native(ctx, 0, hc, hp, points_out, &direct);
   if (rc) return rc;
   const ShardPlan& S = ctx->plan;
   if (owned_mask_out) std::memset(owned_mask_out, 0, (size_t)(S.M + S.N));
@@ -988,14 +1014,7 @@ extern "C" int daba_get_state(daba_ctx* ctx, double* cameras_out, double* points
     if (cameras_out) native_to_bal(&hc[(size_t)li * kCamStride], cameras_out + 9 * g);
     if (owned_mask_out) owned_mask_out[g] = 1;
   }
-  parallel_for(S.n_own_pts, [&](int64_t a, int64_t b) {
-    for (int64_t lj = a; lj < b; ++lj) {
-      const int64_t g = S.pt_g[(size_t)lj];
-      if (points_out)
-        for (int k = 0; k < 3; ++k) points_out[3 * g + k] = hp[(size_t)lj * 4 + k];
-      if (owned_mask_out) owned_mask_out[S.M + g] = 1;
-    }
-  });
+  scatter_points(S, hp, direct, points_out, owned_mask_out);
   return DABA_OK;
 }
 

@@ -1286,6 +1286,22 @@ int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* ca
   return 1;
 }
 
+// ------------------------------------------------------------------ state readback
+// owned points (double4, w unused) -> packed xyz, so that one D2H lands in the caller's N x 3 array
+__global__ void k_pts_xyz(const double4* __restrict__ src, double* __restrict__ dst, int32_t n) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double4 v = src[j];
+  dst[3 * (int64_t)j] = v.x;
+  dst[3 * (int64_t)j + 1] = v.y;
+  dst[3 * (int64_t)j + 2] = v.z;
+}
+int launch_pts_xyz(const double4* src, double* dst, int32_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_pts_xyz<<<blocks(n, 256), 256, 0, st>>>(src, dst, n);
+  return 1;
+}
+
 // ------------------------------------------------------------------ create-time point side on the device
 // (one rank, input sorted by (camera, point): the observation index is the camera-side record index)
 __global__ void k_iota(int32_t* v, int64_t n) {
@@ -1319,48 +1335,47 @@ __global__ void k_ptr_from_sorted(const int32_t* keys, int64_t K, int32_t N, int
 
 static inline unsigned grid(int64_t n) { return (unsigned)((n + 255) / 256); }
 
+// Carve aligned pieces out of a scratch region.
+static void* carve(char*& p, size_t bytes) {
+  void* r = p;
+  p += (bytes + 255) & ~size_t(255);
+  return r;
+}
+
 int64_t count_point_jumps_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int32_t N, int32_t far,
-                                 cudaStream_t st) {
-  int32_t* key = nullptr;
-  unsigned long long* cnt = nullptr;
-  if (cudaMalloc(&key, sizeof(int32_t) * (size_t)(N > 0 ? N : 1)) != cudaSuccess ||
-      cudaMalloc(&cnt, sizeof(unsigned long long)) != cudaSuccess)
-    return -1;
+                                 void* scratch, cudaStream_t st) {
+  char* sp = static_cast<char*>(scratch);
+  int32_t* key = static_cast<int32_t*>(carve(sp, sizeof(int32_t) * (size_t)(N > 0 ? N : 1)));
+  unsigned long long* cnt = static_cast<unsigned long long*>(carve(sp, sizeof(unsigned long long)));
   cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st);
   if (N > 0) k_fill_i32<<<grid(N), 256, 0, st>>>(key, N, 0x7fffffff);
   if (K > 0) k_min_camera<<<grid(K), 256, 0, st>>>(d_cam, d_pt, K, key);
   if (N > 1) k_count_jumps<<<grid(N), 256, 0, st>>>(key, N, far, cnt);
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, st);
-  const cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(key);
-  cudaFree(cnt);
-  return e == cudaSuccess ? (int64_t)h : -1;
+  return cudaStreamSynchronize(st) == cudaSuccess ? (int64_t)h : -1;
 }
 
-int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, cudaStream_t st) {
+int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st) {
   if (K == 0) {
     cudaMemsetAsync(d_ptr, 0, sizeof(int64_t) * ((size_t)N + 1), st);
     return cudaStreamSynchronize(st) == cudaSuccess ? 0 : -1;
   }
-  int32_t *vals = nullptr, *keys_out = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0;
   int bits = 1;
   while ((int64_t(1) << bits) < (int64_t)N) ++bits;
+  size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_pt, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                   (int)K, 0, bits, st);
-  if (cudaMalloc(&vals, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
-      cudaMalloc(&keys_out, sizeof(int32_t) * (size_t)K) != cudaSuccess || cudaMalloc(&tmp, tmp_bytes) != cudaSuccess)
-    return -1;
+  char* sp = static_cast<char*>(scratch);
+  int32_t* vals = static_cast<int32_t*>(carve(sp, sizeof(int32_t) * (size_t)K));
+  int32_t* keys_out = static_cast<int32_t*>(carve(sp, sizeof(int32_t) * (size_t)K));
+  void* tmp = carve(sp, tmp_bytes);
+  if ((size_t)(sp - static_cast<char*>(scratch)) > scratch_bytes) return -1;
   k_iota<<<grid(K), 256, 0, st>>>(vals, K);
   cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, d_pt, keys_out, vals, d_src, (int)K, 0, bits, st);  // stable
   k_ptr_from_sorted<<<grid(K), 256, 0, st>>>(keys_out, K, N, d_ptr);
-  const cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(vals);
-  cudaFree(keys_out);
-  cudaFree(tmp);
-  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return cudaStreamSynchronize(st) == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace daba

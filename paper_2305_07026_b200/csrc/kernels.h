@@ -133,12 +133,18 @@ int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* ca
                   const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, int select_inside,
                   cudaStream_t st);
 
+// state readback: owned points as packed xyz (n x 3) in `dst` (device)
+int launch_pts_xyz(const double4* src, double* dst, int32_t n, cudaStream_t st);
+
 // Create time, one rank with input sorted by (camera, point), from device copies of the observations' cameras
 // and points: how many consecutive points have smallest observing cameras more than `far` ids apart (-1 on a
 // CUDA error; shard.h order_owned_points), and the record list of every point in camera order (d_src, K: the
 // observation index is the record index) with its offsets (d_ptr, N + 1; 0 or -1).
+// (scratch: device memory for the temporaries — the record staging buffer, 64 B per observation, before its
+// first use)
 int64_t count_point_jumps_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int32_t N, int32_t far,
-                                 cudaStream_t st);
-int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, cudaStream_t st);
+                                 void* scratch, cudaStream_t st);
+int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st);
 
 }  // namespace daba

@@ -140,6 +140,29 @@ def test_resume_from_set_state():
         np.testing.assert_array_equal(ta[:, :5], tb[:, :5])
 
 
+def test_state_readback_paths(monkeypatch):
+    # the light plan packs points on the device into the record staging buffer and copies them straight into the
+    # caller's array; reading the state mid-run must not perturb the iteration, and both readback paths agree
+    p = gen.generate("small_seq_huber")
+    with solver(p) as a, solver(p) as b:
+        a.iterate(3)
+        mid = a.state()
+        ta = a.iterate_trace(4)
+        b.iterate(3)
+        tb = b.iterate_trace(4)
+        np.testing.assert_array_equal(ta, tb)
+        fa, fb = a.state(), b.state()
+    monkeypatch.setenv("DABA_DEVICE_PLAN", "0")
+    with solver(p) as c:
+        c.iterate(3)
+        midc = c.state()
+        cn, ln, mask = c.state_native(0)
+    for x, y in zip(mid[:2], midc[:2]):
+        np.testing.assert_allclose(x, y, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(fa[1], fb[1])
+    assert mask.all() and mid[2].all()
+
+
 # ---------------------------------------------------------------- edge cases
 def test_isolated_cameras_and_points():
     # a camera and points without observations: the anchor-extrapolated / MM candidates of an empty subproblem
