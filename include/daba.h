@@ -35,7 +35,8 @@
 extern "C" {
 #endif
 
-#define DABA_ABI_VERSION 2  /* 2: restart_scope option, DABA_TR_FDEV trace column, DABA_COMM_NONE */
+#define DABA_ABI_VERSION 3  /* 2: restart_scope option, DABA_TR_FDEV trace column, DABA_COMM_NONE;
+                               3: BAL ingestion / conversion, daba_pixel_error */
 
 enum {
   DABA_OK = 0,
@@ -181,6 +182,41 @@ int daba_plan_array(const daba_plan* p, int which, int32_t* out);
  * GLOBAL ids in exchange order.  Returns the length (call with out = NULL to size). */
 int64_t daba_plan_peer_list(const daba_plan* p, int peer, int kind, int32_t* out);
 void daba_plan_destroy(daba_plan* p);
+
+/* Mean reprojection error in PIXELS of x^k under the BAL forward model — the accuracy metric of Table 2
+ * (SURVEY NEXT-4).  For every observation of this rank's owned cameras: P' = R^T (l - t),
+ * q = P'_xy / P'_z, predicted pixel f (1 + k1 |q|^2 + k2 |q|^4) q with BAL's k1 = f d2, k2 = f^3 d3 + 2 k1^2
+ * (the inverse of daba_bal_to_paper's intrinsics map), residual r against the stored observation.
+ * out[0] = sum |r|, out[1] = sum |r|^2, out[2] = observations with P'_z <= 0 (behind the camera; included in the
+ * sums), out[3] = observations.  Mean = out[0] / out[3], RMS = sqrt(out[1] / out[3]).  Rank-local sums (the
+ * caller adds them over ranks).  Runs on the device (two kernels on the context's stream), blocking. */
+int daba_pixel_error(daba_ctx* ctx, double out[4]);
+
+/* ---- BAL datasets (host only, no CUDA calls) ----
+ * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
+ * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's
+ * FORWARD radial distortion u = f (1 + k1 |p|^2 + k2 |p|^4) p, p = -P_xy / P_z, P = R_w2c X + t_w2c); N points
+ * of 3 numbers; whitespace separated.
+ *
+ * daba_bal_read: with every array NULL, reads only the header into counts[3] = (M, N, K); otherwise parses the
+ * whole file (multithreaded) into caller-allocated cameras (M x 9), points (N x 3), obs_cam, obs_pt (K), obs_uv
+ * (K x 2), exactly as written (BAL convention).  Errors: DABA_E_INVALID_ARG — unreadable file, malformed number,
+ * index out of range, too few numbers, trailing content; daba_bal_last_error() names the line (thread-local). */
+int daba_bal_read(const char* path, int64_t counts[3], double* cameras, double* points, int32_t* obs_cam,
+                  int32_t* obs_pt, double* obs_uv);
+/* Write a BAL file (%.17g: reading it back is exact).  DABA_E_INVALID_ARG on bad arguments or an I/O error. */
+int daba_bal_write(const char* path, const double* cameras, int64_t M, const double* points, int64_t N,
+                   const int32_t* obs_cam, const int32_t* obs_pt, const double* obs_uv, int64_t K);
+const char* daba_bal_last_error(void);
+/* In place: BAL cameras (M x 9) and observations (K x 2) -> the ABI's camera layout in the paper's convention
+ * (eq. reprojection1), ready for daba_create.  The paper's ray (u, f g(|u|)) must be a positive
+ * multiple of R^T (l - t) while BAL's camera looks down -z: v is negated and the camera frame turned by
+ * S = diag(1, -1, -1) (R^T = S R_w2c, same centre); the forward distortion is inverted by series reversion,
+ * k1' = k1 / f^2, k2' = (k2 - 2 k1^2) / f^4 (exact through O(|u|^4); reading Q15).
+ * DABA_E_INVALID_ARG on f = 0 or bad sizes. */
+int daba_bal_to_paper(double* cameras, int64_t M, double* obs_uv, int64_t K);
+/* The inverse map (round trip exact up to rounding). */
+int daba_paper_to_bal(double* cameras, int64_t M, double* obs_uv, int64_t K);
 
 const char* daba_last_error(const daba_ctx* ctx);
 void daba_destroy(daba_ctx* ctx);

@@ -40,6 +40,7 @@ struct daba_ctx {
   size_t dev_bytes = 0;
   IterParams P{};
   int64_t host_k = 0;
+  double* d_metric = nullptr;  // 4 doubles, daba_pixel_error (allocated on first use)
   // halo exchange
   std::vector<PeerSeg> segs;
   int32_t *d_send_cam = nullptr, *d_send_pt = nullptr, *d_recv_cam = nullptr, *d_recv_pt = nullptr;
@@ -169,62 +170,6 @@ int upload(daba_ctx* c, T** p, const std::vector<T, A>& h) {
   if (rc) return rc;
   CUDA_OR(c, h2d(c, *p, h.data(), h.size() * sizeof(T)));
   return DABA_OK;
-}
-
-// BAL (angle-axis R_w2c, t_w2c, f, k1, k2) -> native (R camera->world, centre t, d = (f, f k1, f k2)).
-void bal_to_native(const double* b, double* c) {
-  const double wx = b[0], wy = b[1], wz = b[2];
-  const double th2 = wx * wx + wy * wy + wz * wz;
-  double A, B;
-  if (th2 < 1e-16) {
-    A = 1.0 - th2 / 6.0;
-    B = 0.5 - th2 / 24.0;
-  } else {
-    const double th = std::sqrt(th2);
-    A = std::sin(th) / th;
-    const double h = std::sin(0.5 * th);
-    B = 2.0 * h * h / th2;
-  }
-  // Q = R_w2c = I + A [w]x + B [w]x^2
-  const double Q[9] = {1.0 + B * (wx * wx - th2), -A * wz + B * wx * wy,     A * wy + B * wx * wz,
-                       A * wz + B * wx * wy,      1.0 + B * (wy * wy - th2), -A * wx + B * wy * wz,
-                       -A * wy + B * wx * wz,     A * wx + B * wy * wz,      1.0 + B * (wz * wz - th2)};
-  for (int r = 0; r < 3; ++r)
-    for (int k = 0; k < 3; ++k) c[3 * r + k] = Q[3 * k + r];  // R = Q^T
-  for (int r = 0; r < 3; ++r) c[9 + r] = -(c[3 * r] * b[3] + c[3 * r + 1] * b[4] + c[3 * r + 2] * b[5]);  // t = -R t_w2c
-  c[12] = b[6];
-  c[13] = b[6] * b[7];
-  c[14] = b[6] * b[8];
-  c[15] = 0.0;
-}
-
-// native -> BAL via the quaternion of R_w2c = R^T (robust for every angle)
-void native_to_bal(const double* c, double* b) {
-  const double Q[9] = {c[0], c[3], c[6], c[1], c[4], c[7], c[2], c[5], c[8]};
-  double w, x, y, z;
-  const double tr = Q[0] + Q[4] + Q[8];
-  if (tr > Q[0] && tr > Q[4] && tr > Q[8]) {
-    const double s = 2.0 * std::sqrt(1.0 + tr);
-    w = 0.25 * s; x = (Q[7] - Q[5]) / s; y = (Q[2] - Q[6]) / s; z = (Q[3] - Q[1]) / s;
-  } else if (Q[0] > Q[4] && Q[0] > Q[8]) {
-    const double s = 2.0 * std::sqrt(1.0 + Q[0] - Q[4] - Q[8]);
-    w = (Q[7] - Q[5]) / s; x = 0.25 * s; y = (Q[1] + Q[3]) / s; z = (Q[2] + Q[6]) / s;
-  } else if (Q[4] > Q[8]) {
-    const double s = 2.0 * std::sqrt(1.0 + Q[4] - Q[0] - Q[8]);
-    w = (Q[2] - Q[6]) / s; x = (Q[1] + Q[3]) / s; y = 0.25 * s; z = (Q[5] + Q[7]) / s;
-  } else {
-    const double s = 2.0 * std::sqrt(1.0 + Q[8] - Q[0] - Q[4]);
-    w = (Q[3] - Q[1]) / s; x = (Q[2] + Q[6]) / s; y = (Q[5] + Q[7]) / s; z = 0.25 * s;
-  }
-  if (w < 0) { w = -w; x = -x; y = -y; z = -z; }
-  const double vn = std::sqrt(x * x + y * y + z * z);
-  const double ang = 2.0 * std::atan2(vn, w);
-  const double f = vn > 0 ? ang / vn : 0.0;
-  b[0] = x * f; b[1] = y * f; b[2] = z * f;
-  for (int k = 0; k < 3; ++k) b[3 + k] = -(Q[3 * k] * c[9] + Q[3 * k + 1] * c[10] + Q[3 * k + 2] * c[11]);
-  b[6] = c[12];
-  b[7] = c[13] / c[12];
-  b[8] = c[14] / c[12];
 }
 
 int name_index(daba_ctx* c, const char* name) {
@@ -397,6 +342,64 @@ int upload_states(daba_ctx* c, const double* cams_k, const double* pts_k, const 
 }
 
 }  // namespace
+
+namespace daba {
+// BAL (angle-axis R_w2c, t_w2c, f, k1, k2) -> native (R camera->world, centre t, d = (f, f k1, f k2)).
+void bal_to_native(const double* b, double* c) {
+  const double wx = b[0], wy = b[1], wz = b[2];
+  const double th2 = wx * wx + wy * wy + wz * wz;
+  double A, B;
+  if (th2 < 1e-16) {
+    A = 1.0 - th2 / 6.0;
+    B = 0.5 - th2 / 24.0;
+  } else {
+    const double th = std::sqrt(th2);
+    A = std::sin(th) / th;
+    const double h = std::sin(0.5 * th);
+    B = 2.0 * h * h / th2;
+  }
+  // Q = R_w2c = I + A [w]x + B [w]x^2
+  const double Q[9] = {1.0 + B * (wx * wx - th2), -A * wz + B * wx * wy,     A * wy + B * wx * wz,
+                       A * wz + B * wx * wy,      1.0 + B * (wy * wy - th2), -A * wx + B * wy * wz,
+                       -A * wy + B * wx * wz,     A * wx + B * wy * wz,      1.0 + B * (wz * wz - th2)};
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) c[3 * r + k] = Q[3 * k + r];  // R = Q^T
+  for (int r = 0; r < 3; ++r) c[9 + r] = -(c[3 * r] * b[3] + c[3 * r + 1] * b[4] + c[3 * r + 2] * b[5]);  // t = -R t_w2c
+  c[12] = b[6];
+  c[13] = b[6] * b[7];
+  c[14] = b[6] * b[8];
+  c[15] = 0.0;
+}
+
+// native -> BAL via the quaternion of R_w2c = R^T (robust for every angle)
+void native_to_bal(const double* c, double* b) {
+  const double Q[9] = {c[0], c[3], c[6], c[1], c[4], c[7], c[2], c[5], c[8]};
+  double w, x, y, z;
+  const double tr = Q[0] + Q[4] + Q[8];
+  if (tr > Q[0] && tr > Q[4] && tr > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + tr);
+    w = 0.25 * s; x = (Q[7] - Q[5]) / s; y = (Q[2] - Q[6]) / s; z = (Q[3] - Q[1]) / s;
+  } else if (Q[0] > Q[4] && Q[0] > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + Q[0] - Q[4] - Q[8]);
+    w = (Q[7] - Q[5]) / s; x = 0.25 * s; y = (Q[1] + Q[3]) / s; z = (Q[2] + Q[6]) / s;
+  } else if (Q[4] > Q[8]) {
+    const double s = 2.0 * std::sqrt(1.0 + Q[4] - Q[0] - Q[8]);
+    w = (Q[2] - Q[6]) / s; x = (Q[1] + Q[3]) / s; y = 0.25 * s; z = (Q[5] + Q[7]) / s;
+  } else {
+    const double s = 2.0 * std::sqrt(1.0 + Q[8] - Q[0] - Q[4]);
+    w = (Q[3] - Q[1]) / s; x = (Q[2] + Q[6]) / s; y = (Q[5] + Q[7]) / s; z = 0.25 * s;
+  }
+  if (w < 0) { w = -w; x = -x; y = -y; z = -z; }
+  const double vn = std::sqrt(x * x + y * y + z * z);
+  const double ang = 2.0 * std::atan2(vn, w);
+  const double f = vn > 0 ? ang / vn : 0.0;
+  b[0] = x * f; b[1] = y * f; b[2] = z * f;
+  for (int k = 0; k < 3; ++k) b[3 + k] = -(Q[3 * k] * c[9] + Q[3 * k + 1] * c[10] + Q[3 * k + 2] * c[11]);
+  b[6] = c[12];
+  b[7] = c[13] / c[12];
+  b[8] = c[14] / c[12];
+}
+}  // namespace daba
 
 // ====================================================================== C-ABI
 extern "C" void daba_default_options(daba_options* o) {
@@ -930,6 +933,18 @@ extern "C" int daba_objective(daba_ctx* ctx, double* F_out) {
   if (!ctx || !F_out) return DABA_E_INVALID_ARG;
   cudaSetDevice(ctx->device);
   return compute_objective(ctx, F_out, nullptr);
+}
+
+extern "C" int daba_pixel_error(daba_ctx* ctx, double out[4]) {
+  if (!ctx || !out) return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc;
+  if (!ctx->d_metric && (rc = dalloc(ctx, &ctx->d_metric, 4))) return rc;
+  launch_pixel_error(ctx->P, 1, ctx->d_metric, ctx->stream);
+  CUDA_OR(ctx, cudaGetLastError());
+  CUDA_OR(ctx, cudaMemcpyAsync(out, ctx->d_metric, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  return DABA_OK;
 }
 
 // Reads the owned cameras (native records) into hc and, unless the points go straight to the caller, the owned

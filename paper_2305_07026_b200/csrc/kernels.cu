@@ -382,6 +382,70 @@ __global__ void k_reduce_objective(IterParams p) {
   }
 }
 
+// ------------------------------------------------------------------ pixel metric
+// Mean reprojection error in pixels under the BAL forward model (the metric of Table 2), evaluated in
+// the paper's frame: P' = R^T (l - t) (= S P_BAL with S = diag(1,-1,-1), see daba_bal_to_paper), q = P'_xy / P'_z,
+// predicted u = f (1 + k1 |q|^2 + k2 |q|^4) q with BAL's k1 = f d2, k2 = f^3 d3 + 2 k1^2 (the inverse of the
+// series reversion of the intrinsics), residual against the stored (v-flipped) observation.  Per chunk:
+// [sum |r|, sum |r|^2, #(P'_z <= 0), #observations].
+__global__ void __launch_bounds__(kCamPassThreads) k_pixel_error(IterParams p, int role) {
+  const CamChunk ch = p.chunks[blockIdx.x];
+  const int r = p.roles[role];
+  const double* cam = p.cams[r] + (size_t)ch.cam * kCamStride;
+  const double4* __restrict__ L = p.pts[r];
+  const double f = cam[12], k1 = f * cam[13], k2 = fma(f * f * f, cam[14], 2.0 * k1 * k1);
+  double se = 0, se2 = 0, nb = 0;
+  for (int64_t o = ch.o0 + threadIdx.x; o < ch.o0 + ch.n; o += kCamPassThreads) {
+    const int32_t j = p.c_pt[o];
+    const double2 u = p.c_uv[o];
+    const double4 l = L[j];
+    const double vx = l.x - cam[9], vy = l.y - cam[10], vz = l.z - cam[11];
+    const double cx = fma(cam[0], vx, fma(cam[3], vy, cam[6] * vz));
+    const double cy = fma(cam[1], vx, fma(cam[4], vy, cam[7] * vz));
+    const double cz = fma(cam[2], vx, fma(cam[5], vy, cam[8] * vz));
+    nb += cz <= 0.0 ? 1.0 : 0.0;
+    const double qx = cx / cz, qy = cy / cz;
+    const double q2 = fma(qx, qx, qy * qy);
+    const double g = f * fma(q2, fma(q2, k2, k1), 1.0);
+    const double rx = fma(-g, qx, u.x), ry = fma(-g, qy, u.y);
+    const double r2 = fma(rx, rx, ry * ry);
+    se += sqrt(r2);
+    se2 += r2;
+  }
+  __shared__ double sh[3][kCamPassThreads];
+  sh[0][threadIdx.x] = se;
+  sh[1][threadIdx.x] = se2;
+  sh[2][threadIdx.x] = nb;
+  __syncthreads();
+  for (int st = kCamPassThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int k = 0; k < 3; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* q = p.partial + (size_t)blockIdx.x * 2 * kPartialStride;
+    q[0] = sh[0][0];
+    q[1] = sh[1][0];
+    q[2] = sh[2][0];
+    q[3] = (double)ch.n;
+  }
+}
+
+__global__ void k_reduce_pixel_error(IterParams p, double* out) {
+  __shared__ double sh[4][256];
+  double a[4] = {0, 0, 0, 0};
+  for (int c = threadIdx.x; c < p.n_chunks; c += 256)
+    for (int k = 0; k < 4; ++k) a[k] += p.partial[(size_t)c * 2 * kPartialStride + k];
+  for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] = a[k];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) out[threadIdx.x] = sh[threadIdx.x][0];
+}
+
 // ------------------------------------------------------------------ a4 + a5 + a7: point pass
 template <int LOSS>
 __device__ __forceinline__ void pt_terms(const double* cam, double lx, double ly, double lz, double2 u,
@@ -1245,6 +1309,16 @@ int launch_objective(const IterParams& p, cudaStream_t st) {
     ++n;
   }
   k_reduce_objective<<<1, 256, 0, st>>>(p);
+  return n + 1;
+}
+
+int launch_pixel_error(const IterParams& p, int role, double* out, cudaStream_t st) {
+  int n = 0;
+  if (p.n_chunks > 0) {
+    k_pixel_error<<<p.n_chunks, kCamPassThreads, 0, st>>>(p, role);
+    ++n;
+  }
+  k_reduce_pixel_error<<<1, 256, 0, st>>>(p, out);
   return n + 1;
 }
 

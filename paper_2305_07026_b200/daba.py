@@ -42,7 +42,9 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_objective", "daba_get_state", "daba_get_state_native", "daba_set_state_native",
            "daba_get_schedule", "daba_last_decisions", "daba_shard_info", "daba_stream", "daba_kernel_times",
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
-           "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy"]
+           "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
+           "daba_pixel_error", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
+           "daba_paper_to_bal"]
 
 
 def lib():
@@ -85,6 +87,13 @@ def lib():
         L.daba_plan_peer_list.restype = I64
         L.daba_plan_destroy.argtypes = [V]
         L.daba_plan_destroy.restype = None
+        L.daba_pixel_error.argtypes = [V, V]
+        L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
+        L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
+        L.daba_bal_last_error.argtypes = []
+        L.daba_bal_last_error.restype = ctypes.c_char_p
+        L.daba_bal_to_paper.argtypes = [V, I64, V, I64]
+        L.daba_paper_to_bal.argtypes = [V, I64, V, I64]
         _lib = L
     return _lib
 
@@ -109,6 +118,68 @@ def comm_id() -> bytes:
 
 def _c(x, dtype):
     return np.ascontiguousarray(x, dtype=dtype)
+
+
+class BalProblem:
+    """A BAL dataset as arrays: cameras M x 9, points N x 3, obs_cam / obs_pt (K), obs_uv K x 2."""
+
+    def __init__(self, cams, pts, obs_cam, obs_pt, obs_uv):
+        self.cams, self.pts, self.obs_cam, self.obs_pt, self.obs_uv = cams, pts, obs_cam, obs_pt, obs_uv
+
+    @property
+    def M(self):
+        return self.cams.shape[0]
+
+    @property
+    def N(self):
+        return self.pts.shape[0]
+
+    @property
+    def K(self):
+        return self.obs_cam.shape[0]
+
+
+def read_bal(path) -> BalProblem:
+    """Parse a BAL text file (daba_bal_read; native, multithreaded).  Values as written (BAL convention)."""
+    L, bp = lib(), os.fsencode(path)
+    counts = np.zeros(3, np.int64)
+    if L.daba_bal_read(bp, counts.ctypes.data, None, None, None, None, None):
+        raise DabaError(-1, L.daba_bal_last_error().decode())
+    M, N, K = (int(x) for x in counts)
+    cams, pts = np.empty((M, 9)), np.empty((N, 3))
+    oc, op, uv = np.empty(K, np.int32), np.empty(K, np.int32), np.empty((K, 2))
+    if L.daba_bal_read(bp, counts.ctypes.data, cams.ctypes.data, pts.ctypes.data, oc.ctypes.data, op.ctypes.data,
+                       uv.ctypes.data):
+        raise DabaError(-1, L.daba_bal_last_error().decode())
+    return BalProblem(cams, pts, oc, op, uv)
+
+
+def write_bal(path, prob: BalProblem) -> None:
+    a = [_c(prob.cams, np.float64), _c(prob.pts, np.float64), _c(prob.obs_cam, np.int32),
+         _c(prob.obs_pt, np.int32), _c(prob.obs_uv, np.float64)]
+    L = lib()
+    if L.daba_bal_write(os.fsencode(path), a[0].ctypes.data, a[0].shape[0], a[1].ctypes.data, a[1].shape[0],
+                        a[2].ctypes.data, a[3].ctypes.data, a[4].ctypes.data, a[2].shape[0]):
+        raise DabaError(-1, L.daba_bal_last_error().decode())
+
+
+def _convert(fn, cams, obs_uv):
+    c = np.array(cams, dtype=np.float64, order="C").reshape(-1, 9)
+    u = np.array(obs_uv, dtype=np.float64, order="C").reshape(-1, 2)
+    rc = fn(c.ctypes.data, c.shape[0], u.ctypes.data, u.shape[0])
+    if rc:
+        raise DabaError(rc, "camera with f = 0")
+    return c, u
+
+
+def bal_to_paper(cams, obs_uv):
+    """BAL cameras / observations -> the ABI camera layout in the paper's convention (copies; daba_bal_to_paper)."""
+    return _convert(lib().daba_bal_to_paper, cams, obs_uv)
+
+
+def paper_to_bal(cams, obs_uv):
+    """Inverse of bal_to_paper (copies; daba_paper_to_bal)."""
+    return _convert(lib().daba_paper_to_bal, cams, obs_uv)
 
 
 class Plan:
@@ -198,6 +269,15 @@ class Solver:
         F = ctypes.c_double()
         self._check(lib().daba_objective(self.h, ctypes.byref(F)), "daba_objective")
         return F.value
+
+    def pixel_error(self) -> dict:
+        """BAL-convention pixel reprojection error of x^k over this rank's owned cameras' observations
+        (daba_pixel_error): mean, rms, number behind the camera, observations, and the raw sums."""
+        out = np.zeros(4)
+        self._check(lib().daba_pixel_error(self.h, out.ctypes.data), "daba_pixel_error")
+        n = max(out[3], 1.0)
+        return {"mean": out[0] / n, "rms": float(np.sqrt(out[1] / n)), "behind": int(out[2]), "count": int(out[3]),
+                "sum": float(out[0]), "sum_sq": float(out[1])}
 
     def _out(self, shape):
         # entries this rank does not own stay NaN; one rank owns everything (no fill needed)
