@@ -82,3 +82,23 @@ def test_bal_file_end_to_end(tmp_path):
                                                axis=1)))
     assert g1["mean"] < 0.5 * g0["mean"]
     assert g1["mean"] < 1.2 * noise_floor
+
+
+def test_pixel_error_edge_cases():
+    p = gen.generate("tiny_seq")
+    # no observations: zero sums (the reduction runs over zero chunks)
+    with D.Solver(p.cams, p.pts, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2))) as s:
+        g = s.pixel_error()
+        assert (g["count"], g["sum"], g["sum_sq"], g["behind"]) == (0, 0.0, 0.0, 0)
+    # points mirrored through one of their cameras' centres land behind it: counted, still summed like the oracle
+    pts = p.pts.copy()
+    cam0 = p.obs_cam[0]
+    from oracle import bal_to_native
+    centre = bal_to_native(p.cams[cam0:cam0 + 1])[0, 9:12]
+    flip = np.unique(p.obs_pt[p.obs_cam == cam0])[:5]
+    pts[flip] = 2 * centre - pts[flip]
+    with solver(p.cams, pts, p.obs_cam, p.obs_pt, p.obs_uv) as s:
+        g = s.pixel_error()
+    o = oracle_metric(p.cams, pts, p.obs_cam, p.obs_pt, p.obs_uv)
+    assert g["behind"] == o[2] >= 5
+    assert g["sum"] == pytest.approx(o[0], rel=1e-11)
