@@ -134,7 +134,7 @@ extern "C" int daba_bal_read(const char* path, int64_t counts[3], double* camera
   int64_t h[3];
   const size_t p0 = parse_header(b, n, h);
   if (!p0) return fail("line 1: header \"num_cameras num_points num_observations\" expected");
-  if (h[0] < 0 || h[1] < 0 || h[2] < 0 || h[0] > INT32_MAX || h[1] > INT32_MAX)
+  if (h[0] < 0 || h[1] < 0 || h[2] < 0 || h[0] > INT32_MAX || h[1] > INT32_MAX || h[2] > (INT64_C(1) << 40))
     return fail("line 1: counts out of range");
   counts[0] = h[0];
   counts[1] = h[1];

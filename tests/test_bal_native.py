@@ -99,3 +99,19 @@ def test_conversion_matches_oracle():
     np.testing.assert_allclose(bn[:, 3:], cams[:, 3:], rtol=1e-12, atol=1e-14)
     with pytest.raises(D.DabaError):
         D.bal_to_paper(np.zeros((1, 9)), uv)
+
+
+def test_header_only_and_huge_counts(tmp_path):
+    path = tmp_path / "h.txt"
+    path.write_text("3 4 5\n")
+    counts = np.zeros(3, np.int64)
+    assert D.lib().daba_bal_read(str(path).encode(), counts.ctypes.data, None, None, None, None, None) == 0
+    assert counts.tolist() == [3, 4, 5]
+    with pytest.raises(D.DabaError, match="end of file"):
+        D.read_bal(str(path))
+    path.write_text("1 1 99999999999999999\n")
+    with pytest.raises(D.DabaError, match="out of range"):
+        D.read_bal(str(path))
+    path.write_text("")
+    with pytest.raises(D.DabaError, match="header"):
+        D.read_bal(str(path))
