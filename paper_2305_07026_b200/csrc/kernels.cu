@@ -1370,6 +1370,16 @@ __global__ void k_pts_xyz(const double4* __restrict__ src, double* __restrict__ 
   dst[3 * (int64_t)j + 1] = v.y;
   dst[3 * (int64_t)j + 2] = v.z;
 }
+__global__ void k_xyz_pts(const double* __restrict__ src, double4* __restrict__ dst, int32_t n) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  dst[j] = make_double4(src[3 * (int64_t)j], src[3 * (int64_t)j + 1], src[3 * (int64_t)j + 2], 0.0);
+}
+int launch_xyz_pts(const double* src, double4* dst, int32_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_xyz_pts<<<blocks(n, 256), 256, 0, st>>>(src, dst, n);
+  return 1;
+}
 int launch_pts_xyz(const double4* src, double* dst, int32_t n, cudaStream_t st) {
   if (n <= 0) return 0;
   k_pts_xyz<<<blocks(n, 256), 256, 0, st>>>(src, dst, n);

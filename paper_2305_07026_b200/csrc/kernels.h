@@ -138,6 +138,8 @@ int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* ca
 
 // state readback: owned points as packed xyz (n x 3) in `dst` (device)
 int launch_pts_xyz(const double4* src, double* dst, int32_t n, cudaStream_t st);
+// and back: packed xyz (device) -> 32 B point records
+int launch_xyz_pts(const double* src, double4* dst, int32_t n, cudaStream_t st);
 
 // Create time, one rank with input sorted by (camera, point), from device copies of the observations' cameras
 // and points: how many consecutive points have smallest observing cameras more than `far` ids apart (-1 on a
