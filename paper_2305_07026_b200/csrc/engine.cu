@@ -97,7 +97,9 @@ struct PhaseTimer {
   void mark(const char* what) {
     if (!on) return;
     const auto n = std::chrono::steady_clock::now();
-    fprintf(stderr, "daba_create %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    const cudaError_t e = cudaPeekAtLastError();
+    fprintf(stderr, "daba_create %-28s %8.1f ms%s%s\n", what, std::chrono::duration<double, std::milli>(n - t).count(),
+            e ? "  pending CUDA error: " : "", e ? cudaGetErrorString(e) : "");
     t = n;
   }
 };
@@ -158,41 +160,90 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
 // Host -> device copy on the context's stream.  Small or page-locked sources go directly; large pageable ones
 // through a process-wide page-locked staging buffer (two 32 MB halves: the host threads fill one half while
 // the copy engine drains the other).  Returns once the source may be reused.
+// process-wide page-locked staging buffer of two 32 MB halves (allocated on first use; null if that failed)
+constexpr size_t kStageHalf = 32u << 20;
+std::mutex g_stage_mu;
+char* g_stage = nullptr;
+cudaEvent_t g_stage_ev[2] = {nullptr, nullptr};
+bool g_stage_tried = false;
+
+char* stage_buffer() {  // call with g_stage_mu held
+  if (!g_stage_tried) {
+    g_stage_tried = true;
+    if (cudaMallocHost(&g_stage, 2 * kStageHalf) != cudaSuccess) {
+      g_stage = nullptr;
+      cudaGetLastError();
+    } else {
+      cudaEventCreateWithFlags(&g_stage_ev[0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g_stage_ev[1], cudaEventDisableTiming);
+    }
+  }
+  return g_stage;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer may leave an error behind on some drivers
+  return pinned;
+}
+
 cudaError_t h2d(daba_ctx* c, void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return cudaSuccess;
-  cudaPointerAttributes at{};
-  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
-  cudaGetLastError();  // a pageable pointer may leave an error behind on some drivers
-  if (pinned || bytes < (8u << 20)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
-  static std::mutex mu;
-  static char* stage = nullptr;
-  static cudaEvent_t ev[2] = {nullptr, nullptr};
-  constexpr size_t kHalf = 32u << 20;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!stage) {
-    if (cudaMallocHost(&stage, 2 * kHalf) != cudaSuccess) {
-      stage = nullptr;
-      cudaGetLastError();
-      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
-    }
-    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-  }
+  if (bytes < (8u << 20) || is_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  char* stage = stage_buffer();
+  if (!stage) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
   bool used[2] = {false, false};
-  for (size_t off = 0, h = 0; off < bytes; off += kHalf, h ^= 1) {
-    const size_t n = std::min(kHalf, bytes - off);
-    if (used[h]) cudaEventSynchronize(ev[h]);
-    char* buf = stage + h * kHalf;
+  for (size_t off = 0, h = 0; off < bytes; off += kStageHalf, h ^= 1) {
+    const size_t n = std::min(kStageHalf, bytes - off);
+    if (used[h]) cudaEventSynchronize(g_stage_ev[h]);
+    char* buf = stage + h * kStageHalf;
     const char* s = static_cast<const char*>(src) + off;
     parallel_for((int64_t)n, [&](int64_t a, int64_t b) { std::memcpy(buf + a, s + a, (size_t)(b - a)); });
     cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, buf, n, cudaMemcpyHostToDevice, c->stream);
     if (e != cudaSuccess) return e;
-    cudaEventRecord(ev[h], c->stream);
+    cudaEventRecord(g_stage_ev[h], c->stream);
     used[h] = true;
   }
   for (int h = 0; h < 2; ++h)
-    if (used[h]) cudaEventSynchronize(ev[h]);  // the staging buffer is free for the next caller
+    if (used[h]) cudaEventSynchronize(g_stage_ev[h]);  // the staging buffer is free for the next caller
   return cudaSuccess;
+}
+
+// Device -> host, blocking: large pageable destinations through the staging halves (the copy engine fills one
+// half while host threads empty the other) instead of the driver's single-threaded pageable path.
+cudaError_t d2h(daba_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  if (bytes < (8u << 20) || is_pinned(dst)) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(c->stream);
+  }
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  char* stage = stage_buffer();
+  if (!stage) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(c->stream);
+  }
+  const size_t nchunk = (bytes + kStageHalf - 1) / kStageHalf;
+  auto issue = [&](size_t q) {
+    const size_t off = q * kStageHalf, n = std::min(kStageHalf, bytes - off);
+    cudaError_t e = cudaMemcpyAsync(stage + (q & 1) * kStageHalf, static_cast<const char*>(src) + off, n,
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(g_stage_ev[q & 1], c->stream);
+    return e;
+  };
+  cudaError_t e = issue(0);
+  for (size_t q = 0; q < nchunk && e == cudaSuccess; ++q) {
+    if (q + 1 < nchunk && (e = issue(q + 1)) != cudaSuccess) break;
+    if ((e = cudaEventSynchronize(g_stage_ev[q & 1])) != cudaSuccess) break;
+    const size_t off = q * kStageHalf, n = std::min(kStageHalf, bytes - off);
+    const char* buf = stage + (q & 1) * kStageHalf;
+    char* d = static_cast<char*>(dst) + off;
+    parallel_for((int64_t)n, [&](int64_t a, int64_t b) { std::memcpy(d + a, buf + a, (size_t)(b - a)); });
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e;
 }
 
 template <class T, class A>
@@ -564,8 +615,12 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
         h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess)
       return bail(DABA_E_CUDA);
-    const int64_t jumps = count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far,
-                                                   Q.staging + ((size_t)K + 7) / 2, C->stream);
+    // scratch after the K camera ids: N int32 keys + a counter; with more points than the buffer holds (isolated
+    // points) or no observations the check is skipped (nothing to gather, the numbering is kept)
+    const bool fits = K > 0 && sizeof(int32_t) * ((size_t)K + 8 + (size_t)N) + 64 <= 64 * (size_t)Q.n_records;
+    const int64_t jumps = fits ? count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far,
+                                                          Q.staging + ((size_t)K + 7) / 2, C->stream)
+                               : 0;
     if (jumps < 0) return bail(DABA_E_CUDA);
     if (point_order != 0 && jumps * 4 >= N && N > 1) {  // scattered numbering: full plan, renumbered
       std::string e2 = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, false);
@@ -1008,14 +1063,11 @@ static int get_native(daba_ctx* c, int which, hvec<double>& hc, hvec<double>& hp
     if (points_out && np > 0) {
       launch_pts_xyz(c->P.pts[r], c->P.staging, np, c->stream);
       CUDA_OR(c, cudaGetLastError());
-      CUDA_OR(c, cudaMemcpyAsync(points_out, c->P.staging, 3 * (size_t)np * sizeof(double), cudaMemcpyDeviceToHost,
-                                 c->stream));
+      CUDA_OR(c, d2h(c, points_out, c->P.staging, 3 * (size_t)np * sizeof(double)));
     }
   } else {
     hp.resize((size_t)np * 4);
-    if (!hp.empty())
-      CUDA_OR(c, cudaMemcpyAsync(hp.data(), c->P.pts[r], hp.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                                 c->stream));
+    if (!hp.empty()) CUDA_OR(c, d2h(c, hp.data(), c->P.pts[r], hp.size() * sizeof(double)));
   }
   CUDA_OR(c, cudaStreamSynchronize(c->stream));
   return DABA_OK;

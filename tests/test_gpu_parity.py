@@ -179,6 +179,22 @@ def test_isolated_cameras_and_points():
         assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= 1e-10
 
 
+def test_more_isolated_points_than_observations():
+    # N >> K: the create-time device scratch (carved from the 64 B/observation record buffer) cannot hold the
+    # per-point keys, so the locality check is skipped; the iterates still match the oracle
+    p = gen.generate("tiny_seq")
+    extra = np.random.default_rng(3).normal(size=(30 * p.K, 3)) * 5
+    q = gen.Problem("iso_many", p.cams, np.vstack([p.pts, extra]), p.obs_cam, p.obs_pt, p.obs_uv, p.gt_cams,
+                    np.vstack([p.gt_pts, extra]), p.loss)
+    o = oracle_for(q)
+    tro = o.iterate(5)
+    with solver(q) as s:
+        trg = s.iterate_trace(5)
+        assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
+        assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= 1e-10
+        assert s.pixel_error()["count"] == p.K
+
+
 def test_empty_observation_set():
     p = gen.generate("tiny_seq")
     with D.Solver(p.cams, p.pts, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2))) as s:
