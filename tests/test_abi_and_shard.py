@@ -156,3 +156,14 @@ def test_halo_exchange_over_gloo_world2():
     [pr.join(timeout=60) for pr in procs]
     assert all(ok for _, ok, _ in res), res
     assert all(c["halo_pts"] > 0 and c["halo_cams"] > 0 for _, _, c in res)
+
+
+def test_missing_extension_fails_loudly(tmp_path):
+    # no CPU fallback: without libdaba.so the binding raises on first use
+    import subprocess
+    import sys
+    env = dict(os.environ, DABA_LIB=str(tmp_path / "absent" / "libdaba.so"))
+    code = ("import paper_2305_07026_b200 as D\n"
+            "try:\n    D.lib()\nexcept ImportError as e:\n    print('raised', e)\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert "raised" in out.stdout and "missing" in out.stdout, out.stdout + out.stderr
