@@ -192,6 +192,11 @@ void daba_plan_destroy(daba_plan* p);
  * caller adds them over ranks).  Runs on the device (two kernels on the context's stream), blocking. */
 int daba_pixel_error(daba_ctx* ctx, double out[4]);
 
+/* The same metric per observation: resid_out[q] = |r| (pixels) for every observation q (index into the arrays
+ * given to daba_create) whose camera this rank owns; other entries are left untouched.  K doubles, host.
+ * Blocking; for statistics beyond the mean (median, percentiles).  DABA_E_STATE if the context has no scratch. */
+int daba_pixel_residuals(daba_ctx* ctx, double* resid_out);
+
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
  * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's

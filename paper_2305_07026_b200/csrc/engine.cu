@@ -1037,10 +1037,35 @@ extern "C" int daba_pixel_error(daba_ctx* ctx, double out[4]) {
   cudaSetDevice(ctx->device);
   int rc;
   if (!ctx->d_metric && (rc = dalloc(ctx, &ctx->d_metric, 4))) return rc;
-  launch_pixel_error(ctx->P, 1, ctx->d_metric, ctx->stream);
+  launch_pixel_error(ctx->P, 1, ctx->d_metric, nullptr, ctx->stream);
   CUDA_OR(ctx, cudaGetLastError());
   CUDA_OR(ctx, cudaMemcpyAsync(out, ctx->d_metric, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_OR(ctx, cudaStreamSynchronize(ctx->stream));
+  return DABA_OK;
+}
+
+extern "C" int daba_pixel_residuals(daba_ctx* ctx, double* resid_out) {
+  if (!ctx || !resid_out) return DABA_E_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  const ShardPlan& S = ctx->plan;
+  const bool identity = S.point_side_deferred || S.cam_side_identity;
+  const int64_t kc = ctx->P.n_cam_side;
+  if (kc == 0) return DABA_OK;
+  if (!ctx->P.staging || (size_t)kc > 8 * (size_t)ctx->P.n_records) return fail(ctx, DABA_E_STATE, "no scratch");
+  int rc;
+  if (!ctx->d_metric && (rc = dalloc(ctx, &ctx->d_metric, 4))) return rc;
+  // per-observation residuals in the record staging buffer (free between iterations)
+  launch_pixel_error(ctx->P, 1, ctx->d_metric, ctx->P.staging, ctx->stream);
+  CUDA_OR(ctx, cudaGetLastError());
+  if (identity) {
+    CUDA_OR(ctx, d2h(ctx, resid_out, ctx->P.staging, (size_t)kc * sizeof(double)));
+    return DABA_OK;
+  }
+  hvec<double> h((size_t)kc);
+  CUDA_OR(ctx, d2h(ctx, h.data(), ctx->P.staging, (size_t)kc * sizeof(double)));
+  parallel_for(kc, [&](int64_t a, int64_t b) {
+    for (int64_t q = a; q < b; ++q) resid_out[S.c_obs[(size_t)q]] = h[(size_t)q];
+  });
   return DABA_OK;
 }
 

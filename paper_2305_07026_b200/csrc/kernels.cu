@@ -388,7 +388,22 @@ __global__ void k_reduce_objective(IterParams p) {
 // predicted u = f (1 + k1 |q|^2 + k2 |q|^4) q with BAL's k1 = f d2, k2 = f^3 d3 + 2 k1^2 (the inverse of the
 // series reversion of the intrinsics), residual against the stored (v-flipped) observation.  Per chunk:
 // [sum |r|, sum |r|^2, #(P'_z <= 0), #observations].
-__global__ void __launch_bounds__(kCamPassThreads) k_pixel_error(IterParams p, int role) {
+// |r| of one observation (pixels) and whether the point is behind the camera (P'_z <= 0)
+__device__ __forceinline__ double pixel_residual(const double* cam, double f, double k1, double k2, double4 l,
+                                                 double2 u, bool* behind) {
+  const double vx = l.x - cam[9], vy = l.y - cam[10], vz = l.z - cam[11];
+  const double cx = fma(cam[0], vx, fma(cam[3], vy, cam[6] * vz));
+  const double cy = fma(cam[1], vx, fma(cam[4], vy, cam[7] * vz));
+  const double cz = fma(cam[2], vx, fma(cam[5], vy, cam[8] * vz));
+  *behind = cz <= 0.0;
+  const double qx = cx / cz, qy = cy / cz;
+  const double q2 = fma(qx, qx, qy * qy);
+  const double g = f * fma(q2, fma(q2, k2, k1), 1.0);
+  const double rx = fma(-g, qx, u.x), ry = fma(-g, qy, u.y);
+  return sqrt(fma(rx, rx, ry * ry));
+}
+
+__global__ void __launch_bounds__(kCamPassThreads) k_pixel_error(IterParams p, int role, double* resid) {
   const CamChunk ch = p.chunks[blockIdx.x];
   const int r = p.roles[role];
   const double* cam = p.cams[r] + (size_t)ch.cam * kCamStride;
@@ -396,21 +411,12 @@ __global__ void __launch_bounds__(kCamPassThreads) k_pixel_error(IterParams p, i
   const double f = cam[12], k1 = f * cam[13], k2 = fma(f * f * f, cam[14], 2.0 * k1 * k1);
   double se = 0, se2 = 0, nb = 0;
   for (int64_t o = ch.o0 + threadIdx.x; o < ch.o0 + ch.n; o += kCamPassThreads) {
-    const int32_t j = p.c_pt[o];
-    const double2 u = p.c_uv[o];
-    const double4 l = L[j];
-    const double vx = l.x - cam[9], vy = l.y - cam[10], vz = l.z - cam[11];
-    const double cx = fma(cam[0], vx, fma(cam[3], vy, cam[6] * vz));
-    const double cy = fma(cam[1], vx, fma(cam[4], vy, cam[7] * vz));
-    const double cz = fma(cam[2], vx, fma(cam[5], vy, cam[8] * vz));
-    nb += cz <= 0.0 ? 1.0 : 0.0;
-    const double qx = cx / cz, qy = cy / cz;
-    const double q2 = fma(qx, qx, qy * qy);
-    const double g = f * fma(q2, fma(q2, k2, k1), 1.0);
-    const double rx = fma(-g, qx, u.x), ry = fma(-g, qy, u.y);
-    const double r2 = fma(rx, rx, ry * ry);
-    se += sqrt(r2);
-    se2 += r2;
+    bool behind;
+    const double e = pixel_residual(cam, f, k1, k2, L[p.c_pt[o]], p.c_uv[o], &behind);
+    nb += behind ? 1.0 : 0.0;
+    se += e;
+    se2 = fma(e, e, se2);
+    if (resid) resid[o] = e;
   }
   __shared__ double sh[3][kCamPassThreads];
   sh[0][threadIdx.x] = se;
@@ -1312,10 +1318,10 @@ int launch_objective(const IterParams& p, cudaStream_t st) {
   return n + 1;
 }
 
-int launch_pixel_error(const IterParams& p, int role, double* out, cudaStream_t st) {
+int launch_pixel_error(const IterParams& p, int role, double* out, double* resid, cudaStream_t st) {
   int n = 0;
   if (p.n_chunks > 0) {
-    k_pixel_error<<<p.n_chunks, kCamPassThreads, 0, st>>>(p, role);
+    k_pixel_error<<<p.n_chunks, kCamPassThreads, 0, st>>>(p, role, resid);
     ++n;
   }
   k_reduce_pixel_error<<<1, 256, 0, st>>>(p, out);

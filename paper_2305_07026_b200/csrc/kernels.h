@@ -122,8 +122,9 @@ int launch_trace_post(const IterParams& p, cudaStream_t st);
 // F(x^k) only (create-time F-bar^{(-1)} and daba_objective): writes local[0] (and local[7] = degenerate count)
 int launch_objective(const IterParams& p, cudaStream_t st);
 // BAL pixel reprojection error of the state in role slot `role` (1: x^k, 0: x^{k-1}) over the camera-side
-// observations: out[0..3] (device) = sum |r|, sum |r|^2, #(P'_z <= 0), #observations
-int launch_pixel_error(const IterParams& p, int role, double* out, cudaStream_t st);
+// observations: out[0..3] (device) = sum |r|, sum |r|^2, #(P'_z <= 0), #observations; resid (device, or null):
+// |r| per camera-side observation
+int launch_pixel_error(const IterParams& p, int role, double* out, double* resid, cudaStream_t st);
 // halo exchange helpers: gather owned boundary entries of x^k into a send buffer / scatter received entries
 // (selected = 1: after a local decision both slots carry x^{k+1})
 int launch_pack(const IterParams& p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,

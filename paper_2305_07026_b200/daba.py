@@ -43,7 +43,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_get_schedule", "daba_last_decisions", "daba_shard_info", "daba_stream", "daba_kernel_times",
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
-           "daba_pixel_error", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
+           "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
            "daba_paper_to_bal"]
 
 
@@ -88,6 +88,7 @@ def lib():
         L.daba_plan_destroy.argtypes = [V]
         L.daba_plan_destroy.restype = None
         L.daba_pixel_error.argtypes = [V, V]
+        L.daba_pixel_residuals.argtypes = [V, V]
         L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
         L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
         L.daba_bal_last_error.argtypes = []
@@ -278,6 +279,13 @@ class Solver:
         n = max(out[3], 1.0)
         return {"mean": out[0] / n, "rms": float(np.sqrt(out[1] / n)), "behind": int(out[2]), "count": int(out[3]),
                 "sum": float(out[0]), "sum_sq": float(out[1])}
+
+    def pixel_residuals(self) -> np.ndarray:
+        """|r| in pixels per observation (input order) for this rank's owned cameras; NaN elsewhere
+        (daba_pixel_residuals)."""
+        out = np.full(self.K, np.nan)
+        self._check(lib().daba_pixel_residuals(self.h, out.ctypes.data), "daba_pixel_residuals")
+        return out
 
     def _out(self, shape):
         # entries this rank does not own stay NaN; one rank owns everything (no fill needed)

@@ -102,3 +102,40 @@ def test_pixel_error_edge_cases():
     o = oracle_metric(p.cams, pts, p.obs_cam, p.obs_pt, p.obs_uv)
     assert g["behind"] == o[2] >= 5
     assert g["sum"] == pytest.approx(o[0], rel=1e-11)
+
+
+@pytest.mark.parametrize("name", ["small_huber", "ladybug49"])
+def test_pixel_residuals_match_oracle(name):
+    p = gen.generate(name)
+    with solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv) as s:
+        s.iterate(5)
+        r = s.pixel_residuals()
+        g = s.pixel_error()
+        cams, pts, _ = s.state()
+    cb, ub = B.paper_to_bal(cams, p.obs_uv)
+    o, behind = B.pixel_residuals(cb, pts, p.obs_cam, p.obs_pt, ub)
+    np.testing.assert_allclose(r, o, rtol=1e-10, atol=1e-10)
+    assert r.sum() == pytest.approx(g["sum"], rel=1e-12)
+
+
+def test_pixel_residuals_unsorted_and_ranks():
+    # a permuted observation order (full host plan) and 2 LOCAL ranks: entries land at their input index
+    p = gen.generate("small_huber")
+    perm = np.random.default_rng(5).permutation(p.K)
+    oc, op, uv = p.obs_cam[perm], p.obs_pt[perm], p.obs_uv[perm]
+    with solver(p.cams, p.pts, oc, op, uv) as s:
+        ref = s.pixel_residuals()
+    assert np.isfinite(ref).all()
+    key = np.random.default_rng(8).bytes(128)
+    out = [None] * 2
+
+    def work(r):
+        with solver(p.cams, p.pts, oc, op, uv, rank=r, nranks=2, comm_key=key, comm=D.COMM_LOCAL) as s:
+            out[r] = s.pixel_residuals()
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    have = [np.isfinite(o) for o in out]
+    assert not (have[0] & have[1]).any() and (have[0] | have[1]).all()
+    merged = np.where(have[0], out[0], out[1])
+    np.testing.assert_allclose(merged, ref, rtol=1e-13)
