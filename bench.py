@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="final13682")
+    ap.add_argument("--config", default="final13682", help="a gen config name or the path of a BAL file")
     ap.add_argument("--restart", default="global", choices=["global", "device"])
     # test plumbing: "none" runs every rank's shard alone (DABA_COMM_NONE: no collectives, NOT the method's
     # iterates) so that the multi-rank driver logic can be exercised on a one-GPU box
@@ -115,6 +115,12 @@ WEAK = {"weak_slab"}  # BASELINE.json configs[4]: per-GPU slab fixed, N slabs at
 
 def make_problem(config, world):
     import gen
+    if os.path.isfile(config):  # a BAL file (the paper's datasets, when present): read natively, Huber loss
+        import paper_2305_07026_b200 as daba
+        b = daba.read_bal(config)
+        cams, uv = daba.bal_to_paper(b.cams, b.obs_uv)
+        return gen.Problem(os.path.basename(config), cams, b.pts, b.obs_cam, b.obs_pt, uv, cams, b.pts,
+                           daba.LOSS_HUBER, 1.0), "strong"
     if config in WEAK:
         cM, cN, cK = gen.CONFIGS[config][:3]
         return gen.generate(config, M=cM * world, N=cN * world, K=cK * world), "weak"
@@ -174,7 +180,7 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "obs/s", "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64", "data": ("bal file" if os.path.isfile(a.config) else "synthetic"),
             "config": {"workload": a.config, "sample": sp.name, "sample_obs": int(sp.K)},
             "cpu_baseline": {"value": v, "unit": "obs/s", "cores": 1, "kind": "oracle",
                              "sample": f"{sp.name}: {sp.K} observations, {a.steps} iterations"},
@@ -324,7 +330,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3), "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": ("bal file" if os.path.isfile(a.config) else "synthetic"),
         "config": {"workload": a.config if scaling == "strong" else f"{a.config} x{world}", "cameras": p.M, "points": p.N, "observations": int(p.K),
                    "loss": ["trivial", "huber", "cauchy"][p.loss], "parallelism": f"camera-partitioned x{world}",
                    "restart": a.restart,
