@@ -197,6 +197,25 @@ int daba_pixel_error(daba_ctx* ctx, double out[4]);
  * Blocking; for statistics beyond the mean (median, percentiles).  DABA_E_STATE if the context has no scratch. */
 int daba_pixel_residuals(daba_ctx* ctx, double* resid_out);
 
+/* ---- NEXT-3 building block: Gauss-Newton blocks of the coarse-partition surrogate ----
+ * For a device's intra-device pairs E', whose penalties eq. Ealpha keeps exact: the blocks a
+ * Schur-complement LM step on the device eliminates (readings R-N3a, R-N3b).  With the world-frame
+ * residual r_k = R e (eq. error rotated; |r| = |e|), its Jacobians J_c (3x9, camera tangent (dtheta, dt, dd), left
+ * rotation perturbation) and J_l (3x3), and w_k = rho'(|r_k|^2) (loss: 0 trivial, 1 Huber, 2 Cauchy; scale delta):
+ *   U[i]  (81, row-major 9x9) = sum_{k of camera i} w J_c^T J_c      gc[i] (9) = sum_{k of camera i} w J_c^T r
+ *   V[j]  (9, row-major 3x3)  = sum_{k of point j}  w J_l^T J_l      gl[j] (3) = sum_{k of point j}  w J_l^T r
+ *   W[k]  (27, row-major 9x3) = w J_c^T J_l                          F_cam[i]  = sum_{k of camera i} rho(|r|^2)/2
+ * ALL pointers are DEVICE pointers (fp64 unless stated); the caller owns every buffer.  cams: M x 15 in the native
+ * layout (R camera->world row-major, t = camera centre, d = (f, f k1, f k2)); pts: N x 3; obs_pt (int32) and
+ * obs_uv (K x 2) sorted by camera, with camera i's observations at [cam_off[i], cam_off[i+1]) (int64, M+1 entries).
+ * A pair with |l - t| <= eps (Assumption 2) adds nothing and gets W[k] = 0.  V / gl are zeroed and then
+ * accumulated with fp64 atomics (summation order not fixed); U / gc / F_cam are written in a fixed order.
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).  Returns 0, DABA_E_INVALID_ARG (-1) for
+ * bad sizes / NULL buffers / unknown loss, DABA_E_CUDA (-3) if a launch fails. */
+int daba_coarse_blocks(const double* cams, int64_t M, const double* pts, int64_t N, const int32_t* obs_pt,
+                       const double* obs_uv, const int64_t* cam_off, int64_t K, int loss, double scale, double eps,
+                       double* U, double* gc, double* V, double* gl, double* W, double* F_cam, void* stream);
+
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
  * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's

@@ -268,3 +268,27 @@ def run(prob: Problem, iters: int):
         rows.append([Fk, Fbar, E_acc, float(restart and o.accelerate), E_mm])
         s = s_next
     return np.array(rows), cams, pts
+
+
+def normal_blocks(prob: Problem, cams, pts):
+    """The Gauss-Newton blocks of sum_k F_k over ALL pairs (one device: every pair intra-device) at (cams, pts),
+    reading R-N3a: per camera U_i = sum w J_c^T J_c, gc_i = sum w J_c^T r, F_cam_i = sum rho / 2; per point
+    V_j = sum w J_l^T J_l, gl_j = sum w J_l^T r; per observation W_k = w J_c^T J_l.  Degenerate pairs add nothing
+    (R-N3d).  The same terms device_step() adds for E' pairs."""
+    o = prob.opt
+    U, gc, Fc = np.zeros((prob.M, 9, 9)), np.zeros((prob.M, 9)), np.zeros(prob.M)
+    V, gl, W = np.zeros((prob.N, 3, 3)), np.zeros((prob.N, 3)), np.zeros((prob.K, 9, 3))
+    for k in range(prob.K):
+        i, j = prob.oc[k], prob.op[k]
+        rj = residual_jacobians(cams[i], pts[j], prob.uv[k], o.eps)
+        if rj is None:
+            continue
+        r, Jc, Jl = rj
+        rho, w = loss(o.kind, o.scale, r @ r)
+        U[i] += w * Jc.T @ Jc
+        gc[i] += w * Jc.T @ r
+        Fc[i] += 0.5 * rho
+        V[j] += w * Jl.T @ Jl
+        gl[j] += w * Jl.T @ r
+        W[k] = w * Jc.T @ Jl
+    return U, gc, V, gl, W, Fc

@@ -44,7 +44,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
-           "daba_paper_to_bal"]
+           "daba_paper_to_bal", "daba_coarse_blocks"]
 
 
 def lib():
@@ -89,6 +89,8 @@ def lib():
         L.daba_plan_destroy.restype = None
         L.daba_pixel_error.argtypes = [V, V]
         L.daba_pixel_residuals.argtypes = [V, V]
+        L.daba_coarse_blocks.argtypes = [V, I64, V, I64, V, V, V, I64, I32, ctypes.c_double, ctypes.c_double, V, V, V,
+                                         V, V, V, V]
         L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
         L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
         L.daba_bal_last_error.argtypes = []
@@ -181,6 +183,31 @@ def bal_to_paper(cams, obs_uv):
 def paper_to_bal(cams, obs_uv):
     """Inverse of bal_to_paper (copies; daba_paper_to_bal)."""
     return _convert(lib().daba_paper_to_bal, cams, obs_uv)
+
+
+def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1.0, eps=1e-8, stream=None):
+    """daba_coarse_blocks (include/daba.h): the Gauss-Newton blocks of the intra-device penalties.
+    Inputs are CUDA tensors already on the device (torch: device memory only): cams (M, 15) fp64 native layout,
+    pts (N, 3) fp64, obs_pt (K,) int32 and obs_uv (K, 2) fp64 sorted by camera, cam_off (M + 1,) int64.  Returns
+    the CUDA tensors (U (M, 9, 9), gc (M, 9), V (N, 3, 3), gl (N, 3), W (K, 9, 3), F_cam (M,)); the call is
+    asynchronous on `stream` (default: torch's current stream)."""
+    import torch
+    M, N, K = cams.shape[0], pts.shape[0], obs_pt.shape[0]
+    for t, dt in ((cams, torch.float64), (pts, torch.float64), (obs_uv, torch.float64), (obs_pt, torch.int32),
+                  (cam_off, torch.int64)):
+        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+            raise DabaError(-1, "coarse_blocks: contiguous CUDA tensors of the documented dtypes required")
+    dev, f64 = cams.device, torch.float64
+    U, gc = torch.empty((M, 9, 9), dtype=f64, device=dev), torch.empty((M, 9), dtype=f64, device=dev)
+    V, gl = torch.empty((N, 3, 3), dtype=f64, device=dev), torch.empty((N, 3), dtype=f64, device=dev)
+    W, F = torch.empty((K, 9, 3), dtype=f64, device=dev), torch.empty((M,), dtype=f64, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    rc = lib().daba_coarse_blocks(cams.data_ptr(), M, pts.data_ptr(), N, obs_pt.data_ptr(), obs_uv.data_ptr(),
+                                  cam_off.data_ptr(), K, int(loss), float(scale), float(eps), U.data_ptr(),
+                                  gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(), F.data_ptr(), st)
+    if rc != 0:
+        raise DabaError(rc, "daba_coarse_blocks")
+    return U, gc, V, gl, W, F
 
 
 class Plan:

@@ -125,3 +125,33 @@ def test_one_device_solves_a_zero_residual_problem():
     # xi move by kappa / (kappa + xi) per iteration), so the pin is a large factor, not quadratic convergence
     assert F1 < 1e-6 * t1[0, 0], (F1, t1[0, 0])
     assert F1 < 1e-3 * Ff, (F1, Ff)
+
+
+@pytest.mark.parametrize("loss", [oracle.LOSS_TRIVIAL, oracle.LOSS_HUBER, oracle.LOSS_CAUCHY])
+def test_normal_blocks_gradient_is_the_fd_gradient_of_F(loss):
+    """sum_k w J^T r is the gradient of F = sum_k rho(|e_k|^2) / 2 (chain rule, eq. Fij), and F_cam sums to F."""
+    p = gen.generate("tiny_seq", loss=loss, outlier_frac=0.05 if loss else 0.0)
+    cp = coarse.Problem(p, np.zeros(p.M, int), np.zeros(p.N, int))
+    c0, l0 = cp.cams0, cp.pts0
+    U, gc, V, gl, W, Fc = coarse.normal_blocks(cp, c0, l0)
+    assert Fc.sum() == pytest.approx(cp.objective(c0, l0), rel=1e-12)
+    smax = float(np.max(np.sum(cp.uv ** 2, axis=1)))  # |u|^2: d2, d3 multiply |u|^2, |u|^4 (eq. ray)
+    for i in (0, p.M - 1):
+        for m in range(9):
+            h = 1e-6 * (max(1.0, abs(c0[i, 6 + m])) / max(1.0, smax ** (m - 6) if m >= 6 else 1.0) if m >= 3 else 1.0)
+            d = np.zeros(9)
+            d[m] = h
+            cpl, cmi = c0.copy(), c0.copy()
+            cpl[i] = coarse.retract_camera(c0[i], d)
+            cmi[i] = coarse.retract_camera(c0[i], -d)
+            fd = (cp.objective(cpl, l0) - cp.objective(cmi, l0)) / (2 * h)
+            assert fd == pytest.approx(gc[i, m], rel=1e-5, abs=1e-6 * np.abs(gc[i]).max())
+    for j in (0, p.N // 2):
+        for m in range(3):
+            h = 1e-6 * max(1.0, abs(l0[j, m]))
+            lp, lm = l0.copy(), l0.copy()
+            lp[j, m] += h
+            lm[j, m] -= h
+            fd = (cp.objective(c0, lp) - cp.objective(c0, lm)) / (2 * h)
+            assert fd == pytest.approx(gl[j, m], rel=1e-5, abs=1e-6 * np.abs(gl[j]).max())
+    assert np.all(np.linalg.eigvalsh(U) > -1e-9 * np.abs(U).max())  # w >= 0: PSD blocks
