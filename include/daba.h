@@ -216,6 +216,23 @@ int daba_coarse_blocks(const double* cams, int64_t M, const double* pts, int64_t
                        const double* obs_uv, const int64_t* cam_off, int64_t K, int loss, double scale, double eps,
                        double* U, double* gc, double* V, double* gl, double* W, double* F_cam, void* stream);
 
+/* The damped LM direction of a device's coarse subproblem (reading R-N3c) from the blocks above:
+ *   [[U + Pc, W], [W^T, V + Pl]] + mu diag(same)   [dc; dl] = -[gc; gl],
+ * Pc = xi diag(2,2,2,1,1,1,1,1,1) per camera and Pl = xi I per point (the proximal term of eq. Ealpha, reading Q7).
+ * Points are eliminated exactly; the reduced camera system is solved by block-Jacobi preconditioned conjugate
+ * gradients (implicit Schur products, two observation passes each) until |r|_P <= tol |b|_P or max_iter
+ * iterations; then dl = -(V + Pl)'^-1 (gl + W^T dc).  Inputs are daba_coarse_blocks' outputs plus obs_cam (int32,
+ * sorted by camera) and the same obs_pt / cam_off; all DEVICE pointers, caller-owned.  dc: M x 9, dl: N x 3
+ * (device, written).  work: daba_coarse_solve_workspace(M, N) doubles of device scratch.  info (HOST, 2 doubles):
+ * PCG iterations taken, final preconditioned residual ratio.  Blocking (synchronises `stream`).  Returns 0,
+ * DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3), or DABA_E_STATE (-6) if a damped 3x3 / 9x9 block is not positive
+ * definite (a failed LM trial: retry with a larger mu). */
+int64_t daba_coarse_solve_workspace(int64_t M, int64_t N);
+int daba_coarse_solve(const double* U, const double* gc, const double* V, const double* gl, const double* W,
+                      const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N,
+                      int64_t K, double xi, double mu, int max_iter, double tol, double* dc, double* dl, double* work,
+                      double info[2], void* stream);
+
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
  * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's

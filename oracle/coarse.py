@@ -144,9 +144,9 @@ class Problem:
         return tot + 0.5 * self.opt.xi * prox
 
     # ------------------------------------------------------------ one device subproblem, one successful LM step
-    def device_step(self, a, cams_hat, pts_hat):
-        """argmin_{x^a} E^a(x^a | x_hat) approximated by one successful LM step from x_hat^a (P:L596; R-N3a, R-N3c).
-        Returns (cams, pts) with only device a's variables changed, and the accepted trial (-1: none)."""
+    def device_system(self, a, cams_hat, pts_hat):
+        """Gauss-Newton normal equations (H, g) of E^a(. | x_hat) at x_hat^a on the device's stacked tangent (9 per
+        camera in ascending id, then 3 per point), proximal term included (R-N3a); also the variable layout."""
         o = self.opt
         ci = np.flatnonzero(self.cam_dev == a)
         pj = np.flatnonzero(self.pt_dev == a)
@@ -192,21 +192,33 @@ class Problem:
                 # eq. Q: Q(l) = w |lam l - g|^2 + a/2: gradient 2 w lam (lam l - g), Hessian 2 w lam^2 I
                 H[sp:sp + 3, sp:sp + 3] += 2.0 * w * lam * lam * np.eye(3)
                 g[sp:sp + 3] += 2.0 * w * lam * (lam * pts_hat[j] - gq)
-        E0 = self.surrogate(cams_hat, pts_hat, cams_hat, pts_hat, [a])
-        dg = np.diag(H).copy()
-        sc = 1.0 / np.sqrt(dg)
+        return H, g, ci, pj, cpos, ppos
+
+    @staticmethod
+    def lm_direction(H, g, mu):
+        """The LM trial direction of reading R-N3c: (H + mu diag H) delta = -g solved by Jacobi-scaled Cholesky;
+        None on a non-positive pivot (a failed trial)."""
+        sc = 1.0 / np.sqrt(np.diag(H))
         Hs = H * np.outer(sc, sc)
-        gs = g * sc
+        A = Hs + mu * np.diag(np.diag(Hs))
+        try:
+            L = np.linalg.cholesky(A)
+        except np.linalg.LinAlgError:
+            return None
+        return np.linalg.solve(L.T, np.linalg.solve(L, -g * sc)) * sc
+
+    def device_step(self, a, cams_hat, pts_hat):
+        """argmin_{x^a} E^a(x^a | x_hat) approximated by one successful LM step from x_hat^a (P:L596; R-N3a, R-N3c).
+        Returns (cams, pts) with only device a's variables changed, and the accepted trial (-1: none)."""
+        o = self.opt
+        H, g, ci, pj, cpos, ppos = self.device_system(a, cams_hat, pts_hat)
+        E0 = self.surrogate(cams_hat, pts_hat, cams_hat, pts_hat, [a])
         mu = o.lm_mu0
         for tau in range(o.lm_max_trials):
-            A = Hs + mu * np.diag(np.diag(Hs))
-            try:
-                L = np.linalg.cholesky(A)
-            except np.linalg.LinAlgError:
+            delta = self.lm_direction(H, g, mu)
+            if delta is None:
                 mu *= o.lm_mu_up
                 continue
-            y = np.linalg.solve(L.T, np.linalg.solve(L, -gs))
-            delta = y * sc
             cams, pts = cams_hat.copy(), pts_hat.copy()
             for i in ci:
                 s = cpos[int(i)]

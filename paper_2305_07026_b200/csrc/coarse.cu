@@ -8,6 +8,7 @@
 // Product code only: shares nothing with oracle/.  Citations "P:L<n>" are PAPER.md lines.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "device_math.cuh"
 
@@ -179,5 +180,348 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
       k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, U, gc, V, gl, W, F_cam);
   }
   if (N > 0) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// ------------------------------------------------------------------ the damped LM direction by Schur complement + PCG
+// (H + mu diag H) delta = -g for H = [[U + Pc, W], [W^T, V + Pl]] (per-observation W blocks, prox Pc = xi diag(2,2,2,
+// 1,...,1), Pl = xi I; reading R-N3c without the Jacobi scaling, which does not change the solution).  Points are
+// eliminated exactly (3x3 inverses); the reduced camera system S dc = b, S = U' - W V'^-1 W^T, is solved by
+// preconditioned conjugate gradients with the inverted 9x9 diagonal blocks of S, S applied implicitly (two
+// observation passes per product); dl = -V'^-1 (g_l + W^T dc).
+namespace daba {
+namespace {
+
+struct CS {  // workspace views (doubles)
+  double *Pinv, *Vinv, *yv, *t, *x, *r, *z, *p, *q, *s;
+};
+enum { S_RZ = 0, S_PQ, S_RZN, S_RZ0, S_DONE, S_ITERS, S_COLS = 8 };
+
+__device__ __forceinline__ double damp_cam(const double* Ui, int a, double xi, double mu) {  // diagonal of U'
+  const double d = Ui[10 * a] + xi * (a < 3 ? 2.0 : 1.0);
+  return d * (1.0 + mu);
+}
+
+// Cholesky inverse of an n x n SPD matrix A (row-major, overwritten by scratch) into Ainv; false if not SPD.
+template <int n>
+__device__ bool spd_inverse(double* A, double* Ainv) {
+  for (int j = 0; j < n; ++j) {
+    double d = A[n * j + j];
+    for (int k = 0; k < j; ++k) d -= A[n * j + k] * A[n * j + k];
+    if (!(d > 0)) return false;
+    d = sqrt(d);
+    A[n * j + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double v = A[n * i + j];
+      for (int k = 0; k < j; ++k) v -= A[n * i + k] * A[n * j + k];
+      A[n * i + j] = v / d;
+    }
+  }
+  for (int c = 0; c < n; ++c) {  // solve L L^T x = e_c
+    double y[n];
+    for (int i = 0; i < n; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) v -= A[n * i + k] * y[k];
+      y[i] = v / A[n * i + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double v = y[i];
+      for (int k = i + 1; k < n; ++k) v -= A[n * k + i] * Ainv[n * k + c];
+      Ainv[n * i + c] = v / A[n * i + i];
+    }
+  }
+  return true;
+}
+
+__global__ void k_cs_points(const double* __restrict__ V, const double* __restrict__ gl, int64_t N, double xi,
+                            double mu, CS w, int* bad) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double A[9], Ai[9];
+  for (int e = 0; e < 9; ++e) A[e] = V[9 * j + e];
+  for (int a = 0; a < 3; ++a) A[4 * a] = (A[4 * a] + xi) * (1.0 + mu);
+  if (!spd_inverse<3>(A, Ai)) {
+    atomicAdd(bad, 1);
+    for (int e = 0; e < 9; ++e) Ai[e] = 0.0;
+  }
+  for (int e = 0; e < 9; ++e) w.Vinv[9 * j + e] = Ai[e];
+  for (int a = 0; a < 3; ++a)
+    w.yv[3 * j + a] = Ai[3 * a] * gl[3 * j] + Ai[3 * a + 1] * gl[3 * j + 1] + Ai[3 * a + 2] * gl[3 * j + 2];
+}
+
+// Per camera: the diagonal block of S and its inverse, and b_i = -g_c,i + sum_k W_k V'^-1 g_l,j.
+__global__ void __launch_bounds__(kCoarseThreads) k_cs_cams(const double* __restrict__ U, const double* __restrict__ gc,
+                                                            const double* __restrict__ W,
+                                                            const int32_t* __restrict__ obs_pt,
+                                                            const int64_t* __restrict__ cam_off, double xi, double mu,
+                                                            CS w, int* bad) {
+  const int i = blockIdx.x;
+  double acc[kUCols];
+#pragma unroll
+  for (int k = 0; k < kUCols; ++k) acc[k] = 0.0;
+  for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
+    const int32_t j = obs_pt[k];
+    const double* Wk = W + (size_t)k * 27;
+    const double* Vi = w.Vinv + 9 * (size_t)j;
+    double WV[27];  // W_k V'^-1 (9x3)
+#pragma unroll
+    for (int a = 0; a < 9; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) WV[3 * a + c] = Wk[3 * a] * Vi[c] + Wk[3 * a + 1] * Vi[3 + c] + Wk[3 * a + 2] * Vi[6 + c];
+    const double* gj = w.yv + 3 * (size_t)j;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) {
+#pragma unroll
+      for (int c = 0; c <= a; ++c)
+        acc[tri9(a, c)] += WV[3 * a] * Wk[3 * c] + WV[3 * a + 1] * Wk[3 * c + 1] + WV[3 * a + 2] * Wk[3 * c + 2];
+      acc[45 + a] += Wk[3 * a] * gj[0] + Wk[3 * a + 1] * gj[1] + Wk[3 * a + 2] * gj[2];
+    }
+  }
+  __shared__ double red[kCoarseThreads / 32][kUCols];
+  __shared__ double tot[kUCols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kUCols; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    if (lane == 0) red[warp][k] = x;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kUCols; k += kCoarseThreads) {
+    double x = 0.0;
+    for (int v = 0; v < kCoarseThreads / 32; ++v) x += red[v][k];
+    tot[k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double* Ui = U + (size_t)i * 81;
+    double D[81], Di[81];
+    for (int a = 0; a < 9; ++a)
+      for (int c = 0; c <= a; ++c) {
+        const double v = (a == c ? damp_cam(Ui, a, xi, mu) : Ui[9 * a + c]) - tot[tri9(a, c)];
+        D[9 * a + c] = v;
+        D[9 * c + a] = v;
+      }
+    if (!spd_inverse<9>(D, Di)) {
+      atomicAdd(bad, 1);
+      for (int e = 0; e < 81; ++e) Di[e] = 0.0;
+    }
+    for (int e = 0; e < 81; ++e) w.Pinv[(size_t)i * 81 + e] = Di[e];
+    for (int a = 0; a < 9; ++a) w.r[(size_t)i * 9 + a] = -gc[(size_t)i * 9 + a] + tot[45 + a];  // b
+  }
+}
+
+// x = 0, r = b (already in r), z = P^-1 r, p = z, s[RZ] = r.z
+__global__ void k_cs_init(int64_t M, CS w) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double rz = 0.0;
+  if (i < M) {
+    const double* Pi = w.Pinv + i * 81;
+    const double* ri = w.r + i * 9;
+    for (int a = 0; a < 9; ++a) {
+      double v = 0.0;
+      for (int c = 0; c < 9; ++c) v += Pi[9 * a + c] * ri[c];
+      w.z[i * 9 + a] = v;
+      w.p[i * 9 + a] = v;
+      w.x[i * 9 + a] = 0.0;
+      rz += ri[a] * v;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) rz += __shfl_down_sync(0xffffffffu, rz, off);
+  if ((threadIdx.x & 31) == 0 && rz != 0.0) atomicAdd(w.s + S_RZ, rz);
+}
+
+__global__ void k_cs_start(CS w) {
+  w.s[S_RZ0] = w.s[S_RZ];
+  w.s[S_PQ] = w.s[S_RZN] = 0.0;
+  w.s[S_ITERS] = 0.0;
+  w.s[S_DONE] = (w.s[S_RZ] <= 0.0) ? 1.0 : 0.0;
+}
+
+// t_j = sum_{k of j} W_k^T v_{c(k)} (fp64 atomics; t zeroed by the caller)
+__global__ void k_cs_pass1(const double* __restrict__ W, const int32_t* __restrict__ obs_cam,
+                           const int32_t* __restrict__ obs_pt, int64_t K, const double* __restrict__ v, double* t,
+                           const double* s, int check_done) {
+  if (check_done && s[S_DONE] != 0.0) return;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double* Wk = W + k * 27;
+  const double* vi = v + 9 * (size_t)obs_cam[k];
+  const int32_t j = obs_pt[k];
+  for (int c = 0; c < 3; ++c) {
+    double x = 0.0;
+    for (int a = 0; a < 9; ++a) x += Wk[3 * a + c] * vi[a];
+    atomicAdd(t + 3 * (size_t)j + c, x);
+  }
+}
+
+// q_i = U'_i p_i - sum_{k of i} W_k V'^-1 t_j ; s[PQ] += p.q
+__global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __restrict__ U, const double* __restrict__ W,
+                                                             const int32_t* __restrict__ obs_pt,
+                                                             const int64_t* __restrict__ cam_off, double xi, double mu,
+                                                             CS w) {
+  if (w.s[S_DONE] != 0.0) return;
+  const int i = blockIdx.x;
+  double acc[9];
+#pragma unroll
+  for (int a = 0; a < 9; ++a) acc[a] = 0.0;
+  for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
+    const int32_t j = obs_pt[k];
+    const double* Vi = w.Vinv + 9 * (size_t)j;
+    const double* tj = w.t + 3 * (size_t)j;
+    double u[3];
+    for (int c = 0; c < 3; ++c) u[c] = Vi[3 * c] * tj[0] + Vi[3 * c + 1] * tj[1] + Vi[3 * c + 2] * tj[2];
+    const double* Wk = W + (size_t)k * 27;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) acc[a] += Wk[3 * a] * u[0] + Wk[3 * a + 1] * u[1] + Wk[3 * a + 2] * u[2];
+  }
+  __shared__ double red[kCoarseThreads / 32][9];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    double x = acc[a];
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    if (lane == 0) red[warp][a] = x;
+  }
+  __shared__ double pq[9];
+  __syncthreads();
+  if (threadIdx.x < 9) {
+    const int a = threadIdx.x;
+    double x = 0.0;
+    for (int v = 0; v < kCoarseThreads / 32; ++v) x += red[v][a];
+    const double* Ui = U + (size_t)i * 81;
+    const double* pi = w.p + (size_t)i * 9;
+    double up = 0.0;
+    for (int c = 0; c < 9; ++c) up += (c == a ? damp_cam(Ui, a, xi, mu) : Ui[9 * a + c]) * pi[c];
+    const double qa = up - x;
+    w.q[(size_t)i * 9 + a] = qa;
+    pq[a] = pi[a] * qa;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int a = 0; a < 9; ++a) v += pq[a];
+    atomicAdd(w.s + S_PQ, v);
+  }
+}
+
+// x += alpha p, r -= alpha q, z = P^-1 r, s[RZN] += r.z
+__global__ void k_cs_update1(int64_t M, CS w) {
+  if (w.s[S_DONE] != 0.0) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double alpha = w.s[S_RZ] / w.s[S_PQ];
+  double rz = 0.0;
+  if (i < M) {
+    double ri[9];
+    for (int a = 0; a < 9; ++a) {
+      w.x[i * 9 + a] += alpha * w.p[i * 9 + a];
+      ri[a] = w.r[i * 9 + a] - alpha * w.q[i * 9 + a];
+      w.r[i * 9 + a] = ri[a];
+    }
+    const double* Pi = w.Pinv + i * 81;
+    for (int a = 0; a < 9; ++a) {
+      double v = 0.0;
+      for (int c = 0; c < 9; ++c) v += Pi[9 * a + c] * ri[c];
+      w.z[i * 9 + a] = v;
+      rz += ri[a] * v;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) rz += __shfl_down_sync(0xffffffffu, rz, off);
+  if ((threadIdx.x & 31) == 0 && rz != 0.0) atomicAdd(w.s + S_RZN, rz);
+}
+
+// p = z + beta p
+__global__ void k_cs_update2(int64_t M, CS w) {
+  if (w.s[S_DONE] != 0.0) return;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= 9 * M) return;
+  const double beta = w.s[S_RZN] / w.s[S_RZ];
+  w.p[e] = w.z[e] + beta * w.p[e];
+}
+
+__global__ void k_cs_scalars(CS w, double tol2) {
+  if (w.s[S_DONE] != 0.0) return;
+  w.s[S_RZ] = w.s[S_RZN];
+  w.s[S_PQ] = w.s[S_RZN] = 0.0;
+  w.s[S_ITERS] += 1.0;
+  if (!(w.s[S_RZ] > tol2 * w.s[S_RZ0])) w.s[S_DONE] = 1.0;
+}
+
+// dl_j = -V'^-1 (g_l,j + t_j) with t = W^T dc; dc = x
+__global__ void k_cs_backsub(const double* __restrict__ gl, int64_t N, CS w, double* dl) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const double* Vi = w.Vinv + 9 * j;
+  double h[3];
+  for (int c = 0; c < 3; ++c) h[c] = gl[3 * j + c] + w.t[3 * j + c];
+  for (int a = 0; a < 3; ++a) dl[3 * j + a] = -(Vi[3 * a] * h[0] + Vi[3 * a + 1] * h[1] + Vi[3 * a + 2] * h[2]);
+}
+
+}  // namespace
+}  // namespace daba
+
+extern "C" int64_t daba_coarse_solve_workspace(int64_t M, int64_t N) {
+  if (M < 0 || N < 0) return -1;
+  return M * 81 + N * 9 + N * 3 + N * 3 + 5 * M * 9 + daba::S_COLS + 8;
+}
+
+extern "C" int daba_coarse_solve(const double* U, const double* gc, const double* V, const double* gl, const double* W,
+                                 const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M,
+                                 int64_t N, int64_t K, double xi, double mu, int max_iter, double tol, double* dc,
+                                 double* dl, double* work, double info[2], void* stream) {
+  using namespace daba;
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(xi >= 0) || !(mu >= 0) || max_iter < 0 || !(tol >= 0) || !info)
+    return -1;
+  if ((M > 0 && (!U || !gc || !cam_off || !dc || !work)) || (N > 0 && (!V || !gl || !dl || !work)) ||
+      (K > 0 && (!W || !obs_cam || !obs_pt)))
+    return -1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CS w;
+  double* o = work;
+  w.Pinv = o; o += M * 81;
+  w.Vinv = o; o += N * 9;
+  w.yv = o; o += N * 3;
+  w.t = o; o += N * 3;
+  w.r = o; o += M * 9;
+  w.z = o; o += M * 9;
+  w.p = o; o += M * 9;
+  w.q = o; o += M * 9;
+  w.s = o; o += S_COLS;
+  int* bad = reinterpret_cast<int*>(o);
+  w.x = dc;  // the camera direction is PCG's iterate
+  const int T = 256;
+  const unsigned gM = (unsigned)((M + T - 1) / T), gN = (unsigned)((N + T - 1) / T), gK = (unsigned)((K + T - 1) / T),
+                 g9M = (unsigned)((9 * M + T - 1) / T);
+  if (cudaMemsetAsync(w.s, 0, (S_COLS + 8) * sizeof(double), st) != cudaSuccess) return -3;
+  if (N > 0) k_cs_points<<<gN, T, 0, st>>>(V, gl, N, xi, mu, w, bad);
+  if (M > 0) {
+    k_cs_cams<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, gc, W, obs_pt, cam_off, xi, mu, w, bad);
+    k_cs_init<<<gM, T, 0, st>>>(M, w);
+  }
+  k_cs_start<<<1, 1, 0, st>>>(w);
+  for (int it = 0; it < max_iter && M > 0; ++it) {
+    if (N > 0) {
+      if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
+      if (K > 0) k_cs_pass1<<<gK, T, 0, st>>>(W, obs_cam, obs_pt, K, w.p, w.t, w.s, 1);
+    }
+    k_cs_pass2<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, W, obs_pt, cam_off, xi, mu, w);
+    k_cs_update1<<<gM, T, 0, st>>>(M, w);
+    k_cs_update2<<<g9M, T, 0, st>>>(M, w);
+    k_cs_scalars<<<1, 1, 0, st>>>(w, tol * tol);
+  }
+  if (N > 0) {  // back-substitution for the points
+    if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
+    if (K > 0 && M > 0) k_cs_pass1<<<gK, T, 0, st>>>(W, obs_cam, obs_pt, K, dc, w.t, w.s, 0);
+    k_cs_backsub<<<gN, T, 0, st>>>(gl, N, w, dl);
+  }
+  double s[S_COLS + 1];
+  if (cudaMemcpyAsync(s, w.s, (S_COLS + 1) * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -3;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -3;
+  int nbad;
+  memcpy(&nbad, &s[S_COLS], sizeof nbad);
+  info[0] = s[S_ITERS];
+  info[1] = s[S_RZ0] > 0 ? sqrt(s[S_RZ] / s[S_RZ0]) : 0.0;
+  if (nbad) return -6;  // a damped block is not positive definite: a failed LM trial (R-N3c)
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

@@ -44,7 +44,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
-           "daba_paper_to_bal", "daba_coarse_blocks"]
+           "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve"]
 
 
 def lib():
@@ -91,6 +91,10 @@ def lib():
         L.daba_pixel_residuals.argtypes = [V, V]
         L.daba_coarse_blocks.argtypes = [V, I64, V, I64, V, V, V, I64, I32, ctypes.c_double, ctypes.c_double, V, V, V,
                                          V, V, V, V]
+        L.daba_coarse_solve_workspace.argtypes = [I64, I64]
+        L.daba_coarse_solve_workspace.restype = I64
+        L.daba_coarse_solve.argtypes = [V, V, V, V, V, V, V, V, I64, I64, I64, ctypes.c_double, ctypes.c_double, I32,
+                                        ctypes.c_double, V, V, V, V, V]
         L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
         L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
         L.daba_bal_last_error.argtypes = []
@@ -208,6 +212,30 @@ def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1
     if rc != 0:
         raise DabaError(rc, "daba_coarse_blocks")
     return U, gc, V, gl, W, F
+
+
+def coarse_solve(blocks, obs_cam, obs_pt, cam_off, xi=1e-4, mu=1e-3, max_iter=500, tol=1e-14, stream=None):
+    """daba_coarse_solve (include/daba.h): the damped LM direction (dc (M, 9), dl (N, 3), CUDA
+    tensors) of one device's coarse subproblem from coarse_blocks()' output, and (PCG iterations, residual ratio)."""
+    import torch
+    U, gc, V, gl, W, _ = blocks
+    M, N, K = U.shape[0], V.shape[0], W.shape[0]
+    for t, dt in ((obs_cam, torch.int32), (obs_pt, torch.int32), (cam_off, torch.int64)):
+        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+            raise DabaError(-1, "coarse_solve: contiguous CUDA tensors of the documented dtypes required")
+    dev = U.device
+    dc = torch.zeros((M, 9), dtype=torch.float64, device=dev)
+    dl = torch.zeros((N, 3), dtype=torch.float64, device=dev)
+    work = torch.empty((max(1, lib().daba_coarse_solve_workspace(M, N)),), dtype=torch.float64, device=dev)
+    info = np.zeros(2)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    rc = lib().daba_coarse_solve(U.data_ptr(), gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(),
+                                 obs_cam.data_ptr(), obs_pt.data_ptr(), cam_off.data_ptr(), M, N, K, float(xi), float(mu),
+                                 int(max_iter), float(tol), dc.data_ptr(), dl.data_ptr(), work.data_ptr(),
+                                 info.ctypes.data, st)
+    if rc != 0:
+        raise DabaError(rc, "daba_coarse_solve")
+    return dc, dl, (int(info[0]), float(info[1]))
 
 
 class Plan:
