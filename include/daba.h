@@ -233,6 +233,22 @@ int daba_coarse_solve(const double* U, const double* gc, const double* V, const 
                       int64_t K, double xi, double mu, int max_iter, double tol, double* dc, double* dl, double* work,
                       double info[2], void* stream);
 
+/* Algorithm 1 with the coarse-partition surrogate on ONE device (SURVEY NEXT-3 at N = 1): every pair
+ * is intra-device, so E(x | x_hat) = F(x) + xi/2 |x - x_hat|^2 (eq. Ealpha) and each of the two subproblems per
+ * iteration (anchors x-bar^k and x^k, eqs. update_amm / update_mm) is one successful LM step on the whole problem
+ * (readings R-N3a..d): daba_coarse_blocks, then daba_coarse_solve with mu = mu0 * mu_up^tau, tau <
+ * lm_trials, accepting the first trial with a strict decrease of E.  Nesterov extrapolation with ProjRot3D and the
+ * global restart test E(x_acc | x^k) > F-bar^k as in daba_iterate (reading D2; accelerate = 0: plain MM).
+ * cams (M x 15 native layout) and pts (N x 3) are DEVICE buffers holding x^0 on entry and x^n on return;
+ * obs_cam / obs_pt (int32), obs_uv (K x 2) DEVICE, sorted by camera with offsets cam_off (int64, M + 1, DEVICE).
+ * trace (HOST, n_iters x 5, nullable): F(x^k), F-bar^k, E(x_acc | x^k), restart flag, E(x_mm | x^k).
+ * Host-driven and blocking (scalars read back per LM trial); scratch is allocated stream-ordered and freed.
+ * Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3), DABA_E_OOM (-5). */
+int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam, const int32_t* obs_pt,
+                    const double* obs_uv, const int64_t* cam_off, int64_t K, int loss, double scale, double eps,
+                    double xi, double eta, double mu0, double mu_up, int lm_trials, int accelerate, int pcg_max_iter,
+                    double pcg_tol, int n_iters, double* trace, void* stream);
+
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
  * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's

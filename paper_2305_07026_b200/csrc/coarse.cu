@@ -10,6 +10,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "device_math.cuh"
 
 namespace daba {
@@ -524,4 +526,270 @@ extern "C" int daba_coarse_solve(const double* U, const double* gc, const double
   info[1] = s[S_RZ0] > 0 ? sqrt(s[S_RZ] / s[S_RZ0]) : 0.0;
   if (nbad) return -6;  // a damped block is not positive definite: a failed LM trial (R-N3c)
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+extern "C" int daba_coarse_blocks(const double*, int64_t, const double*, int64_t, const int32_t*, const double*,
+                                  const int64_t*, int64_t, int, double, double, double*, double*, double*, double*,
+                                  double*, double*, void*);
+extern "C" int64_t daba_coarse_solve_workspace(int64_t M, int64_t N);
+extern "C" int daba_coarse_solve(const double*, const double*, const double*, const double*, const double*,
+                                 const int32_t*, const int32_t*, const int64_t*, int64_t, int64_t, int64_t, double,
+                                 double, int, double, double*, double*, double*, double*, void*);
+
+// ------------------------------------------------------------------ Algorithm 1 with the coarse surrogate, one device
+// With one device every pair is intra-device (E'' empty), so E(x | x_hat) = F(x) + xi/2 |x - x_hat|^2 (eq. Ealpha)
+// and each subproblem is one successful LM step on the whole problem (R-N3a..d).  Host-driven: the LM
+// acceptance and the restart test read scalars back (first correct version; the finest-partition engine is the
+// graph-captured production path).
+namespace daba {
+namespace {
+
+__device__ bool pair_residual(const double* __restrict__ cam, const double* __restrict__ l, double2 u, double eps2,
+                              double r[3]) {
+  const double s = u.x * u.x + u.y * u.y;
+  const double pz = cam[12] + cam[13] * s + cam[14] * s * s;  // eq. ray
+  double q[3], v[3];
+  for (int a = 0; a < 3; ++a) {
+    q[a] = cam[3 * a] * u.x + cam[3 * a + 1] * u.y + cam[3 * a + 2] * pz;
+    v[a] = l[a] - cam[9 + a];
+  }
+  const double nv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  if (!(nv > eps2)) return false;
+  const double lam = (v[0] * q[0] + v[1] * q[1] + v[2] * q[2]) / nv;  // eq. lambdaij
+  for (int a = 0; a < 3; ++a) r[a] = q[a] - lam * v[a];              // R e (eq. error)
+  return true;
+}
+
+// F per camera (eq. Fobj restricted to the camera's observations), one CTA per camera, fixed-order reduction.
+template <int LOSS>
+__global__ void __launch_bounds__(kCoarseThreads) k_cr_F(const double* __restrict__ cams, const double* __restrict__ pts,
+                                                         const int32_t* __restrict__ obs_pt,
+                                                         const double2* __restrict__ uv,
+                                                         const int64_t* __restrict__ cam_off, double delta, double eps2,
+                                                         double* Fc) {
+  const int i = blockIdx.x;
+  const double* cam = cams + (size_t)i * 15;
+  const double delta2 = delta * delta, idelta2 = 1.0 / delta2;
+  double F = 0.0;
+  for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
+    const int32_t j = obs_pt[k];
+    const double l[3] = {pts[3 * (size_t)j], pts[3 * (size_t)j + 1], pts[3 * (size_t)j + 2]};
+    double r[3];
+    if (!pair_residual(cam, l, uv[k], eps2, r)) continue;  // Q17
+    double rho = 0.0;
+    loss_eval<LOSS, true>(r[0] * r[0] + r[1] * r[1] + r[2] * r[2], delta, delta2, idelta2, &rho);
+    F += 0.5 * rho;  // eq. Fij
+  }
+  __shared__ double red[kCoarseThreads / 32];
+  for (int off = 16; off > 0; off >>= 1) F += __shfl_down_sync(0xffffffffu, F, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = F;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kCoarseThreads / 32; ++w) t += red[w];
+    Fc[i] = t;
+  }
+}
+
+// out = sum_i Fc[i] + xi/2 (|c - c_hat|^2 + |l - l_hat|^2), one block, fixed order (c_hat == nullptr: no prox term)
+__global__ void __launch_bounds__(1024) k_cr_eval(const double* Fc, int64_t M, const double* c, const double* ch,
+                                                  int64_t N, const double* l, const double* lh, double xi, double* out) {
+  double F = 0.0, d = 0.0;
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) F += Fc[i];
+  if (ch) {
+    for (int64_t e = threadIdx.x; e < 15 * M; e += blockDim.x) d += (c[e] - ch[e]) * (c[e] - ch[e]);
+    for (int64_t e = threadIdx.x; e < 3 * N; e += blockDim.x) d += (l[e] - lh[e]) * (l[e] - lh[e]);
+  }
+  __shared__ double sF[32], sd[32];
+  for (int off = 16; off > 0; off >>= 1) {
+    F += __shfl_down_sync(0xffffffffu, F, off);
+    d += __shfl_down_sync(0xffffffffu, d, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sF[threadIdx.x >> 5] = F;
+    sd[threadIdx.x >> 5] = d;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) {
+      a += sF[w];
+      b += sd[w];
+    }
+    *out = a + 0.5 * xi * b;
+  }
+}
+
+// x-bar (eqs. nesterov_x): R through ProjRot3D (eq. proj_rot3d), t, d, l linear
+__global__ void k_cr_extrapolate(const double* c, const double* cp, const double* l, const double* lp, int64_t M,
+                                 int64_t N, double gamma, double* cb, double* lb) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < M) {
+    const double* ck = c + 15 * e;
+    const double* cq = cp + 15 * e;
+    double Mx[9], R[9];
+    for (int k = 0; k < 9; ++k) Mx[k] = ck[k] + gamma * (ck[k] - cq[k]);
+    proj_rot3d(Mx, R);
+    for (int k = 0; k < 9; ++k) cb[15 * e + k] = R[k];
+    for (int k = 9; k < 15; ++k) cb[15 * e + k] = ck[k] + gamma * (ck[k] - cq[k]);
+  }
+  if (e < 3 * N) lb[e] = l[e] + gamma * (l[e] - lp[e]);
+}
+
+// trial = (Exp(dtheta) R_hat, t_hat + dt, d_hat + dd; l_hat + dl) (reading Q5)
+__global__ void k_cr_retract(const double* ch, const double* lh, const double* dc, const double* dl, int64_t M,
+                             int64_t N, double* c, double* l) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < M) {
+    const double* a = ch + 15 * e;
+    const double* d = dc + 9 * e;
+    double E[9];
+    expm_minus_identity(d, E);
+    for (int r = 0; r < 3; ++r)
+      for (int q = 0; q < 3; ++q)
+        c[15 * e + 3 * r + q] = a[3 * r + q] + (E[3 * r] * a[q] + E[3 * r + 1] * a[3 + q] + E[3 * r + 2] * a[6 + q]);
+    for (int k = 0; k < 6; ++k) c[15 * e + 9 + k] = a[9 + k] + d[3 + k];
+  }
+  if (e < 3 * N) l[e] = lh[e] + dl[e];
+}
+
+struct Run {
+  int64_t M, N, K;
+  const int32_t *oc, *op;
+  const double2* uv;
+  const int64_t* off;
+  int loss;
+  double scale, eps2, eps, xi, mu0, mu_up;
+  int trials, pcg_iter;
+  double pcg_tol;
+  double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal;
+  cudaStream_t st;
+};
+
+int run_F(const Run& R, const double* c, const double* l, const double* ch, const double* lh, double* out) {
+  if (R.M > 0) {
+    if (R.loss == kHuber)
+      k_cr_F<kHuber><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
+    else if (R.loss == kCauchy)
+      k_cr_F<kCauchy><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
+    else
+      k_cr_F<kTrivial><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
+  }
+  k_cr_eval<<<1, 1024, 0, R.st>>>(R.Fc, R.M, c, ch, R.N, l, lh, R.xi, R.scal);
+  if (cudaMemcpyAsync(out, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess) return -3;
+  return cudaStreamSynchronize(R.st) == cudaSuccess ? 0 : -3;
+}
+
+// One successful LM step on E(. | anchor) = F + xi/2 |. - anchor|^2 from the anchor (R-N3c); out = the accepted
+// trial or the anchor.  *trial = accepted trial index or -1.
+int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
+            int* trial) {
+  int rc = daba_coarse_blocks(ca, R.M, la, R.N, R.op, reinterpret_cast<const double*>(R.uv), R.off, R.K, R.loss,
+                              R.scale, R.eps, R.U, R.gc, R.V, R.gl, R.W, R.Fc, R.st);
+  if (rc) return rc;
+  double E0;
+  if ((rc = run_F(R, ca, la, nullptr, nullptr, &E0))) return rc;
+  *trial = -1;
+  double mu = R.mu0;
+  const unsigned g = (unsigned)((std::max(R.M, 3 * R.N) + 255) / 256);
+  for (int tau = 0; tau < R.trials; ++tau, mu *= R.mu_up) {
+    double info[2];
+    rc = daba_coarse_solve(R.U, R.gc, R.V, R.gl, R.W, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter,
+                           R.pcg_tol, R.dcv, R.dlv, R.work, info, R.st);
+    if (rc == -6) continue;  // a damped block not positive definite: a failed trial
+    if (rc) return rc;
+    if (g) k_cr_retract<<<g, 256, 0, R.st>>>(ca, la, R.dcv, R.dlv, R.M, R.N, ct, lt);
+    double E;
+    if ((rc = run_F(R, ct, lt, ca, la, &E))) return rc;
+    if (E - E0 < 0) {
+      *trial = tau;
+      break;
+    }
+  }
+  const double* cs = *trial >= 0 ? ct : ca;
+  const double* ls = *trial >= 0 ? lt : la;
+  if (R.M && cudaMemcpyAsync(co, cs, R.M * 15 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    return -3;
+  if (R.N && cudaMemcpyAsync(lo, ls, R.N * 3 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    return -3;
+  return 0;
+}
+
+}  // namespace
+}  // namespace daba
+
+extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
+                               const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
+                               int loss, double scale, double eps, double xi, double eta, double mu0, double mu_up,
+                               int lm_trials, int accelerate, int pcg_max_iter, double pcg_tol, int n_iters,
+                               double* trace, void* stream) {
+  using namespace daba;
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || n_iters < 0 || !(scale > 0) || !(eps >= 0) || !(xi > 0) ||
+      !(eta > 0 && eta <= 1) || !(mu0 >= 0) || !(mu_up >= 1) || lm_trials < 1 || pcg_max_iter < 1 ||
+      !(pcg_tol >= 0) || loss < 0 || loss > 2)
+    return -1;
+  if ((M > 0 && (!cams || !cam_off)) || (N > 0 && !pts) || (K > 0 && (!obs_cam || !obs_pt || !obs_uv)))
+    return -1;
+  Run R{M, N, K, obs_cam, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, loss, scale, eps * eps, eps, xi,
+        mu0, mu_up, lm_trials, pcg_max_iter, pcg_tol};
+  R.st = static_cast<cudaStream_t>(stream);
+  const size_t nc = (size_t)M * 15, nl = (size_t)N * 3;
+  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9) + (size_t)N * (9 + 3 + 3) + (size_t)K * 27 +
+                       (size_t)daba_coarse_solve_workspace(M, N) + 8;
+  double* base = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), R.st) != cudaSuccess) return -5;
+  double* o = base;
+  auto take = [&](size_t n) { double* p = o; o += n; return p; };
+  double *cp = take(nc), *lp = take(nl), *cb = take(nc), *lb = take(nl), *ca = take(nc), *la = take(nl),
+         *cm = take(nc), *lm = take(nl), *ct = take(nc), *lt = take(nl);
+  R.U = take((size_t)M * 81);
+  R.gc = take((size_t)M * 9);
+  R.Fc = take((size_t)M);
+  R.dcv = take((size_t)M * 9);
+  R.V = take((size_t)N * 9);
+  R.gl = take((size_t)N * 3);
+  R.dlv = take((size_t)N * 3);
+  R.W = take((size_t)K * 27);
+  R.work = take((size_t)daba_coarse_solve_workspace(M, N));
+  R.scal = take(8);
+  int rc = 0;
+  // x^{-1} = x^0 (eq. Fainit); F-bar^{-1} = F(x^0) (A18, global form); s^0 = 1
+  if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
+      cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    rc = -3;
+  double Fbar = 0.0, s = 1.0;
+  if (!rc) rc = run_F(R, cams, pts, nullptr, nullptr, &Fbar);
+  const unsigned g = (unsigned)((std::max(M, 3 * N) + 255) / 256);
+  for (int it = 0; it < n_iters && !rc; ++it) {
+    const double s_next = (sqrt(4.0 * s * s + 1.0) + 1.0) / 2.0;  // eq. nesterov_scalar, Alg. 1
+    const double gamma = accelerate ? (s - 1.0) / s_next : 0.0;
+    if (g) k_cr_extrapolate<<<g, 256, 0, R.st>>>(cams, cp, pts, lp, M, N, gamma, cb, lb);
+    double Fk, Eacc, Emm;
+    int ta, tm;
+    if ((rc = run_F(R, cams, pts, nullptr, nullptr, &Fk))) break;
+    Fbar = (1.0 - eta) * Fbar + eta * Fk;  // eq. lFak
+    if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, &ta))) break;      // eq. update_amm
+    if ((rc = lm_step(R, cams, pts, cm, lm, ct, lt, &tm))) break;   // eq. update_mm
+    if ((rc = run_F(R, ca, la, cams, pts, &Eacc))) break;           // E(x_acc | x^k), eq. Eak
+    if ((rc = run_F(R, cm, lm, cams, pts, &Emm))) break;
+    const bool restart = accelerate ? (Eacc > Fbar) : true;         // Alg. 1, strict ">"
+    if (trace) {
+      double* t = trace + 5 * (size_t)it;
+      t[0] = Fk;
+      t[1] = Fbar;
+      t[2] = Eacc;
+      t[3] = (accelerate && restart) ? 1.0 : 0.0;
+      t[4] = Emm;
+    }
+    // x^{k-1} <- x^k, x^k <- x^{k+1}
+    if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
+        cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
+        cudaMemcpyAsync(cams, restart ? cm : ca, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
+        cudaMemcpyAsync(pts, restart ? lm : la, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+      rc = -3;
+    s = s_next;
+  }
+  cudaFreeAsync(base, R.st);
+  if (cudaStreamSynchronize(R.st) != cudaSuccess && !rc) rc = -3;
+  return rc;
 }

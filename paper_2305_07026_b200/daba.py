@@ -44,7 +44,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
-           "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve"]
+           "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve", "daba_coarse_run"]
 
 
 def lib():
@@ -95,6 +95,8 @@ def lib():
         L.daba_coarse_solve_workspace.restype = I64
         L.daba_coarse_solve.argtypes = [V, V, V, V, V, V, V, V, I64, I64, I64, ctypes.c_double, ctypes.c_double, I32,
                                         ctypes.c_double, V, V, V, V, V]
+        D = ctypes.c_double
+        L.daba_coarse_run.argtypes = [V, I64, V, I64, V, V, V, V, I64, I32, D, D, D, D, D, D, I32, I32, I32, D, I32, V, V]
         L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
         L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
         L.daba_bal_last_error.argtypes = []
@@ -236,6 +238,28 @@ def coarse_solve(blocks, obs_cam, obs_pt, cam_off, xi=1e-4, mu=1e-3, max_iter=50
     if rc != 0:
         raise DabaError(rc, "daba_coarse_solve")
     return dc, dl, (int(info[0]), float(info[1]))
+
+
+def coarse_run(cams, pts, obs_cam, obs_pt, obs_uv, cam_off, n_iters, loss=LOSS_TRIVIAL, scale=1.0, eps=1e-8,
+               xi=1e-4, eta=0.1, mu0=1e-3, mu_up=10.0, lm_trials=5, accelerate=1, pcg_max_iter=500, pcg_tol=1e-14,
+               stream=None):
+    """daba_coarse_run (include/daba.h; SURVEY NEXT-3 at one device): n_iters DABA iterations with the coarse
+    surrogate.  cams (M, 15) / pts (N, 3) CUDA fp64 tensors are updated in place; returns the (n_iters, 5) trace."""
+    import torch
+    for t, dt in ((cams, torch.float64), (pts, torch.float64), (obs_uv, torch.float64), (obs_cam, torch.int32),
+                  (obs_pt, torch.int32), (cam_off, torch.int64)):
+        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+            raise DabaError(-1, "coarse_run: contiguous CUDA tensors of the documented dtypes required")
+    tr = np.zeros((n_iters, 5))
+    st = stream if stream is not None else torch.cuda.current_stream(cams.device).cuda_stream
+    rc = lib().daba_coarse_run(cams.data_ptr(), cams.shape[0], pts.data_ptr(), pts.shape[0], obs_cam.data_ptr(),
+                               obs_pt.data_ptr(), obs_uv.data_ptr(), cam_off.data_ptr(), obs_pt.shape[0], int(loss),
+                               float(scale), float(eps), float(xi), float(eta), float(mu0), float(mu_up),
+                               int(lm_trials), int(accelerate), int(pcg_max_iter), float(pcg_tol), int(n_iters),
+                               tr.ctypes.data, st)
+    if rc != 0:
+        raise DabaError(rc, "daba_coarse_run")
+    return tr
 
 
 class Plan:
