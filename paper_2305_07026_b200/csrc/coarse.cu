@@ -82,9 +82,10 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
     const int32_t j = obs_pt[k];
     const double l[3] = {pts[3 * (size_t)j], pts[3 * (size_t)j + 1], pts[3 * (size_t)j + 2]};
     double r[3], Jc[27], Jl[9];
-    double* Wk = W + (size_t)k * 27;
+    double* Wk = W ? W + (size_t)k * 27 : nullptr;
     if (!pair_jacobians(scam, l, uv[k], eps2, r, Jc, Jl)) {  // R-N3d: the pair contributes nothing
-      for (int e = 0; e < 27; ++e) Wk[e] = 0.0;
+      if (Wk)
+        for (int e = 0; e < 27; ++e) Wk[e] = 0.0;
       continue;
     }
     const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
@@ -97,9 +98,10 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
       for (int c = 0; c <= a; ++c)
         acc[tri9(a, c)] += w * (Jc[a] * Jc[c] + Jc[9 + a] * Jc[9 + c] + Jc[18 + a] * Jc[18 + c]);
       acc[45 + a] += w * (Jc[a] * r[0] + Jc[9 + a] * r[1] + Jc[18 + a] * r[2]);
+      if (Wk)
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
+        for (int c = 0; c < 3; ++c)
+          Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -163,7 +165,7 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
   using namespace daba;
   if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(scale > 0) || !(eps >= 0) || loss < 0 || loss > 2) return -1;
   if ((M > 0 && (!cams || !cam_off || !U || !gc || !F_cam)) || (N > 0 && (!pts || !V || !gl)) ||
-      (K > 0 && (!obs_pt || !obs_uv || !W)))
+      (K > 0 && (!obs_pt || !obs_uv)))
     return -1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (N > 0) {
@@ -235,6 +237,38 @@ __device__ bool spd_inverse(double* A, double* Ainv) {
   return true;
 }
 
+// Where the per-observation W_k = w J_c^T J_l comes from: stored by daba_coarse_blocks, or recomputed from the
+// anchor state (44 B per observation read instead of 216 B; the same arithmetic as k_coarse_blocks).
+struct WSrc {
+  const double* W;
+  const double* cams;
+  const double* pts;
+  const double2* uv;
+  int loss;
+  double delta, eps2;
+};
+
+__device__ __forceinline__ void get_W(const WSrc& s, int64_t k, const double* cam, int32_t j, double Wk[27]) {
+  if (s.W) {
+    for (int e = 0; e < 27; ++e) Wk[e] = s.W[(size_t)k * 27 + e];
+    return;
+  }
+  const double l[3] = {s.pts[3 * (size_t)j], s.pts[3 * (size_t)j + 1], s.pts[3 * (size_t)j + 2]};
+  double r[3], Jc[27], Jl[9];
+  if (!pair_jacobians(cam, l, s.uv[k], s.eps2, r, Jc, Jl)) {
+    for (int e = 0; e < 27; ++e) Wk[e] = 0.0;
+    return;
+  }
+  const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+  const double d2 = s.delta * s.delta, id2 = 1.0 / d2;
+  double rho;
+  const double w = s.loss == kHuber    ? loss_eval<kHuber, false>(sh, s.delta, d2, id2, &rho)
+                   : s.loss == kCauchy ? loss_eval<kCauchy, false>(sh, s.delta, d2, id2, &rho)
+                                       : 1.0;
+  for (int a = 0; a < 9; ++a)
+    for (int c = 0; c < 3; ++c) Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
+}
+
 __global__ void k_cs_points(const double* __restrict__ V, const double* __restrict__ gl, int64_t N, double xi,
                             double mu, CS w, int* bad) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -253,17 +287,20 @@ __global__ void k_cs_points(const double* __restrict__ V, const double* __restri
 
 // Per camera: the diagonal block of S and its inverse, and b_i = -g_c,i + sum_k W_k V'^-1 g_l,j.
 __global__ void __launch_bounds__(kCoarseThreads) k_cs_cams(const double* __restrict__ U, const double* __restrict__ gc,
-                                                            const double* __restrict__ W,
-                                                            const int32_t* __restrict__ obs_pt,
+                                                            WSrc ws, const int32_t* __restrict__ obs_pt,
                                                             const int64_t* __restrict__ cam_off, double xi, double mu,
                                                             CS w, int* bad) {
   const int i = blockIdx.x;
+  __shared__ double scam[15];
+  if (threadIdx.x < 15) scam[threadIdx.x] = ws.cams ? ws.cams[(size_t)i * 15 + threadIdx.x] : 0.0;
+  __syncthreads();
   double acc[kUCols];
 #pragma unroll
   for (int k = 0; k < kUCols; ++k) acc[k] = 0.0;
   for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
     const int32_t j = obs_pt[k];
-    const double* Wk = W + (size_t)k * 27;
+    double Wk[27];
+    get_W(ws, k, scam, j, Wk);
     const double* Vi = w.Vinv + 9 * (size_t)j;
     double WV[27];  // W_k V'^-1 (9x3)
 #pragma unroll
@@ -342,15 +379,16 @@ __global__ void k_cs_start(CS w) {
 }
 
 // t_j = sum_{k of j} W_k^T v_{c(k)} (fp64 atomics; t zeroed by the caller)
-__global__ void k_cs_pass1(const double* __restrict__ W, const int32_t* __restrict__ obs_cam,
+__global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
                            const int32_t* __restrict__ obs_pt, int64_t K, const double* __restrict__ v, double* t,
                            const double* s, int check_done) {
   if (check_done && s[S_DONE] != 0.0) return;
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
-  const double* Wk = W + k * 27;
-  const double* vi = v + 9 * (size_t)obs_cam[k];
-  const int32_t j = obs_pt[k];
+  const int32_t i = obs_cam[k], j = obs_pt[k];
+  double Wk[27];
+  get_W(ws, k, ws.cams ? ws.cams + 15 * (size_t)i : nullptr, j, Wk);
+  const double* vi = v + 9 * (size_t)i;
   for (int c = 0; c < 3; ++c) {
     double x = 0.0;
     for (int a = 0; a < 9; ++a) x += Wk[3 * a + c] * vi[a];
@@ -359,12 +397,15 @@ __global__ void k_cs_pass1(const double* __restrict__ W, const int32_t* __restri
 }
 
 // q_i = U'_i p_i - sum_{k of i} W_k V'^-1 t_j ; s[PQ] += p.q
-__global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __restrict__ U, const double* __restrict__ W,
+__global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __restrict__ U, WSrc ws,
                                                              const int32_t* __restrict__ obs_pt,
                                                              const int64_t* __restrict__ cam_off, double xi, double mu,
                                                              CS w) {
   if (w.s[S_DONE] != 0.0) return;
   const int i = blockIdx.x;
+  __shared__ double scam[15];
+  if (threadIdx.x < 15) scam[threadIdx.x] = ws.cams ? ws.cams[(size_t)i * 15 + threadIdx.x] : 0.0;
+  __syncthreads();
   double acc[9];
 #pragma unroll
   for (int a = 0; a < 9; ++a) acc[a] = 0.0;
@@ -374,7 +415,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __res
     const double* tj = w.t + 3 * (size_t)j;
     double u[3];
     for (int c = 0; c < 3; ++c) u[c] = Vi[3 * c] * tj[0] + Vi[3 * c + 1] * tj[1] + Vi[3 * c + 2] * tj[2];
-    const double* Wk = W + (size_t)k * 27;
+    double Wk[27];
+    get_W(ws, k, scam, j, Wk);
 #pragma unroll
     for (int a = 0; a < 9; ++a) acc[a] += Wk[3 * a] * u[0] + Wk[3 * a + 1] * u[1] + Wk[3 * a + 2] * u[2];
   }
@@ -468,16 +510,12 @@ extern "C" int64_t daba_coarse_solve_workspace(int64_t M, int64_t N) {
   return M * 81 + N * 9 + N * 3 + N * 3 + 5 * M * 9 + daba::S_COLS + 8;
 }
 
-extern "C" int daba_coarse_solve(const double* U, const double* gc, const double* V, const double* gl, const double* W,
-                                 const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M,
-                                 int64_t N, int64_t K, double xi, double mu, int max_iter, double tol, double* dc,
-                                 double* dl, double* work, double info[2], void* stream) {
-  using namespace daba;
-  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(xi >= 0) || !(mu >= 0) || max_iter < 0 || !(tol >= 0) || !info)
-    return -1;
-  if ((M > 0 && (!U || !gc || !cam_off || !dc || !work)) || (N > 0 && (!V || !gl || !dl || !work)) ||
-      (K > 0 && (!W || !obs_cam || !obs_pt)))
-    return -1;
+namespace daba {
+namespace {
+int coarse_solve_impl(const double* U, const double* gc, const double* V, const double* gl, WSrc ws,
+                      const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N,
+                      int64_t K, double xi, double mu, int max_iter, double tol, double* dc, double* dl, double* work,
+                      double info[2], void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CS w;
   double* o = work;
@@ -498,23 +536,23 @@ extern "C" int daba_coarse_solve(const double* U, const double* gc, const double
   if (cudaMemsetAsync(w.s, 0, (S_COLS + 8) * sizeof(double), st) != cudaSuccess) return -3;
   if (N > 0) k_cs_points<<<gN, T, 0, st>>>(V, gl, N, xi, mu, w, bad);
   if (M > 0) {
-    k_cs_cams<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, gc, W, obs_pt, cam_off, xi, mu, w, bad);
+    k_cs_cams<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, gc, ws, obs_pt, cam_off, xi, mu, w, bad);
     k_cs_init<<<gM, T, 0, st>>>(M, w);
   }
   k_cs_start<<<1, 1, 0, st>>>(w);
   for (int it = 0; it < max_iter && M > 0; ++it) {
     if (N > 0) {
       if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
-      if (K > 0) k_cs_pass1<<<gK, T, 0, st>>>(W, obs_cam, obs_pt, K, w.p, w.t, w.s, 1);
+      if (K > 0) k_cs_pass1<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, w.p, w.t, w.s, 1);
     }
-    k_cs_pass2<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, W, obs_pt, cam_off, xi, mu, w);
+    k_cs_pass2<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, ws, obs_pt, cam_off, xi, mu, w);
     k_cs_update1<<<gM, T, 0, st>>>(M, w);
     k_cs_update2<<<g9M, T, 0, st>>>(M, w);
     k_cs_scalars<<<1, 1, 0, st>>>(w, tol * tol);
   }
   if (N > 0) {  // back-substitution for the points
     if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
-    if (K > 0 && M > 0) k_cs_pass1<<<gK, T, 0, st>>>(W, obs_cam, obs_pt, K, dc, w.t, w.s, 0);
+    if (K > 0 && M > 0) k_cs_pass1<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, dc, w.t, w.s, 0);
     k_cs_backsub<<<gN, T, 0, st>>>(gl, N, w, dl);
   }
   double s[S_COLS + 1];
@@ -527,7 +565,27 @@ extern "C" int daba_coarse_solve(const double* U, const double* gc, const double
   if (nbad) return -6;  // a damped block is not positive definite: a failed LM trial (R-N3c)
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+}  // namespace
+}  // namespace daba
 
+extern "C" int daba_coarse_solve(const double* U, const double* gc, const double* V, const double* gl, const double* W,
+                                 const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M,
+                                 int64_t N, int64_t K, double xi, double mu, int max_iter, double tol, double* dc,
+                                 double* dl, double* work, double info[2], void* stream) {
+  using namespace daba;
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(xi >= 0) || !(mu >= 0) || max_iter < 0 || !(tol >= 0) || !info)
+    return -1;
+  if ((M > 0 && (!U || !gc || !cam_off || !dc || !work)) || (N > 0 && (!V || !gl || !dl || !work)) ||
+      (K > 0 && (!W || !obs_cam || !obs_pt)))
+    return -1;
+  WSrc ws{W, nullptr, nullptr, nullptr, 0, 1.0, 0.0};
+  return coarse_solve_impl(U, gc, V, gl, ws, obs_cam, obs_pt, cam_off, M, N, K, xi, mu, max_iter, tol, dc, dl, work,
+                           info, stream);
+}
+
+namespace daba {
+cudaMemPool_t shared_pool(int device);  // engine.cu: the process-wide retained pool
+}
 extern "C" int daba_coarse_blocks(const double*, int64_t, const double*, int64_t, const int32_t*, const double*,
                                   const int64_t*, int64_t, int, double, double, double*, double*, double*, double*,
                                   double*, double*, void*);
@@ -685,7 +743,7 @@ int run_F(const Run& R, const double* c, const double* l, const double* ch, cons
 int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
             int* trial) {
   int rc = daba_coarse_blocks(ca, R.M, la, R.N, R.op, reinterpret_cast<const double*>(R.uv), R.off, R.K, R.loss,
-                              R.scale, R.eps, R.U, R.gc, R.V, R.gl, R.W, R.Fc, R.st);
+                              R.scale, R.eps, R.U, R.gc, R.V, R.gl, nullptr, R.Fc, R.st);  // W recomputed in the PCG
   if (rc) return rc;
   double E0;
   if ((rc = run_F(R, ca, la, nullptr, nullptr, &E0))) return rc;
@@ -694,8 +752,9 @@ int lm_step(const Run& R, const double* ca, const double* la, double* co, double
   const unsigned g = (unsigned)((std::max(R.M, 3 * R.N) + 255) / 256);
   for (int tau = 0; tau < R.trials; ++tau, mu *= R.mu_up) {
     double info[2];
-    rc = daba_coarse_solve(R.U, R.gc, R.V, R.gl, R.W, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter,
-                           R.pcg_tol, R.dcv, R.dlv, R.work, info, R.st);
+    const WSrc ws{nullptr, ca, la, R.uv, R.loss, R.scale, R.eps2};
+    rc = coarse_solve_impl(R.U, R.gc, R.V, R.gl, ws, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter, R.pcg_tol,
+                           R.dcv, R.dlv, R.work, info, R.st);
     if (rc == -6) continue;  // a damped block not positive definite: a failed trial
     if (rc) return rc;
     if (g) k_cr_retract<<<g, 256, 0, R.st>>>(ca, la, R.dcv, R.dlv, R.M, R.N, ct, lt);
@@ -734,10 +793,16 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
         mu0, mu_up, lm_trials, pcg_max_iter, pcg_tol};
   R.st = static_cast<cudaStream_t>(stream);
   const size_t nc = (size_t)M * 15, nl = (size_t)N * 3;
-  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9) + (size_t)N * (9 + 3 + 3) + (size_t)K * 27 +
+  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9) + (size_t)N * (9 + 3 + 3) +
                        (size_t)daba_coarse_solve_workspace(M, N) + 8;
   double* base = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), R.st) != cudaSuccess) return -5;
+  // scratch from the retained pool: mapping ~1.6 GB afresh on every call (Final-13682) cost more than an iteration
+  int device = 0;
+  cudaGetDevice(&device);
+  cudaMemPool_t pool = shared_pool(device);
+  if ((pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, R.st)
+            : cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), R.st)) != cudaSuccess)
+    return -5;
   double* o = base;
   auto take = [&](size_t n) { double* p = o; o += n; return p; };
   double *cp = take(nc), *lp = take(nl), *cb = take(nc), *lb = take(nl), *ca = take(nc), *la = take(nl),
@@ -749,7 +814,7 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
   R.V = take((size_t)N * 9);
   R.gl = take((size_t)N * 3);
   R.dlv = take((size_t)N * 3);
-  R.W = take((size_t)K * 27);
+  R.W = nullptr;
   R.work = take((size_t)daba_coarse_solve_workspace(M, N));
   R.scal = take(8);
   int rc = 0;

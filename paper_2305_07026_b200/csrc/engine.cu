@@ -1265,3 +1265,8 @@ extern "C" void daba_destroy(daba_ctx* ctx) {
   if (ctx->ev_join0) cudaEventDestroy(ctx->ev_join0);
   delete ctx;
 }
+
+// The same retained pool for the stateless NEXT-3 entry points (coarse.cu).
+namespace daba {
+cudaMemPool_t shared_pool(int device) { return context_pool(device); }
+}  // namespace daba
