@@ -167,3 +167,37 @@ def test_missing_extension_fails_loudly(tmp_path):
             "try:\n    D.lib()\nexcept ImportError as e:\n    print('raised', e)\n")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
     assert "raised" in out.stdout and "missing" in out.stdout, out.stdout + out.stderr
+
+
+def test_coarse_entry_points_reject_bad_arguments():
+    """include/daba.h NEXT-3 calls: invalid sizes, NULL buffers and unknown losses return DABA_E_INVALID_ARG (-1)
+    before any CUDA call (so this runs without a GPU)."""
+    L = D.lib()
+    dummy = np.zeros(64)
+    p = dummy.ctypes.data
+    # daba_coarse_blocks(cams, M, pts, N, obs_pt, obs_uv, cam_off, K, loss, scale, eps, U, gc, V, gl, W, F, stream)
+    assert L.daba_coarse_blocks(p, -1, p, 1, p, p, p, 1, 0, 1.0, 1e-8, p, p, p, p, p, p, None) == -1
+    assert L.daba_coarse_blocks(p, 1, p, 1, p, p, p, 1, 3, 1.0, 1e-8, p, p, p, p, p, p, None) == -1   # loss
+    assert L.daba_coarse_blocks(p, 1, p, 1, p, p, p, 1, 0, 0.0, 1e-8, p, p, p, p, p, p, None) == -1   # scale
+    assert L.daba_coarse_blocks(None, 1, p, 1, p, p, p, 1, 0, 1.0, 1e-8, p, p, p, p, p, p, None) == -1
+    assert L.daba_coarse_blocks(p, 1, p, 1, None, p, p, 1, 0, 1.0, 1e-8, p, p, p, p, p, p, None) == -1
+    assert L.daba_coarse_solve_workspace(-1, 0) == -1
+    assert L.daba_coarse_solve_workspace(2, 3) > 0
+    info = np.zeros(2)
+    args = [p, p, p, p, p, p, p, p, 1, 1, 1, 1e-4, 1e-3, 10, 1e-12, p, p, p, info.ctypes.data, None]
+    bad = list(args)
+    bad[12] = -1.0  # mu
+    assert L.daba_coarse_solve(*bad) == -1
+    bad = list(args)
+    bad[18] = None  # info
+    assert L.daba_coarse_solve(*bad) == -1
+    bad = list(args)
+    bad[4] = None  # W with K > 0
+    assert L.daba_coarse_solve(*bad) == -1
+    # daba_coarse_run(cams, M, pts, N, oc, op, uv, off, K, loss, scale, eps, xi, eta, mu0, mu_up, trials, acc,
+    #                 pcg_iter, pcg_tol, n_iters, trace, stream)
+    run = [p, 1, p, 1, p, p, p, p, 1, 0, 1.0, 1e-8, 1e-4, 0.1, 1e-3, 10.0, 5, 1, 10, 1e-10, 1, None, None]
+    for idx, v in ((12, 0.0), (13, 0.0), (13, 1.5), (15, 0.5), (16, 0), (18, 0), (20, -1), (9, 7)):
+        bad = list(run)
+        bad[idx] = v
+        assert L.daba_coarse_run(*bad) == -1, idx
