@@ -649,33 +649,54 @@ __global__ void __launch_bounds__(kCoarseThreads) k_cr_F(const double* __restric
   }
 }
 
-// out = sum_i Fc[i] + xi/2 (|c - c_hat|^2 + |l - l_hat|^2), one block, fixed order (c_hat == nullptr: no prox term)
-__global__ void __launch_bounds__(1024) k_cr_eval(const double* Fc, int64_t M, const double* c, const double* ch,
-                                                  int64_t N, const double* l, const double* lh, double xi, double* out) {
-  double F = 0.0, d = 0.0;
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) F += Fc[i];
-  if (ch) {
-    for (int64_t e = threadIdx.x; e < 15 * M; e += blockDim.x) d += (c[e] - ch[e]) * (c[e] - ch[e]);
-    for (int64_t e = threadIdx.x; e < 3 * N; e += blockDim.x) d += (l[e] - lh[e]) * (l[e] - lh[e]);
-  }
-  __shared__ double sF[32], sd[32];
+// out = sum_i Fc[i] + xi/2 (|c - c_hat|^2 + |l - l_hat|^2) (c_hat == nullptr: no prox term), fixed order: per-block
+// partials over grid-stride ranges, then one block adds them (a single 1024-thread block took 1.8 ms at Final-13682)
+constexpr int kEvalBlocks = 296;
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* sa, double* sb) {
   for (int off = 16; off > 0; off >>= 1) {
-    F += __shfl_down_sync(0xffffffffu, F, off);
-    d += __shfl_down_sync(0xffffffffu, d, off);
+    a += __shfl_down_sync(0xffffffffu, a, off);
+    b += __shfl_down_sync(0xffffffffu, b, off);
   }
   if ((threadIdx.x & 31) == 0) {
-    sF[threadIdx.x >> 5] = F;
-    sd[threadIdx.x >> 5] = d;
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
+    a = b = 0.0;
     for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) {
-      a += sF[w];
-      b += sd[w];
+      a += sa[w];
+      b += sb[w];
     }
-    *out = a + 0.5 * xi * b;
   }
+}
+
+__global__ void __launch_bounds__(256) k_cr_eval_part(const double* Fc, int64_t M, const double* c, const double* ch,
+                                                      int64_t N, const double* l, const double* lh, double* part) {
+  double F = 0.0, d = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < M; i += stride) F += Fc[i];
+  if (ch) {
+    for (int64_t e = t0; e < 15 * M; e += stride) d += (c[e] - ch[e]) * (c[e] - ch[e]);
+    for (int64_t e = t0; e < 3 * N; e += stride) d += (l[e] - lh[e]) * (l[e] - lh[e]);
+  }
+  __shared__ double sF[8], sd[8];
+  block_sum2(F, d, sF, sd);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = F;
+    part[2 * blockIdx.x + 1] = d;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cr_eval_final(const double* part, int nb, double xi, double* out) {
+  double F = 0.0, d = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    F += part[2 * b];
+    d += part[2 * b + 1];
+  }
+  __shared__ double sF[8], sd[8];
+  block_sum2(F, d, sF, sd);
+  if (threadIdx.x == 0) *out = F + 0.5 * xi * d;
 }
 
 // x-bar (eqs. nesterov_x): R through ProjRot3D (eq. proj_rot3d), t, d, l linear
@@ -733,7 +754,8 @@ int run_F(const Run& R, const double* c, const double* l, const double* ch, cons
     else
       k_cr_F<kTrivial><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
   }
-  k_cr_eval<<<1, 1024, 0, R.st>>>(R.Fc, R.M, c, ch, R.N, l, lh, R.xi, R.scal);
+  k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, c, ch, R.N, l, lh, R.scal + 8);
+  k_cr_eval_final<<<1, 256, 0, R.st>>>(R.scal + 8, kEvalBlocks, R.xi, R.scal);
   if (cudaMemcpyAsync(out, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess) return -3;
   return cudaStreamSynchronize(R.st) == cudaSuccess ? 0 : -3;
 }
@@ -794,7 +816,7 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
   R.st = static_cast<cudaStream_t>(stream);
   const size_t nc = (size_t)M * 15, nl = (size_t)N * 3;
   const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9) + (size_t)N * (9 + 3 + 3) +
-                       (size_t)daba_coarse_solve_workspace(M, N) + 8;
+                       (size_t)daba_coarse_solve_workspace(M, N) + 8 + 2 * kEvalBlocks;
   double* base = nullptr;
   // scratch from the retained pool: mapping ~1.6 GB afresh on every call (Final-13682) cost more than an iteration
   int device = 0;
@@ -816,7 +838,7 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
   R.dlv = take((size_t)N * 3);
   R.W = nullptr;
   R.work = take((size_t)daba_coarse_solve_workspace(M, N));
-  R.scal = take(8);
+  R.scal = take(8 + 2 * kEvalBlocks);
   int rc = 0;
   // x^{-1} = x^0 (eq. Fainit); F-bar^{-1} = F(x^0) (A18, global form); s^0 = 1
   if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
