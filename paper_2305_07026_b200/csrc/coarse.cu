@@ -269,6 +269,22 @@ __device__ __forceinline__ void get_W(const WSrc& s, int64_t k, const double* ca
     for (int c = 0; c < 3; ++c) Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
 }
 
+// J_c, J_l and w of observation k at the anchor (false: degenerate pair, contributes nothing) -- for the W-free
+// products w J_l^T (J_c v) and w J_c^T (J_l u), which never hold W (fewer live registers than get_W).
+__device__ __forceinline__ bool get_J(const WSrc& s, int64_t k, const double* cam, int32_t j, double Jc[27],
+                                      double Jl[9], double* w) {
+  const double l[3] = {s.pts[3 * (size_t)j], s.pts[3 * (size_t)j + 1], s.pts[3 * (size_t)j + 2]};
+  double r[3];
+  if (!pair_jacobians(cam, l, s.uv[k], s.eps2, r, Jc, Jl)) return false;
+  const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+  const double d2 = s.delta * s.delta, id2 = 1.0 / d2;
+  double rho;
+  *w = s.loss == kHuber    ? loss_eval<kHuber, false>(sh, s.delta, d2, id2, &rho)
+       : s.loss == kCauchy ? loss_eval<kCauchy, false>(sh, s.delta, d2, id2, &rho)
+                           : 1.0;
+  return true;
+}
+
 __global__ void k_cs_points(const double* __restrict__ V, const double* __restrict__ gl, int64_t N, double xi,
                             double mu, CS w, int* bad) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -386,9 +402,21 @@ __global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
   const int32_t i = obs_cam[k], j = obs_pt[k];
-  double Wk[27];
-  get_W(ws, k, ws.cams ? ws.cams + 15 * (size_t)i : nullptr, j, Wk);
   const double* vi = v + 9 * (size_t)i;
+  if (!ws.W) {  // w J_l^T (J_c v)
+    double Jc[27], Jl[9], w;
+    if (!get_J(ws, k, ws.cams + 15 * (size_t)i, j, Jc, Jl, &w)) return;
+    double y[3];
+    for (int r = 0; r < 3; ++r) {
+      double x = 0.0;
+      for (int a = 0; a < 9; ++a) x += Jc[9 * r + a] * vi[a];
+      y[r] = w * x;
+    }
+    for (int c = 0; c < 3; ++c) atomicAdd(t + 3 * (size_t)j + c, Jl[c] * y[0] + Jl[3 + c] * y[1] + Jl[6 + c] * y[2]);
+    return;
+  }
+  double Wk[27];
+  get_W(ws, k, nullptr, j, Wk);
   for (int c = 0; c < 3; ++c) {
     double x = 0.0;
     for (int a = 0; a < 9; ++a) x += Wk[3 * a + c] * vi[a];
@@ -397,7 +425,7 @@ __global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
 }
 
 // q_i = U'_i p_i - sum_{k of i} W_k V'^-1 t_j ; s[PQ] += p.q
-__global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __restrict__ U, WSrc ws,
+__global__ void __launch_bounds__(kCoarseThreads, 4) k_cs_pass2(const double* __restrict__ U, WSrc ws,
                                                              const int32_t* __restrict__ obs_pt,
                                                              const int64_t* __restrict__ cam_off, double xi, double mu,
                                                              CS w) {
@@ -415,6 +443,15 @@ __global__ void __launch_bounds__(kCoarseThreads) k_cs_pass2(const double* __res
     const double* tj = w.t + 3 * (size_t)j;
     double u[3];
     for (int c = 0; c < 3; ++c) u[c] = Vi[3 * c] * tj[0] + Vi[3 * c + 1] * tj[1] + Vi[3 * c + 2] * tj[2];
+    if (!ws.W) {  // w J_c^T (J_l u)
+      double Jc[27], Jl[9], w;
+      if (!get_J(ws, k, scam, j, Jc, Jl, &w)) continue;
+      double y[3];
+      for (int r = 0; r < 3; ++r) y[r] = w * (Jl[3 * r] * u[0] + Jl[3 * r + 1] * u[1] + Jl[3 * r + 2] * u[2]);
+#pragma unroll
+      for (int a = 0; a < 9; ++a) acc[a] += Jc[a] * y[0] + Jc[9 + a] * y[1] + Jc[18 + a] * y[2];
+      continue;
+    }
     double Wk[27];
     get_W(ws, k, scam, j, Wk);
 #pragma unroll
