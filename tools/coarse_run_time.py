@@ -16,8 +16,8 @@ from tools.coarse_common import bal_to_native, camera_sorted  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "venice1778_1m"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-pcg = int(sys.argv[3]) if len(sys.argv) > 3 else 50
-tol = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-6
+pcg = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+tol = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-2
 p = gen.generate(cfg)
 order, off = camera_sorted(p)
 dev = torch.device("cuda:0")
@@ -54,4 +54,14 @@ s2.close()
 s.close()
 F_end = float(daba.coarse_blocks(cams, pts, args[1], args[2], args[3], loss=p.loss, scale=p.loss_scale)[5].sum())
 res["coarse"]["F"][-1] = F_end
+res["coarse"]["time_s"] = n * res["coarse"]["ms_per_iter"] / 1e3
+# time to the coarse run's final accuracy on the finest partition: first k with F(x^k) <= F_end
+s3 = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, loss=p.loss, loss_scale=p.loss_scale)
+cap = int(os.environ.get("FINEST_CAP", "3000"))
+Ftr, _ = s3.iterate(cap, F_trace=True)
+s3.close()
+hit = np.flatnonzero(np.asarray(Ftr) <= F_end)
+k = int(hit[0]) if hit.size else None
+res["finest"]["iters_to_coarse_F"] = k
+res["finest"]["time_s_to_coarse_F"] = None if k is None else k * res["finest"]["ms_per_iter"] / 1e3
 print(json.dumps(res))
