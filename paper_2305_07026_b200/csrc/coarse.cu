@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <math.h>
 
 #include <algorithm>
 
@@ -806,13 +807,22 @@ int run_F(const Run& R, const double* c, const double* l, const double* ch, cons
 
 // One successful LM step on E(. | anchor) = F + xi/2 |. - anchor|^2 from the anchor (R-N3c); out = the accepted
 // trial or the anchor.  *trial = accepted trial index or -1.
+// E0_known: E(anchor | anchor) = F(anchor) if the caller has it (the x^k anchor: F(x^k)), else NaN — then it is
+// summed from the blocks kernel's per-camera F.  *E_out: E of the accepted trial (E0 if none), i.e. E(x_new | anchor).
 int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
-            int* trial) {
+            int* trial, double E0_known, double* E_out) {
   int rc = daba_coarse_blocks(ca, R.M, la, R.N, R.op, reinterpret_cast<const double*>(R.uv), R.off, R.K, R.loss,
                               R.scale, R.eps, R.U, R.gc, R.V, R.gl, nullptr, R.Fc, R.st);  // W recomputed in the PCG
   if (rc) return rc;
-  double E0;
-  if ((rc = run_F(R, ca, la, nullptr, nullptr, &E0))) return rc;
+  double E0 = E0_known;
+  if (!(E0 == E0)) {  // NaN: sum the anchor's per-camera F written by the blocks kernel
+    k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, nullptr, nullptr, R.N, nullptr, nullptr, R.scal + 8);
+    k_cr_eval_final<<<1, 256, 0, R.st>>>(R.scal + 8, kEvalBlocks, R.xi, R.scal);
+    if (cudaMemcpyAsync(&E0, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess ||
+        cudaStreamSynchronize(R.st) != cudaSuccess)
+      return -3;
+  }
+  *E_out = E0;
   *trial = -1;
   double mu = R.mu0;
   const unsigned g = (unsigned)((std::max(R.M, 3 * R.N) + 255) / 256);
@@ -828,6 +838,7 @@ int lm_step(const Run& R, const double* ca, const double* la, double* co, double
     if ((rc = run_F(R, ct, lt, ca, la, &E))) return rc;
     if (E - E0 < 0) {
       *trial = tau;
+      *E_out = E;
       break;
     }
   }
@@ -899,10 +910,10 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
     int ta, tm;
     if ((rc = run_F(R, cams, pts, nullptr, nullptr, &Fk))) break;
     Fbar = (1.0 - eta) * Fbar + eta * Fk;  // eq. lFak
-    if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, &ta))) break;      // eq. update_amm
-    if ((rc = lm_step(R, cams, pts, cm, lm, ct, lt, &tm))) break;   // eq. update_mm
-    if ((rc = run_F(R, ca, la, cams, pts, &Eacc))) break;           // E(x_acc | x^k), eq. Eak
-    if ((rc = run_F(R, cm, lm, cams, pts, &Emm))) break;
+    double Ebar;
+    if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, &ta, NAN, &Ebar))) break;  // eq. update_amm
+    if ((rc = lm_step(R, cams, pts, cm, lm, ct, lt, &tm, Fk, &Emm))) break;  // eq. update_mm; Emm = E(x_mm | x^k)
+    if ((rc = run_F(R, ca, la, cams, pts, &Eacc))) break;                   // E(x_acc | x^k), eq. Eak
     const bool restart = accelerate ? (Eacc > Fbar) : true;         // Alg. 1, strict ">"
     if (trace) {
       double* t = trace + 5 * (size_t)it;
