@@ -151,3 +151,28 @@ def test_coarse_run_one_device_matches_the_oracle(loss, eta):
     assert np.abs(c - c_ref).max() <= 1e-7 * np.abs(c_ref).max()
     assert np.abs(l - l_ref).max() <= 1e-7 * np.abs(l_ref).max()
     assert tr[-1, 0] < tr[0, 0]
+
+
+@pytest.mark.parametrize("eta", [0.1, 1.0])
+def test_coarse_run_inexact_solve_keeps_the_mm_invariants(eta):
+    """The timed configuration (PCG capped at a few iterations) is a different, inexact iterate sequence, so it is
+    checked by what holds for any accepted LM step: E(x_mm | x^k) <= F(x^k) (accepted only on a decrease),
+    E(x_acc | x^k) <= F-bar^k when not restarted (Alg. 1), and F(x^{k+1}) <= E(x^{k+1} | x^k) (Prop. 2)."""
+    import paper_2305_07026_b200 as daba
+    p = gen.generate("small_cauchy", K=3001, N=700, M=29)
+    cp = coarse.Problem(p, np.zeros(p.M, int), np.zeros(p.N, int))
+    dev = torch.device("cuda:0")
+    order = np.argsort(cp.oc, kind="stable")
+    cam_off = np.concatenate([[0], np.cumsum(np.bincount(cp.oc, minlength=cp.M))]).astype(np.int64)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
+    cams, pts = t(cp.cams0, torch.float64), t(cp.pts0, torch.float64)
+    tr = daba.coarse_run(cams, pts, t(cp.oc[order], torch.int32), t(cp.op[order], torch.int32),
+                         t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 12, loss=cp.opt.kind,
+                         scale=cp.opt.scale, eta=eta, pcg_max_iter=3, pcg_tol=1e-2)
+    F, Fbar, Eacc, rs, Emm = tr.T
+    rel = 1e-12
+    assert np.all(Emm <= F * (1 + rel))
+    assert np.all(Eacc[rs == 0] <= Fbar[rs == 0] * (1 + rel))
+    Esel = np.where(rs == 1, Emm, Eacc)
+    assert np.all(F[1:] <= Esel[:-1] * (1 + rel))
+    assert F[-1] < F[0]
