@@ -176,3 +176,37 @@ def test_coarse_run_inexact_solve_keeps_the_mm_invariants(eta):
     Esel = np.where(rs == 1, Emm, Eacc)
     assert np.all(F[1:] <= Esel[:-1] * (1 + rel))
     assert F[-1] < F[0]
+
+
+def test_coarse_run_isolated_camera_and_point():
+    """A camera and a point without observations (degenerate cases of the method): their gradient is zero and only
+    the proximal term acts on them, so they do not move (beyond ProjRot3D's rounding), and the rest of the run is
+    the run without them."""
+    import paper_2305_07026_b200 as daba
+    p = gen.generate("tiny_seq", loss=oracle.LOSS_HUBER, outlier_frac=0.05)
+    cp = coarse.Problem(p, np.zeros(p.M, int), np.zeros(p.N, int))
+    dev = torch.device("cuda:0")
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
+    order = np.argsort(cp.oc, kind="stable")
+
+    def run(cams0, pts0, M):
+        off = np.concatenate([[0], np.cumsum(np.bincount(cp.oc, minlength=M))]).astype(np.int64)
+        c, l = t(cams0, torch.float64), t(pts0, torch.float64)
+        tr = daba.coarse_run(c, l, t(cp.oc[order], torch.int32), t(cp.op[order], torch.int32),
+                             t(cp.uv[order], torch.float64), t(off, torch.int64), 5, loss=cp.opt.kind,
+                             scale=cp.opt.scale, pcg_max_iter=2000, pcg_tol=1e-15)
+        return tr, c.cpu().numpy(), l.cpu().numpy()
+
+    tr0, c0, l0 = run(cp.cams0, cp.pts0, cp.M)
+    extra_cam = cp.cams0[:1].copy()
+    extra_cam[0, 9:12] += 3.0
+    cams = np.vstack([cp.cams0, extra_cam])
+    pts = np.vstack([cp.pts0, [[1.0, 2.0, 3.0]]])
+    tr1, c1, l1 = run(cams, pts, cp.M + 1)
+    np.testing.assert_array_equal(tr1[:, 3], tr0[:, 3])
+    np.testing.assert_allclose(tr1[:, [0, 1, 2, 4]], tr0[:, [0, 1, 2, 4]], rtol=1e-11)
+    np.testing.assert_allclose(c1[:-1], c0, rtol=0, atol=1e-9 * np.abs(c0).max())
+    np.testing.assert_allclose(l1[:-1], l0, rtol=0, atol=1e-9 * np.abs(l0).max())
+    # unchanged up to the rounding of ProjRot3D in the extrapolation (x-bar of a variable with x^k = x^{k-1})
+    np.testing.assert_allclose(c1[-1], cams[-1], rtol=0, atol=1e-13 * np.abs(cams[-1]).max())
+    np.testing.assert_array_equal(l1[-1], pts[-1])
