@@ -82,6 +82,10 @@ def lib():
         L.orc_proj_rot3d.restype = None
         L.orc_schedule.argtypes = [ctypes.c_double, _dp, _dp]
         L.orc_schedule.restype = None
+        L.orc_extrapolate_camera.argtypes = [V, V, ctypes.c_double, V]
+        L.orc_extrapolate_camera.restype = None
+        L.orc_extrapolate_point.argtypes = [V, V, ctypes.c_double, V]
+        L.orc_extrapolate_point.restype = None
         L.orc_expmap.argtypes = [V, V]
         L.orc_expmap.restype = None
         L.orc_bal_to_native.argtypes = [V, V]
@@ -167,6 +171,22 @@ def schedule(s):
     sn, g = ctypes.c_double(), ctypes.c_double()
     lib().orc_schedule(s, ctypes.byref(sn), ctypes.byref(g))
     return sn.value, g.value
+
+
+def extrapolate_camera(c, cp, gamma):
+    """x-bar of one native camera (eqs. nesterov_R/t/d)."""
+    c, cp = _a(c), _a(cp)
+    out = np.empty(15)
+    lib().orc_extrapolate_camera(c.ctypes.data, cp.ctypes.data, gamma, out.ctypes.data)
+    return out
+
+
+def extrapolate_point(l, lp, gamma):
+    """x-bar of one point (eq. nesterov_l)."""
+    l, lp = _a(l), _a(lp)
+    out = np.empty(3)
+    lib().orc_extrapolate_point(l.ctypes.data, lp.ctypes.data, gamma, out.ctypes.data)
+    return out
 
 
 def expmap(w):

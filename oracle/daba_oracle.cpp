@@ -621,6 +621,18 @@ void extrapolate_camera(const double* c, const double* cp, double gamma, double*
 void extrapolate_point(const double* l, const double* lp, double gamma, double* out) {
   for (int k = 0; k < 3; ++k) out[k] = l[k] + gamma * (l[k] - lp[k]);
 }
+}  // namespace
+
+// The two extrapolations above, exported for their pins (tests/test_oracle_iteration.py: closed-form worked values
+// of eqs. nesterov_R/t/d/l).
+extern "C" void orc_extrapolate_camera(const double c[15], const double cp[15], double gamma, double out[15]) {
+  extrapolate_camera(c, cp, gamma, out);
+}
+extern "C" void orc_extrapolate_point(const double l[3], const double lp[3], double gamma, double out[3]) {
+  extrapolate_point(l, lp, gamma, out);
+}
+
+namespace {
 
 double objective(const orc_ctx* h, const double* cams, const double* pts, int64_t* ndegen) {
   // eq. Fobj: F(x) = sum over E of F_ij; degenerate pairs contribute nothing (Q17)

@@ -53,6 +53,10 @@ double orc_Q(double a, double w, double lambda, const double g[3], const double 
 /* ---- acceleration (§5) ---- */
 void orc_proj_rot3d(const double M[9], double R[9]);                                       /* eq. proj_rot3d */
 void orc_schedule(double s, double* s_next, double* gamma);                                /* eq. nesterov_scalar */
+/* x-bar from x^k (c, l) and x^{k-1} (cp, lp): eqs. nesterov_R/t/d (ProjRot3D of the extrapolated R) and
+ * nesterov_l */
+void orc_extrapolate_camera(const double c[15], const double cp[15], double gamma, double out[15]);
+void orc_extrapolate_point(const double l[3], const double lp[3], double gamma, double out[3]);
 void orc_expmap(const double w[3], double R[9]);
 void orc_bal_to_native(const double bal[9], double cam[15]);
 void orc_native_to_bal(const double cam[15], double bal[9]);

@@ -188,3 +188,111 @@ def test_convergence_to_critical_point():
     assert F[-1] < 1e-5 * F[0]
     assert g1 < 1e-4 * g0
     assert np.all(np.diff(tr[:, oracle.TR_FBAR]) <= 1e-12 * F[0])
+
+
+# ---------------------------------------------------------------- extrapolation (eqs. nesterov_R/t/d/l)
+import dataclasses
+import json
+import os
+
+EXTRAP = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_values.json")))["extrapolate"]
+
+
+def rz(a):
+    c, s = math.cos(a), math.sin(a)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
+@pytest.mark.parametrize("case", range(len(EXTRAP)))
+def test_camera_extrapolation_worked_value(case):
+    # tests/golden/worked_values.json "extrapolate": R^k = Rz(theta) R0, R^{k-1} = R0 -> x-bar rotation Rz(phi) R0
+    v = EXTRAP[case]
+    R0 = Rotation.from_rotvec([0.3, -1.1, 0.7]).as_matrix()
+    c, cp = np.zeros(15), np.zeros(15)
+    c[:9], cp[:9] = (rz(v["theta"]) @ R0).ravel(), R0.ravel()
+    c[9:12], cp[9:12] = v.get("t", [1.0, 2.0, 3.0]), v.get("t_prev", [1.0, 2.0, 3.0])
+    c[12:], cp[12:] = v.get("d", [800.0, 0.0, 0.0]), v.get("d_prev", [800.0, 0.0, 0.0])
+    out = oracle.extrapolate_camera(c, cp, v["gamma"])
+    np.testing.assert_allclose(out[:9].reshape(3, 3), rz(v["phi"]) @ R0, atol=2e-15)
+    if "t_bar" in v:
+        np.testing.assert_allclose(out[9:12], v["t_bar"], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(out[12:], v["d_bar"], rtol=1e-15)
+        # eq. nesterov_l, the same linear rule for a point
+        np.testing.assert_allclose(oracle.extrapolate_point(v["t"], v["t_prev"], v["gamma"]), v["t_bar"], atol=1e-15)
+
+
+def with_isolated(p):
+    """p plus one camera and one point that no observation touches (their subproblems are the proximal term
+    alone, minimised at the anchor: the accelerated candidate of each is x-bar itself)."""
+    cams = np.vstack([p.cams, p.cams[:1]])
+    pts = np.vstack([p.pts, p.pts[:1] + 1.0])
+    return dataclasses.replace(p, cams=cams, pts=pts)
+
+
+def isolated_setup(p, Rk, Rkm1, s=PHI):
+    """Oracle on p + isolated camera / point, x^k = x^0 except the isolated camera rotation Rk (x^{k-1}: Rkm1)
+    and the isolated point moved by (0.5, -0.25, 2); s^{(k)} = s, F-bar^{(k-1)} large (no restart)."""
+    q = with_isolated(p)
+    o = oracle.Oracle(q)
+    ck, lk = o.state(0)
+    ckm1, lkm1 = ck.copy(), lk.copy()
+    ck[-1, :9], ckm1[-1, :9] = np.ravel(Rk), np.ravel(Rkm1)
+    ck[-1, 9:12], ckm1[-1, 9:12] = [1.0, 2.0, 3.0], [0.5, 2.5, 3.0]
+    lkm1[-1] = lk[-1] - [0.5, -0.25, 2.0]
+    o.set_state(0, ck, lk)
+    o.set_state(1, ckm1, lkm1)
+    o.set_schedule(s, 1e30)
+    return o, ck, lk, ckm1, lkm1
+
+
+def test_isolated_camera_moves_by_its_extrapolation():
+    # Alg. 1 L407-414 on an isolated camera and point: no restart (F-bar huge), so x^{k+1} = x_acc = x-bar^k, and
+    # x-bar^k is fixed in closed form by the worked value (gamma_1 from s = phi)
+    v = EXTRAP[0]
+    R0 = Rotation.from_rotvec([0.3, -1.1, 0.7]).as_matrix()
+    o, ck, lk, ckm1, lkm1 = isolated_setup(gen.generate("tiny_seq"), rz(v["theta"]) @ R0, R0)
+    tr = o.iterate(1)
+    assert tr[0, oracle.TR_RESTART] == 0
+    assert tr[0, oracle.TR_GAMMA] == pytest.approx(v["gamma"], abs=1e-12)
+    c1, l1 = o.state(0)
+    np.testing.assert_allclose(c1[-1, :9].reshape(3, 3), rz(v["phi"]) @ R0, atol=1e-14)
+    np.testing.assert_allclose(c1[-1, 9:12], v["t_bar"], atol=1e-14)
+    np.testing.assert_allclose(l1[-1], lk[-1] + v["gamma"] * np.array([0.5, -0.25, 2.0]), atol=1e-14)
+    # the other variables are unaffected by the isolated pair of variables: same iterate as without them
+    p = gen.generate("tiny_seq")
+    ref = oracle.Oracle(p)
+    ref.set_schedule(PHI, 1e30)
+    ref.iterate(1)
+    cr, lr = ref.state(0)
+    np.testing.assert_array_equal(c1[:-1], cr)
+    np.testing.assert_array_equal(l1[:-1], lr)
+
+
+def test_isolated_camera_extrapolation_with_negative_determinant():
+    # ProjRot3D's det < 0 case (eq. proj_rot3d, Q14) inside the iteration: R^k = R^{k-1} = U diag(3,2,-1/2) V^T
+    # (not a rotation, so only reachable through set_state) -> x-bar rotation = U V^T in closed form (the sign
+    # flip lands on the smallest singular direction)
+    U = Rotation.from_rotvec([0.2, 0.5, -0.4]).as_matrix()
+    V = Rotation.from_rotvec([-1.0, 0.3, 0.8]).as_matrix()
+    M = U @ np.diag([3.0, 2.0, -0.5]) @ V.T
+    assert np.linalg.det(M) < 0
+    o, *_ = isolated_setup(gen.generate("tiny_seq"), M, M)
+    tr = o.iterate(1)
+    assert tr[0, oracle.TR_RESTART] == 0
+    c1, _ = o.state(0)
+    np.testing.assert_allclose(c1[-1, :9].reshape(3, 3), U @ V.T, atol=1e-13)
+
+
+@pytest.mark.parametrize("loss", [oracle.LOSS_TRIVIAL, oracle.LOSS_HUBER])
+def test_acceleration_reaches_F_delta_sooner(loss):
+    # P:L612-613: DABA reaches F_Delta (eq. Fdelta P:L603-606, Delta = 2.5e-4 as in the tables' captions) in fewer
+    # iterations than its unaccelerated ablation DUBA; F_ref = the best F either reaches in 600 iterations
+    p = gen.generate("tiny_seq", loss=loss, outlier_frac=0.03 if loss else 0.0)
+    Fa = oracle.Oracle(p).iterate(600)[:, oracle.TR_F]
+    Fd = oracle.Oracle(p, accelerate=0).iterate(600)[:, oracle.TR_F]
+    Fref = min(Fa.min(), Fd.min())
+    Fdelta = Fref + 2.5e-4 * (Fa[0] - Fref)
+    ia = int(np.argmax(Fa <= Fdelta))
+    assert Fa[ia] <= Fdelta
+    idd = int(np.argmax(Fd <= Fdelta)) if (Fd <= Fdelta).any() else 10 ** 9
+    assert 2 * ia < idd, (ia, idd)
