@@ -275,6 +275,9 @@ int daba_bal_to_paper(double* cameras, int64_t M, double* obs_uv, int64_t K);
 /* The inverse map (round trip exact up to rounding). */
 int daba_paper_to_bal(double* cameras, int64_t M, double* obs_uv, int64_t K);
 
+/* Human-readable detail of ctx's last non-OK return; with ctx = NULL, why this thread's last daba_create failed
+ * (empty if it did not).  The string is owned by the library and valid until the next call on the same ctx /
+ * thread. */
 const char* daba_last_error(const daba_ctx* ctx);
 void daba_destroy(daba_ctx* ctx);
 

@@ -25,6 +25,9 @@
 
 using namespace daba;
 
+thread_local std::string g_create_err = "";  // why this thread's last daba_create failed
+thread_local int g_bail_line = 0;
+
 struct daba_ctx {
   std::string err;
   int device = 0, rank = 0, nranks = 1;
@@ -155,6 +158,34 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
   c->allocs.push_back(*p);
   c->dev_bytes += n * sizeof(T);
   return DABA_OK;
+}
+
+// Release one dalloc'd buffer before destroy (create-time buffers whose job is done).
+void dfree(daba_ctx* c, void* p, size_t bytes) {
+  if (!p) return;
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+  if (it == c->allocs.end()) return;
+  c->allocs.erase(it);
+  c->dev_bytes -= bytes;
+  if (c->pooled)
+    cudaFreeAsync(p, c->stream);
+  else
+    cudaFree(p);
+}
+
+// Create-time temporary device memory (stream-ordered from the context pool when there is one).
+void* talloc(daba_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  cudaMemPool_t pool = context_pool(c->device);
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, pool, c->stream) : cudaMalloc(&p, bytes ? bytes : 1);
+  return e == cudaSuccess ? p : nullptr;
+}
+void tfree(daba_ctx* c, void* p) {
+  if (!p) return;
+  if (context_pool(c->device))
+    cudaFreeAsync(p, c->stream);
+  else
+    cudaFree(p);
 }
 
 // Host -> device copy on the context's stream.  Small or page-locked sources go directly; large pageable ones
@@ -313,6 +344,25 @@ void collect_times(daba_ctx* c) {
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
+  if (P.pt_mode == 1) {
+    // point pass by recomputation: it reads only x^k and x-bar^k, so it runs beside the camera pass and the
+    // camera solve (parallel graph branches); profiling serialises so that events bracket one kernel
+    if (c->opt.profile || !c->fork1) {
+      n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
+      n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
+      n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
+      n += timed(c, "k_pt_pass", [&] { return launch_pt_recompute(P, c->stream); });
+    } else {
+      CUDA_OR(c, cudaEventRecord(c->ev_fork, c->stream));
+      CUDA_OR(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      n += launch_pt_recompute(P, c->side);
+      CUDA_OR(c, cudaEventRecord(c->ev_join, c->side));
+      n += launch_cam_pass(P, c->stream);
+      n += launch_inter(P, c->stream);
+      n += launch_cam_solve(P, c->stream);
+      CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    }
+  } else {
   if (!c->opt.profile && c->fork0 && (P.n_boundary > 0 || P.n_inter_blocks > 0)) {
     // the boundary records and the inter-device terms only read x^k, x-bar^k and the halo: a parallel branch
     // beside the camera pass
@@ -342,6 +392,7 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
     CUDA_OR(c, cudaEventRecord(c->ev_join, c->side));
     n += launch_pt_sum(P, c->stream);
     CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
   }
   if (c->comm) {
     const bool halo = !c->segs.empty();
@@ -596,8 +647,14 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
   }
   int rc = DABA_OK;
+  // a failed create leaves its reason for daba_last_error(NULL) (this thread)
   auto bail = [&](int code) {
+    std::string why = C->err;
+    const cudaError_t ce = cudaGetLastError();
+    if (why.empty()) why = code == DABA_E_CUDA ? std::string("CUDA: ") + cudaGetErrorString(ce) : "daba_create failed";
+    why += " (line " + std::to_string(g_bail_line) + ")";
     daba_destroy(c.release());
+    g_create_err = why;
     return code;
   };
   // light plan: decide on the device whether the input point numbering follows the cameras; if not, fall back
@@ -610,21 +667,21 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     IterParams& Q = C->P;
     Q.n_records = std::max<int64_t>(K, 1);
     if ((rc = dalloc(C, &Q.staging, 8 * (size_t)Q.n_records)) || (rc = dalloc(C, &d_opt, (size_t)Q.n_records)))
-      return bail(rc);
+      return g_bail_line = __LINE__, bail(rc);
     int32_t* d_ocam = reinterpret_cast<int32_t*>(Q.staging);
     if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
         h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess)
-      return bail(DABA_E_CUDA);
+      return g_bail_line = __LINE__, bail(DABA_E_CUDA);
     // scratch after the K camera ids: N int32 keys + a counter; with more points than the buffer holds (isolated
     // points) or no observations the check is skipped (nothing to gather, the numbering is kept)
     const bool fits = K > 0 && sizeof(int32_t) * ((size_t)K + 8 + (size_t)N) + 64 <= 64 * (size_t)Q.n_records;
     const int64_t jumps = fits ? count_point_jumps_device(d_ocam, d_opt, K, (int32_t)N, point_far,
                                                           Q.staging + ((size_t)K + 7) / 2, C->stream)
                                : 0;
-    if (jumps < 0) return bail(DABA_E_CUDA);
+    if (jumps < 0) return g_bail_line = __LINE__, bail(DABA_E_CUDA);
     if (point_order != 0 && jumps * 4 >= N && N > 1) {  // scattered numbering: full plan, renumbered
       std::string e2 = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, false);
-      if (!e2.empty()) return bail(DABA_E_INVALID_ARG);
+      if (!e2.empty()) return g_bail_line = __LINE__, bail(DABA_E_INVALID_ARG);
       order_owned_points(&C->plan, obs_cam, true);
       Q.staging = nullptr;  // (re-allocated at its final size by the full path; this one stays until destroy)
     }
@@ -636,6 +693,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   P.n_own_cams = S.n_own_cams;
   P.n_pts = (int32_t)S.pt_g.size();
   P.n_own_pts = S.n_own_pts;
+  P.pt_mode = (int32_t)env_int("DABA_PT_MODE", 0);  // 1: point pass by recomputation (no records; measured slower)
   P.loss = loss.kind;
   P.delta = loss.scale;
   P.delta2 = loss.scale * loss.scale;
@@ -649,19 +707,19 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   P.accelerate = o.accelerate ? 1 : 0;
   P.restart_scope = o.restart_scope;
   for (int r = 0; r < 4; ++r) {
-    if ((rc = dalloc(C, &P.cams[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
-    if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return bail(rc);
+    if ((rc = dalloc(C, &P.cams[r], (size_t)P.n_cams * kCamStride))) return g_bail_line = __LINE__, bail(rc);
+    if ((rc = dalloc(C, &P.pts[r], (size_t)P.n_pts))) return g_bail_line = __LINE__, bail(rc);
   }
-  for (int r = 0; r < 2; ++r)
-    if ((rc = dalloc(C, &P.cbarb[r], (size_t)P.n_cams * kCamStride))) return bail(rc);
-  if ((rc = dalloc(C, &P.counter, 1))) return bail(rc);
+  for (int r = 0; r < 3; ++r)
+    if ((rc = dalloc(C, &P.cbarb[r], (size_t)P.n_cams * kCamStride))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.counter, 1))) return g_bail_line = __LINE__, bail(rc);
   cudaMemsetAsync(P.counter, 0, sizeof(int32_t), C->stream);
   P.has_comm = C->comm ? 1 : 0;
-  for (int r = 0; r < 2; ++r)
-    if ((rc = dalloc(C, &P.lbar[r], (size_t)P.n_pts))) return bail(rc);
+  for (int r = 0; r < 3; ++r)
+    if ((rc = dalloc(C, &P.lbar[r], (size_t)P.n_pts))) return g_bail_line = __LINE__, bail(rc);
   {
-    std::vector<int32_t> roles = {0, 1, 2, 3, 0};
-    if ((rc = upload(C, &P.roles, roles))) return bail(rc);
+    std::vector<int32_t> roles = {0, 1, 2, 3, 0, 1, 2};
+    if ((rc = upload(C, &P.roles, roles))) return g_bail_line = __LINE__, bail(rc);
   }
   timer.mark("device, stream, comm");
   // camera side + chunks
@@ -671,9 +729,9 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     const size_t kc = light ? (size_t)K : S.c_obs.size();
     double2* duv;
     int32_t* dpt = d_opt;
-    if ((rc = dalloc(C, &duv, kc))) return bail(rc);
+    if ((rc = dalloc(C, &duv, kc))) return g_bail_line = __LINE__, bail(rc);
     if (!light) {
-      if ((rc = dalloc(C, &dpt, kc))) return bail(rc);
+      if ((rc = dalloc(C, &dpt, kc))) return g_bail_line = __LINE__, bail(rc);
       CUDA_OR(C, h2d(C, dpt, S.c_pt.data(), kc * sizeof(int32_t)));
     }
     if (S.cam_side_identity) {
@@ -708,13 +766,19 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     // one CTA per chunk for both anchors once the chunks fill the GPU four times over (6 CTAs per SM)
     P.cam_shared_ctas = (int32_t)env_int("DABA_CAM_SHARED", P.n_chunks >= 4 * 6 * C->num_sms ? 1 : 0);
     const CamChunk* dch;
-    if ((rc = upload(C, const_cast<CamChunk**>(&dch), chunks))) return bail(rc);
+    if ((rc = upload(C, const_cast<CamChunk**>(&dch), chunks))) return g_bail_line = __LINE__, bail(rc);
     P.chunks = dch;
     const int32_t* dcp;
-    if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return bail(rc);
+    if ((rc = upload(C, const_cast<int32_t**>(&dcp), cptr))) return g_bail_line = __LINE__, bail(rc);
     P.cam_chunk_ptr = dcp;
   }
   timer.mark("camera side");
+  // pt_mode 1 create-time temporaries: point-major cameras / pixels and the tile build's scratch
+  void* pt_tmp = nullptr;
+  size_t pt_tmp_bytes = 0;
+  int32_t* pm_cam = nullptr;
+  double2* pm_uv = nullptr;
+  char* pt_scratch = nullptr;
   // point side: records written by the camera pass at its observation index; boundary observations (camera
   // owned elsewhere) are recomputed into records n_cam_side + b
   std::vector<int32_t> bcam, bpt;
@@ -723,27 +787,45 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (S.point_side_deferred) {  // light plan: every point's records in camera order, sorted on the device
       int64_t* dptr;
       int32_t* dsrc;
-      if ((rc = dalloc(C, &dptr, (size_t)N + 1)) || (rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1))))
-        return bail(rc);
-      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, P.staging, 64 * (size_t)P.n_records,
-                                 C->stream) != 0)
-        return bail(DABA_E_CUDA);
+      if ((rc = dalloc(C, &dptr, (size_t)N + 1))) return g_bail_line = __LINE__, bail(rc);
+      // pt_mode 1: the record list is a temporary (input of the tile build), and the sort must leave the
+      // observations' cameras (d_ocam, the start of the staging buffer) intact
+      const size_t keep = P.pt_mode ? (4 * (size_t)K + 255) / 256 * 256 : 0;
+      if (P.pt_mode) {
+        pt_tmp_bytes = 20 * (size_t)K + 512 + point_tiles_scratch_bytes(K, (int32_t)N, (int32_t)M, (int32_t)(N / 64 + 2));
+        if (!(pt_tmp = talloc(C, 4 * (size_t)K + pt_tmp_bytes))) return g_bail_line = __LINE__, bail(DABA_E_OOM);
+        dsrc = static_cast<int32_t*>(pt_tmp);
+      } else if ((rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1)))) {
+        return g_bail_line = __LINE__, bail(rc);
+      }
+      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, reinterpret_cast<char*>(P.staging) + keep,
+                                 64 * (size_t)P.n_records - keep, C->stream) != 0)
+        return g_bail_line = __LINE__, bail(DABA_E_CUDA);
       P.p_ptr = dptr;
       P.p_src = dsrc;
+      if (P.pt_mode) {  // point-major cameras and pixels of the tile build
+        char* q = static_cast<char*>(pt_tmp) + (4 * (size_t)K + 255) / 256 * 256;
+        pm_cam = reinterpret_cast<int32_t*>(q);
+        pm_uv = reinterpret_cast<double2*>(q + (4 * (size_t)K + 255) / 256 * 256);
+        pt_scratch = q + (4 * (size_t)K + 255) / 256 * 256 + (16 * (size_t)K + 255) / 256 * 256;
+        launch_gather_i32(reinterpret_cast<const int32_t*>(P.staging), dsrc, K, pm_cam, C->stream);
+        launch_gather_d2(P.c_uv, dsrc, K, pm_uv, C->stream);
+        P.p_src = nullptr;
+      }
       P.n_cam_side = K;
       P.n_boundary = 0;
       const int32_t *d1, *d2;
       const double2* d4;
       if ((rc = upload(C, const_cast<int32_t**>(&d1), bcam)) || (rc = upload(C, const_cast<int32_t**>(&d2), bpt)) ||
           (rc = upload(C, const_cast<double2**>(&d4), buv)))
-        return bail(rc);
+        return g_bail_line = __LINE__, bail(rc);
       P.b_cam = d1;
       P.b_pt = d2;
       P.b_uv = d4;
     } else {
     const size_t kp = S.p_obs.size(), kc = S.c_obs.size();
     const int64_t* dptr;
-    if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return bail(rc);
+    if ((rc = upload(C, const_cast<int64_t**>(&dptr), S.pt_ptr))) return g_bail_line = __LINE__, bail(rc);
     P.p_ptr = dptr;
     hvec<int32_t> src(kp);
     if (S.cam_side_identity) {  // the camera-side index of observation o is o
@@ -772,12 +854,28 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.n_cam_side = (int64_t)kc;
     P.n_boundary = (int64_t)bcam.size();
     P.n_records = std::max<int64_t>(P.n_cam_side + P.n_boundary, 1);
-    if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
+    if (P.pt_mode) {  // no records: a scratch buffer (pixel residuals, state packing) and the tile build inputs
+      P.n_records = std::max<int64_t>(1, (std::max<int64_t>((int64_t)kc, 3 * (int64_t)S.pt_g.size()) + 7) / 8);
+      pt_tmp_bytes = 20 * kp + 512 + point_tiles_scratch_bytes((int64_t)kp, P.n_own_pts, P.n_cams, P.n_own_pts / 64 + 2);
+      if (!(pt_tmp = talloc(C, pt_tmp_bytes))) return g_bail_line = __LINE__, bail(DABA_E_OOM);
+      char* q = static_cast<char*>(pt_tmp);
+      pm_cam = reinterpret_cast<int32_t*>(q);
+      pm_uv = reinterpret_cast<double2*>(q + (4 * kp + 255) / 256 * 256);
+      pt_scratch = q + (4 * kp + 255) / 256 * 256 + (16 * kp + 255) / 256 * 256;
+      hvec<double2> uv(kp);
+      parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) uv[r] = make_double2(obs_uv[2 * S.p_obs[r]], obs_uv[2 * S.p_obs[r] + 1]);
+      });
+      CUDA_OR(C, h2d(C, pm_cam, S.p_cam.data(), kp * sizeof(int32_t)));
+      CUDA_OR(C, h2d(C, pm_uv, uv.data(), kp * sizeof(double2)));
+      CUDA_OR(C, cudaStreamSynchronize(C->stream));  // uv is freed at the end of this scope
+    }
+    if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return g_bail_line = __LINE__, bail(rc);
     const int32_t *d0, *d1, *d2;
     const double2* d4;
     if ((rc = upload(C, const_cast<int32_t**>(&d0), src)) || (rc = upload(C, const_cast<int32_t**>(&d1), bcam)) ||
         (rc = upload(C, const_cast<int32_t**>(&d2), bpt)) || (rc = upload(C, const_cast<double2**>(&d4), buv)))
-      return bail(rc);
+      return g_bail_line = __LINE__, bail(rc);
     P.p_src = d0;
     P.b_cam = d1;
     P.b_pt = d2;
@@ -809,7 +907,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       if ((rc = upload(C, const_cast<int32_t**>(&e0), ic)) || (rc = upload(C, const_cast<int32_t**>(&e1), ip)) ||
           (rc = upload(C, const_cast<int32_t**>(&e2), is)) || (rc = upload(C, const_cast<double2**>(&e3), iu)) ||
           (rc = dalloc(C, &P.inter_part, 2 * (size_t)std::max(P.n_inter_blocks, 1))))
-        return bail(rc);
+        return g_bail_line = __LINE__, bail(rc);
       P.i_cam = e0;
       P.i_pt = e1;
       P.i_sign = e2;
@@ -817,24 +915,85 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
     // point-pass grid: every thread a few points (grid-stride), at least 8 CTAs per SM's worth; measured on
     // Final-13682: 4.46M points 1184 -> 4352 CTAs -17 us, 0.58M points (8 ranks) 1184 better than 2264
+    if (P.pt_mode) {
+      // tile arrays of the point pass, built on the device from the point-major lists; the tiles themselves
+      // (consecutive points, <= kPtTileMax points and <= kPtTileObs observations) are cut on the host
+      const int64_t kp = P.p_ptr ? (S.point_side_deferred ? K : (int64_t)S.p_obs.size()) : 0;
+      std::vector<int64_t> hptr;
+      const int64_t* ptr_h = nullptr;
+      if (S.point_side_deferred) {
+        hptr.resize((size_t)P.n_own_pts + 1);
+        CUDA_OR(C, cudaMemcpyAsync(hptr.data(), P.p_ptr, hptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                   C->stream));
+        CUDA_OR(C, cudaStreamSynchronize(C->stream));
+        ptr_h = hptr.data();
+      } else {
+        ptr_h = S.pt_ptr.data();
+      }
+      std::vector<int32_t> pt0(1, 0);
+      for (int32_t j = 0; j < P.n_own_pts;) {
+        int32_t e = j + 1;
+        while (e < P.n_own_pts && e - j < kPtTileMax && ptr_h[e + 1] - ptr_h[j] <= kPtTileObs) ++e;
+        pt0.push_back(e);
+        j = e;
+      }
+      P.n_pt_tiles = (int32_t)pt0.size() - 1;
+      int64_t* toff;
+      const int32_t* tpt0;
+      int32_t* tcam;
+      double2* tuv;
+      uint16_t *tjl, *tpos;
+      const size_t kk = (size_t)std::max<int64_t>(kp, 1);
+      if ((rc = dalloc(C, &toff, pt0.size())) || (rc = upload(C, const_cast<int32_t**>(&tpt0), pt0)) ||
+          (rc = dalloc(C, &tcam, kk)) || (rc = dalloc(C, &tuv, kk)) || (rc = dalloc(C, &tjl, kk)) ||
+          (rc = dalloc(C, &tpos, kk)))
+        return bail(rc);
+      const size_t need = point_tiles_scratch_bytes(kp, P.n_own_pts, P.n_cams, P.n_pt_tiles);
+      size_t avail = pt_tmp_bytes + (S.point_side_deferred ? 4 * (size_t)K : 0) - (size_t)(pt_scratch - static_cast<char*>(pt_tmp));
+      void* extra = nullptr;
+      char* scr = pt_scratch;
+      if (avail < need) {  // (the tile count is known only now)
+        if (!(extra = talloc(C, need))) return bail(DABA_E_OOM);
+        scr = static_cast<char*>(extra);
+        avail = need;
+      }
+      const int b = build_point_tiles_device(pm_cam, pm_uv, P.p_ptr, P.n_own_pts, kp, P.n_cams, tpt0, P.n_pt_tiles,
+                                             tcam, tuv, tjl, tpos, toff, scr, avail, C->stream);
+      tfree(C, extra);
+      tfree(C, pt_tmp);
+      pt_tmp = nullptr;
+      if (b != 0) return bail(DABA_E_CUDA);
+      P.t_off = toff;
+      P.t_pt0 = tpt0;
+      P.t_cam = tcam;
+      P.t_uv = tuv;
+      P.t_jl = tjl;
+      P.t_pos = tpos;
+      if (S.point_side_deferred) {  // the staging buffer held the observations' cameras: now a small scratch
+        dfree(C, P.staging, 64 * (size_t)P.n_records);
+        P.n_records = std::max<int64_t>(1, (std::max<int64_t>(K, 3 * N) + 7) / 8);
+        if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
+      }
+    }
     const int32_t pt_cap = (int32_t)env_int(
         "DABA_PT_CAP", std::max<int64_t>(148 * 8, ((int64_t)P.n_own_pts + 4 * kPtPassThreads - 1) / (4 * kPtPassThreads)));
-    P.n_pt_blocks = std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, pt_cap));
+    P.n_pt_blocks = P.pt_mode ? std::max(1, std::min(P.n_pt_tiles, C->num_sms))
+                              : std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, pt_cap));
   }
   timer.mark("point side");
   // scratch
   P.n_cam_eval_blocks = (2 * P.n_own_cams + 127) / 128;  // k_cam_solve blocks
   P.trace_cap = 1024;
-  if ((rc = dalloc(C, &P.partial, (size_t)std::max(P.n_chunks, 1) * 2 * kPartialStride))) return bail(rc);
-  if ((rc = dalloc(C, &P.moments, (size_t)std::max(P.n_own_cams, 1) * 2 * kPartialStride))) return bail(rc);
-  if ((rc = dalloc(C, &P.dP_mm, (size_t)std::max(P.n_own_cams, 1)))) return bail(rc);
-  if ((rc = dalloc(C, &P.decisions, (size_t)std::max(P.n_own_cams, 1) * 2))) return bail(rc);
-  if ((rc = dalloc(C, &P.cam_part, (size_t)std::max(P.n_cam_eval_blocks, 1) * kCamEvalCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.pt_part, (size_t)std::max(P.n_pt_blocks, 1) * kPtCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.local, kGlobalCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.global, kGlobalCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return bail(rc);
-  if ((rc = dalloc(C, &P.sched, 8))) return bail(rc);
+  if ((rc = dalloc(C, &P.partial, (size_t)std::max(P.n_chunks, 1) * 2 * kPartialStride))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.moments, (size_t)std::max(P.n_own_cams, 1) * 2 * kPartialStride))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.dP_mm, (size_t)std::max(P.n_own_cams, 1)))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.decisions, (size_t)std::max(P.n_own_cams, 1) * 2))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.cam_part, (size_t)std::max(P.n_cam_eval_blocks, 1) * kCamEvalCols))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.pt_part, (size_t)std::max(P.n_pt_blocks, 1) * kPtCols))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.local, kGlobalCols))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.global, kGlobalCols))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.trace, (size_t)P.trace_cap * kTraceCols))) return g_bail_line = __LINE__, bail(rc);
+  if ((rc = dalloc(C, &P.sched, 8))) return g_bail_line = __LINE__, bail(rc);
   if (!C->comm) P.global = P.local;
   cudaMemsetAsync(P.decisions, 0xff, sizeof(int32_t) * 2 * std::max(P.n_own_cams, 1), C->stream);
   timer.mark("scratch");
@@ -879,10 +1038,10 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
         (rc = upload(C, &C->d_recv_cam, rcm)) || (rc = upload(C, &C->d_recv_pt, rpt)) ||
         (rc = upload(C, &C->d_send_cam_off, sco)) || (rc = upload(C, &C->d_send_pt_off, spo)) ||
         (rc = upload(C, &C->d_recv_cam_off, rco)) || (rc = upload(C, &C->d_recv_pt_off, rpo)))
-      return bail(rc);
+      return g_bail_line = __LINE__, bail(rc);
     if ((rc = dalloc(C, &C->d_sendbuf, (size_t)std::max<int64_t>(soff, 1))) ||
         (rc = dalloc(C, &C->d_recvbuf, (size_t)std::max<int64_t>(roff, 1))))
-      return bail(rc);
+      return g_bail_line = __LINE__, bail(rc);
     // global test: the solves write both candidates into the send slots themselves (no k_pack); per owned
     // variable the list of its slots
     if (P.restart_scope == 0 && !C->segs.empty()) {
@@ -903,7 +1062,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       const int64_t *a1, *a3;
       if ((rc = upload(C, const_cast<int32_t**>(&a0), cptr_s)) || (rc = upload(C, const_cast<int64_t**>(&a1), coff_s)) ||
           (rc = upload(C, const_cast<int32_t**>(&a2), pptr_s)) || (rc = upload(C, const_cast<int64_t**>(&a3), poff_s)))
-        return bail(rc);
+        return g_bail_line = __LINE__, bail(rc);
       P.cam_send_ptr = a0;
       P.cam_send_off = a1;
       P.pt_send_ptr = a2;
@@ -915,13 +1074,13 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // state: x^{-1} = x^0 (Alg. 1)
   {
     rc = upload_states(C, nat.data(), points, nat.data(), points, 1, 0);
-    if (rc) return bail(rc);
+    if (rc) return g_bail_line = __LINE__, bail(rc);
   }
   timer.mark("states");
   // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
   double F0 = 0, nd = 0;
-  if ((rc = compute_objective(C, &F0, &nd))) return bail(rc);
-  if (nd > 0) return bail(DABA_E_DEGENERATE);  // Assumption 2: ||l_j - t_i|| <= eps for some pair
+  if ((rc = compute_objective(C, &F0, &nd))) return g_bail_line = __LINE__, bail(rc);
+  if (nd > 0) return g_bail_line = __LINE__, bail(DABA_E_DEGENERATE);  // Assumption 2: ||l_j - t_i|| <= eps for some pair
   if (P.restart_scope == 1) {
     // eq. Fainit per device: F-bar^{a(-1)} = F^{a(-1)} = E^a(x^{a(0)} | x^{(0)}) = F_kappa(x^0): the rank's
     // camera-side F with its inter-device pairs at weight 1/2 (k_inter at x^{-1} = x^0); D^{a(-1)} = 0
@@ -930,21 +1089,21 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     double loc[kGlobalCols];
     if (cudaMemcpyAsync(loc, P.local, sizeof loc, cudaMemcpyDeviceToHost, C->stream) != cudaSuccess ||
         cudaStreamSynchronize(C->stream) != cudaSuccess)
-      return bail(DABA_E_CUDA);
+      return g_bail_line = __LINE__, bail(DABA_E_CUDA);
     F0 = loc[0] + loc[10];
   }
   {
     const double sched[8] = {1.0, F0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (cudaMemcpyAsync(P.sched, sched, sizeof sched, cudaMemcpyHostToDevice, C->stream) != cudaSuccess)
-      return bail(DABA_E_CUDA);
+      return g_bail_line = __LINE__, bail(DABA_E_CUDA);
     launch_lbar_all(P, C->stream);  // x-bar^0 = x^0 (gamma^{(0)} = 0)
-    if (cudaStreamSynchronize(C->stream) != cudaSuccess) return bail(DABA_E_CUDA);
+    if (cudaStreamSynchronize(C->stream) != cudaSuccess) return g_bail_line = __LINE__, bail(DABA_E_CUDA);
   }
   timer.mark("objective, x-bar");
   // launches per iteration (for bookkeeping)
   {
     const bool unpack = C->n_recv_cam + C->n_recv_pt > 0, dev = P.restart_scope == 1;
-    C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) +
+    C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0 && P.pt_mode == 0) +
                            (P.n_inter_blocks > 0) + (C->comm && (dev || !unpack) ? 1 : 0) +
                            (C->n_send_cam + C->n_send_pt > 0 && !P.sendbuf) + unpack;
   }
@@ -1241,7 +1400,7 @@ extern "C" int daba_reset_kernel_times(daba_ctx* ctx) {
 
 extern "C" int daba_launches_per_iteration(daba_ctx* ctx) { return ctx ? ctx->launches_per_iter : DABA_E_INVALID_ARG; }
 
-extern "C" const char* daba_last_error(const daba_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+extern "C" const char* daba_last_error(const daba_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 extern "C" void daba_destroy(daba_ctx* ctx) {
   if (!ctx) return;

@@ -321,7 +321,7 @@ class Solver:
                            co.ctypes.data if co is not None else None, po.ctypes.data if po is not None else None,
                            rank, nranks, key, device, ctypes.byref(self.opt), ctypes.byref(h))
         if rc:
-            raise DabaError(rc, "daba_create")
+            raise DabaError(rc, "daba_create: " + (L.daba_last_error(None) or b"").decode())
         self.h = h
         self.rank, self.nranks = rank, nranks
 

@@ -78,8 +78,10 @@ def test_fifty_iterations(name, eta):
     tro = o.iterate(50)
     with solver(p, eta=eta) as s:
         trg = s.iterate_trace(50)
-        rel = np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])
-        assert rel.max() <= F_TOL, (rel.max(), int(rel.argmax()))
+        # F, F-bar (eq. lFak), E(x_acc|x^k) and E(x_mm|x^k) (eq. Eak) every iteration
+        for col in (oracle.TR_F, oracle.TR_FBAR, oracle.TR_EACC, oracle.TR_EMM):
+            rel = np.abs(trg[:, col] - tro[:, col]) / np.abs(tro[:, col])
+            assert rel.max() <= F_TOL, (col, rel.max(), int(rel.argmax()))
         np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART], tro[:, oracle.TR_RESTART])
         cg, lg, _ = s.state_native(0)
         co, lo = o.state(0)
@@ -177,6 +179,46 @@ def test_isolated_cameras_and_points():
         trg = s.iterate_trace(6)
         assert np.abs(trg[:, 0] - tro[:, 0]).max() <= F_TOL * tro[0, 0]
         assert max(state_errors(*s.state_native(0)[:2], *o.state(0))) <= 1e-10
+
+
+@pytest.mark.parametrize("det_negative", [False, True])
+def test_isolated_camera_extrapolation(det_negative):
+    # An isolated camera and point move by exactly x-bar (their subproblems are the proximal term alone); with
+    # R^k = R^{k-1} = U diag(3, 2, -1/2) V^T the device ProjRot3D takes its det(M) <= 0 branch (eq. proj_rot3d,
+    # reading Q14), whose closed form is U V^T.  GPU = oracle for the whole iterate (tests/test_oracle_iteration.py
+    # pins the oracle's side in closed form).
+    from scipy.spatial.transform import Rotation
+    p = gen.generate("tiny_seq")
+    q = gen.Problem("iso_x", np.vstack([p.cams, p.cams[:1]]), np.vstack([p.pts, p.pts[:1] + 1.0]), p.obs_cam,
+                    p.obs_pt, p.obs_uv, p.gt_cams, p.gt_pts, p.loss)
+    o = oracle_for(q)
+    ck, lk = o.state(0)
+    cp, lp = ck.copy(), lk.copy()
+    R0 = Rotation.from_rotvec([0.3, -1.1, 0.7]).as_matrix()
+    if det_negative:
+        U = Rotation.from_rotvec([0.2, 0.5, -0.4]).as_matrix()
+        V = Rotation.from_rotvec([-1.0, 0.3, 0.8]).as_matrix()
+        ck[-1, :9] = cp[-1, :9] = (U @ np.diag([3.0, 2.0, -0.5]) @ V.T).ravel()
+    else:
+        ck[-1, :9] = (Rotation.from_rotvec([0, 0, 0.3]).as_matrix() @ R0).ravel()
+        cp[-1, :9] = R0.ravel()
+    ck[-1, 9:12], cp[-1, 9:12] = [1.0, 2.0, 3.0], [0.5, 2.5, 3.0]
+    lp[-1] = lk[-1] - [0.5, -0.25, 2.0]
+    s0 = (1 + 5 ** 0.5) / 2
+    o.set_state(0, ck, lk)
+    o.set_state(1, cp, lp)
+    o.set_schedule(s0, 1e30)
+    tro = o.iterate(1)
+    with solver(q) as s:
+        s.set_state_native(ck, lk, cp, lp, s0, 1e30)
+        trg = s.iterate_trace(1)
+        cg, lg, _ = s.state_native(0)
+    co, lo = o.state(0)
+    assert trg[0, D.daba.TR_RESTART] == tro[0, oracle.TR_RESTART] == 0
+    assert trg[0, 0] == pytest.approx(tro[0, 0], rel=F_TOL)
+    assert max(state_errors(cg, lg, co, lo)) <= 1e-11
+    if det_negative:
+        np.testing.assert_allclose(cg[-1, :9].reshape(3, 3), U @ V.T, atol=1e-12)
 
 
 def test_more_isolated_points_than_observations():
