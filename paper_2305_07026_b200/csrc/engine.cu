@@ -160,34 +160,6 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
   return DABA_OK;
 }
 
-// Release one dalloc'd buffer before destroy (create-time buffers whose job is done).
-void dfree(daba_ctx* c, void* p, size_t bytes) {
-  if (!p) return;
-  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
-  if (it == c->allocs.end()) return;
-  c->allocs.erase(it);
-  c->dev_bytes -= bytes;
-  if (c->pooled)
-    cudaFreeAsync(p, c->stream);
-  else
-    cudaFree(p);
-}
-
-// Create-time temporary device memory (stream-ordered from the context pool when there is one).
-void* talloc(daba_ctx* c, size_t bytes) {
-  void* p = nullptr;
-  cudaMemPool_t pool = context_pool(c->device);
-  cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, pool, c->stream) : cudaMalloc(&p, bytes ? bytes : 1);
-  return e == cudaSuccess ? p : nullptr;
-}
-void tfree(daba_ctx* c, void* p) {
-  if (!p) return;
-  if (context_pool(c->device))
-    cudaFreeAsync(p, c->stream);
-  else
-    cudaFree(p);
-}
-
 // Host -> device copy on the context's stream.  Small or page-locked sources go directly; large pageable ones
 // through a process-wide page-locked staging buffer (two 32 MB halves: the host threads fill one half while
 // the copy engine drains the other).  Returns once the source may be reused.
@@ -344,25 +316,6 @@ void collect_times(daba_ctx* c) {
 int enqueue_iteration(daba_ctx* c, int* launches) {
   const IterParams& P = c->P;
   int n = 0;
-  if (P.pt_mode == 1) {
-    // point pass by recomputation: it reads only x^k and x-bar^k, so it runs beside the camera pass and the
-    // camera solve (parallel graph branches); profiling serialises so that events bracket one kernel
-    if (c->opt.profile || !c->fork1) {
-      n += timed(c, "k_cam_pass", [&] { return launch_cam_pass(P, c->stream); });
-      n += timed(c, "k_inter", [&] { return launch_inter(P, c->stream); });
-      n += timed(c, "k_cam_solve", [&] { return launch_cam_solve(P, c->stream); });
-      n += timed(c, "k_pt_pass", [&] { return launch_pt_recompute(P, c->stream); });
-    } else {
-      CUDA_OR(c, cudaEventRecord(c->ev_fork, c->stream));
-      CUDA_OR(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-      n += launch_pt_recompute(P, c->side);
-      CUDA_OR(c, cudaEventRecord(c->ev_join, c->side));
-      n += launch_cam_pass(P, c->stream);
-      n += launch_inter(P, c->stream);
-      n += launch_cam_solve(P, c->stream);
-      CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    }
-  } else {
   if (!c->opt.profile && c->fork0 && (P.n_boundary > 0 || P.n_inter_blocks > 0)) {
     // the boundary records and the inter-device terms only read x^k, x-bar^k and the halo: a parallel branch
     // beside the camera pass
@@ -392,7 +345,6 @@ int enqueue_iteration(daba_ctx* c, int* launches) {
     CUDA_OR(c, cudaEventRecord(c->ev_join, c->side));
     n += launch_pt_sum(P, c->stream);
     CUDA_OR(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-  }
   }
   if (c->comm) {
     const bool halo = !c->segs.empty();
@@ -652,7 +604,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     std::string why = C->err;
     const cudaError_t ce = cudaGetLastError();
     if (why.empty()) why = code == DABA_E_CUDA ? std::string("CUDA: ") + cudaGetErrorString(ce) : "daba_create failed";
-    why += " (line " + std::to_string(g_bail_line) + ")";
+    why += " (engine.cu:" + std::to_string(g_bail_line) + ")";
     daba_destroy(c.release());
     g_create_err = why;
     return code;
@@ -693,7 +645,6 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   P.n_own_cams = S.n_own_cams;
   P.n_pts = (int32_t)S.pt_g.size();
   P.n_own_pts = S.n_own_pts;
-  P.pt_mode = (int32_t)env_int("DABA_PT_MODE", 0);  // 1: point pass by recomputation (no records; measured slower)
   P.loss = loss.kind;
   P.delta = loss.scale;
   P.delta2 = loss.scale * loss.scale;
@@ -773,12 +724,6 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.cam_chunk_ptr = dcp;
   }
   timer.mark("camera side");
-  // pt_mode 1 create-time temporaries: point-major cameras / pixels and the tile build's scratch
-  void* pt_tmp = nullptr;
-  size_t pt_tmp_bytes = 0;
-  int32_t* pm_cam = nullptr;
-  double2* pm_uv = nullptr;
-  char* pt_scratch = nullptr;
   // point side: records written by the camera pass at its observation index; boundary observations (camera
   // owned elsewhere) are recomputed into records n_cam_side + b
   std::vector<int32_t> bcam, bpt;
@@ -787,31 +732,13 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (S.point_side_deferred) {  // light plan: every point's records in camera order, sorted on the device
       int64_t* dptr;
       int32_t* dsrc;
-      if ((rc = dalloc(C, &dptr, (size_t)N + 1))) return g_bail_line = __LINE__, bail(rc);
-      // pt_mode 1: the record list is a temporary (input of the tile build), and the sort must leave the
-      // observations' cameras (d_ocam, the start of the staging buffer) intact
-      const size_t keep = P.pt_mode ? (4 * (size_t)K + 255) / 256 * 256 : 0;
-      if (P.pt_mode) {
-        pt_tmp_bytes = 20 * (size_t)K + 512 + point_tiles_scratch_bytes(K, (int32_t)N, (int32_t)M, (int32_t)(N / 64 + 2));
-        if (!(pt_tmp = talloc(C, 4 * (size_t)K + pt_tmp_bytes))) return g_bail_line = __LINE__, bail(DABA_E_OOM);
-        dsrc = static_cast<int32_t*>(pt_tmp);
-      } else if ((rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1)))) {
+      if ((rc = dalloc(C, &dptr, (size_t)N + 1)) || (rc = dalloc(C, &dsrc, (size_t)std::max<int64_t>(K, 1))))
         return g_bail_line = __LINE__, bail(rc);
-      }
-      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, reinterpret_cast<char*>(P.staging) + keep,
-                                 64 * (size_t)P.n_records - keep, C->stream) != 0)
+      if (sort_point_side_device(d_opt, K, (int32_t)N, dsrc, dptr, P.staging, 64 * (size_t)P.n_records,
+                                 C->stream) != 0)
         return g_bail_line = __LINE__, bail(DABA_E_CUDA);
       P.p_ptr = dptr;
       P.p_src = dsrc;
-      if (P.pt_mode) {  // point-major cameras and pixels of the tile build
-        char* q = static_cast<char*>(pt_tmp) + (4 * (size_t)K + 255) / 256 * 256;
-        pm_cam = reinterpret_cast<int32_t*>(q);
-        pm_uv = reinterpret_cast<double2*>(q + (4 * (size_t)K + 255) / 256 * 256);
-        pt_scratch = q + (4 * (size_t)K + 255) / 256 * 256 + (16 * (size_t)K + 255) / 256 * 256;
-        launch_gather_i32(reinterpret_cast<const int32_t*>(P.staging), dsrc, K, pm_cam, C->stream);
-        launch_gather_d2(P.c_uv, dsrc, K, pm_uv, C->stream);
-        P.p_src = nullptr;
-      }
       P.n_cam_side = K;
       P.n_boundary = 0;
       const int32_t *d1, *d2;
@@ -854,22 +781,6 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     P.n_cam_side = (int64_t)kc;
     P.n_boundary = (int64_t)bcam.size();
     P.n_records = std::max<int64_t>(P.n_cam_side + P.n_boundary, 1);
-    if (P.pt_mode) {  // no records: a scratch buffer (pixel residuals, state packing) and the tile build inputs
-      P.n_records = std::max<int64_t>(1, (std::max<int64_t>((int64_t)kc, 3 * (int64_t)S.pt_g.size()) + 7) / 8);
-      pt_tmp_bytes = 20 * kp + 512 + point_tiles_scratch_bytes((int64_t)kp, P.n_own_pts, P.n_cams, P.n_own_pts / 64 + 2);
-      if (!(pt_tmp = talloc(C, pt_tmp_bytes))) return g_bail_line = __LINE__, bail(DABA_E_OOM);
-      char* q = static_cast<char*>(pt_tmp);
-      pm_cam = reinterpret_cast<int32_t*>(q);
-      pm_uv = reinterpret_cast<double2*>(q + (4 * kp + 255) / 256 * 256);
-      pt_scratch = q + (4 * kp + 255) / 256 * 256 + (16 * kp + 255) / 256 * 256;
-      hvec<double2> uv(kp);
-      parallel_for((int64_t)kp, [&](int64_t a, int64_t b) {
-        for (int64_t r = a; r < b; ++r) uv[r] = make_double2(obs_uv[2 * S.p_obs[r]], obs_uv[2 * S.p_obs[r] + 1]);
-      });
-      CUDA_OR(C, h2d(C, pm_cam, S.p_cam.data(), kp * sizeof(int32_t)));
-      CUDA_OR(C, h2d(C, pm_uv, uv.data(), kp * sizeof(double2)));
-      CUDA_OR(C, cudaStreamSynchronize(C->stream));  // uv is freed at the end of this scope
-    }
     if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return g_bail_line = __LINE__, bail(rc);
     const int32_t *d0, *d1, *d2;
     const double2* d4;
@@ -915,70 +826,9 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     }
     // point-pass grid: every thread a few points (grid-stride), at least 8 CTAs per SM's worth; measured on
     // Final-13682: 4.46M points 1184 -> 4352 CTAs -17 us, 0.58M points (8 ranks) 1184 better than 2264
-    if (P.pt_mode) {
-      // tile arrays of the point pass, built on the device from the point-major lists; the tiles themselves
-      // (consecutive points, <= kPtTileMax points and <= kPtTileObs observations) are cut on the host
-      const int64_t kp = P.p_ptr ? (S.point_side_deferred ? K : (int64_t)S.p_obs.size()) : 0;
-      std::vector<int64_t> hptr;
-      const int64_t* ptr_h = nullptr;
-      if (S.point_side_deferred) {
-        hptr.resize((size_t)P.n_own_pts + 1);
-        CUDA_OR(C, cudaMemcpyAsync(hptr.data(), P.p_ptr, hptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                   C->stream));
-        CUDA_OR(C, cudaStreamSynchronize(C->stream));
-        ptr_h = hptr.data();
-      } else {
-        ptr_h = S.pt_ptr.data();
-      }
-      std::vector<int32_t> pt0(1, 0);
-      for (int32_t j = 0; j < P.n_own_pts;) {
-        int32_t e = j + 1;
-        while (e < P.n_own_pts && e - j < kPtTileMax && ptr_h[e + 1] - ptr_h[j] <= kPtTileObs) ++e;
-        pt0.push_back(e);
-        j = e;
-      }
-      P.n_pt_tiles = (int32_t)pt0.size() - 1;
-      int64_t* toff;
-      const int32_t* tpt0;
-      int32_t* tcam;
-      double2* tuv;
-      uint16_t *tjl, *tpos;
-      const size_t kk = (size_t)std::max<int64_t>(kp, 1);
-      if ((rc = dalloc(C, &toff, pt0.size())) || (rc = upload(C, const_cast<int32_t**>(&tpt0), pt0)) ||
-          (rc = dalloc(C, &tcam, kk)) || (rc = dalloc(C, &tuv, kk)) || (rc = dalloc(C, &tjl, kk)) ||
-          (rc = dalloc(C, &tpos, kk)))
-        return bail(rc);
-      const size_t need = point_tiles_scratch_bytes(kp, P.n_own_pts, P.n_cams, P.n_pt_tiles);
-      size_t avail = pt_tmp_bytes + (S.point_side_deferred ? 4 * (size_t)K : 0) - (size_t)(pt_scratch - static_cast<char*>(pt_tmp));
-      void* extra = nullptr;
-      char* scr = pt_scratch;
-      if (avail < need) {  // (the tile count is known only now)
-        if (!(extra = talloc(C, need))) return bail(DABA_E_OOM);
-        scr = static_cast<char*>(extra);
-        avail = need;
-      }
-      const int b = build_point_tiles_device(pm_cam, pm_uv, P.p_ptr, P.n_own_pts, kp, P.n_cams, tpt0, P.n_pt_tiles,
-                                             tcam, tuv, tjl, tpos, toff, scr, avail, C->stream);
-      tfree(C, extra);
-      tfree(C, pt_tmp);
-      pt_tmp = nullptr;
-      if (b != 0) return bail(DABA_E_CUDA);
-      P.t_off = toff;
-      P.t_pt0 = tpt0;
-      P.t_cam = tcam;
-      P.t_uv = tuv;
-      P.t_jl = tjl;
-      P.t_pos = tpos;
-      if (S.point_side_deferred) {  // the staging buffer held the observations' cameras: now a small scratch
-        dfree(C, P.staging, 64 * (size_t)P.n_records);
-        P.n_records = std::max<int64_t>(1, (std::max<int64_t>(K, 3 * N) + 7) / 8);
-        if ((rc = dalloc(C, &P.staging, 8 * (size_t)P.n_records))) return bail(rc);
-      }
-    }
     const int32_t pt_cap = (int32_t)env_int(
         "DABA_PT_CAP", std::max<int64_t>(148 * 8, ((int64_t)P.n_own_pts + 4 * kPtPassThreads - 1) / (4 * kPtPassThreads)));
-    P.n_pt_blocks = P.pt_mode ? std::max(1, std::min(P.n_pt_tiles, C->num_sms))
-                              : std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, pt_cap));
+    P.n_pt_blocks = std::max(1, std::min((P.n_own_pts + kPtPassThreads - 1) / kPtPassThreads, pt_cap));
   }
   timer.mark("point side");
   // scratch
@@ -1103,7 +953,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   // launches per iteration (for bookkeeping)
   {
     const bool unpack = C->n_recv_cam + C->n_recv_pt > 0, dev = P.restart_scope == 1;
-    C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0 && P.pt_mode == 0) +
+    C->launches_per_iter = 3 - (P.n_chunks == 0) - (P.n_own_cams == 0) + (P.n_boundary > 0) +
                            (P.n_inter_blocks > 0) + (C->comm && (dev || !unpack) ? 1 : 0) +
                            (C->n_send_cam + C->n_send_pt > 0 && !P.sendbuf) + unpack;
   }

@@ -22,7 +22,6 @@
 //          k_pack / k_unpack halo send / receive buffers (N > 1); k_lbar_all, k_objective at create / resume
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
-#include <cstdlib>
 
 #include "kernels.h"
 #include "device_math.cuh"
@@ -53,34 +52,6 @@ __device__ __forceinline__ void st256(double4* q, double4 v) {
 // with both anchors in one CTA k_pt_sum +0.025 / k_cam_pass +0.033 ms.)
 __device__ __forceinline__ double4* rec_ptr(const IterParams& p, int64_t r, int a) {
   return reinterpret_cast<double4*>(p.staging + (a ? 4 * p.n_records : 0)) + r;
-}
-
-// Streaming loads that must not displace L1-resident data (k_pt_pass keeps its camera records in L1).
-__device__ __forceinline__ double4 ld256_na(const double4* q) {
-  double4 v;
-  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
-  return v;
-}
-__device__ __forceinline__ double2 ld128_na(const double2* q) {
-  double2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(q));
-  return v;
-}
-__device__ __forceinline__ int32_t ld32_na(const int32_t* q) {
-  int32_t v;
-  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(q));
-  return v;
-}
-__device__ __forceinline__ int ldu16_na(const uint16_t* q) {
-  unsigned short v;
-  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(q));
-  return (int)v;
-}
-// camera records read by many observations: kept in L1
-__device__ __forceinline__ double4 ld256_el(const double4* q) {
-  double4 v;
-  asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
-  return v;
 }
 
 // Point record: 32 bytes (x, y, z, pad) — one sector per gather.
@@ -238,14 +209,14 @@ __device__ __forceinline__ void stage_chunk(const IterParams& p, const CamChunk 
 }
 
 // One anchor's pass over a chunk by a group of G threads (lane = rank in the group): observation lane + G k.
-template <int LOSS, bool ACC, int G, bool EMIT>
+template <int LOSS, bool ACC, int G>
 __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChunk ch, double* acc,
                                               double2* ring, const int32_t* sidx, int lane, const double* scam) {
   CamRegs c{scam};
   const double4* __restrict__ L = ACC ? p.lbar[p.roles[4]] : p.pts[p.roles[1]];
   const int tid = threadIdx.x;
   const int n = (ch.n - lane + G - 1) / G;  // observations of this thread
-#define REC(kk) (EMIT ? ch.o0 + lane + (int64_t)(kk) * G : (int64_t)-1)
+#define REC(kk) (ch.o0 + lane + (int64_t)(kk) * G)
   auto uslot = [&](int k) { return ring + (k & (kRing - 1)) * kCamPassThreads + tid; };
   auto issue = [&](int k) {
     if (k < n) cp_async16(uslot(k), p.c_uv + ch.o0 + lane + (int64_t)k * G);
@@ -317,8 +288,7 @@ constexpr int kCamSmemDoubles =
 // anchor, sharing the staged indices (large shards).  Otherwise one CTA per chunk and anchor, all threads on
 // one anchor: twice the CTAs, for shards too small to fill the GPU a few times over (measured: Final-13682 at
 // one rank 0.741 vs 0.764 ms; one rank of eight 0.247 vs 0.251 ms per iteration).
-// EMIT: write the point-side records (pt_mode 0); without them the point pass recomputes its side (pt_mode 1).
-template <int LOSS, bool SHARED, bool EMIT>
+template <int LOSS, bool SHARED>
 __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterParams p) {
   extern __shared__ __align__(16) double smem[];  // kCamSmemDoubles
   constexpr int G = SHARED ? kCamPassThreads / 2 : kCamPassThreads;
@@ -336,9 +306,9 @@ __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterPar
   stage_chunk(p, ch, sidx);
   __syncthreads();
   if (grp == 0)
-    cam_pass_body<LOSS, true, G, EMIT>(p, ch, acc, ring, sidx, lane, scam[0]);
+    cam_pass_body<LOSS, true, G>(p, ch, acc, ring, sidx, lane, scam[0]);
   else
-    cam_pass_body<LOSS, false, G, EMIT>(p, ch, acc, ring, sidx, lane, scam[1]);
+    cam_pass_body<LOSS, false, G>(p, ch, acc, ring, sidx, lane, scam[1]);
   __syncthreads();  // the ring is reused as the reduction buffer
   group_reduce_moments<G>(acc, p.partial + (size_t)(SHARED ? 2 * blockIdx.x : blockIdx.x) * kPartialStride, smem);
 }
@@ -544,12 +514,11 @@ __device__ __forceinline__ void pt_finish(const IterParams& p, int j, const doub
 // Boundary observations (their camera is owned by another rank, N > 1 only): recompute the point-side
 // contribution from the halo camera and write it into the staging record, like the camera pass does.
 // A 128-byte camera record into registers: four 256-bit loads, all in flight together.
-template <bool EL = false>
 __device__ __forceinline__ void load_cam16(const double* c, double* out) {
   const double4* q = reinterpret_cast<const double4*>(c);
   double4 v[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = EL ? ld256_el(q + k) : ld256(q + k);
+  for (int k = 0; k < 4; ++k) v[k] = ld256(q + k);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     out[4 * k] = v[k].x;
@@ -703,149 +672,6 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   }
   finish_block(p);
 }
-
-// Point pass by recomputation (pt_mode 1; a4 + a5 + a7, no records).  The owned points form tiles (consecutive
-// points, <= kPtTileMax of them and <= kPtTileObs observations); a persistent CTA per SM walks a contiguous range
-// of tiles, so that the camera records its observations read — one camera cluster's — stay in that SM's L1.  Per
-// tile: the points (x-bar^k, x^k) go to shared memory; each thread evaluates its observations in (camera, point)
-// order — so that neighbouring lanes mostly read the same camera record — the point side of the pair at both
-// anchors, (w lam^2, w lam R e), the quantities the camera pass forms (eqs. ray, gamma, error, w, P:L111-141,
-// L216-224), and stores them at the observation's point-major position; then every point adds its contiguous run
-// in camera order (two threads per point, one per anchor; deterministic) and takes the exact minimiser of eq. Q +
-// the proximal term (pt_finish).  Independent of the camera pass: both read only x^k and x-bar^k.
-constexpr size_t kPtPassSmem = sizeof(double) * 8 * kPtTileObs + sizeof(double4) * 2 * kPtTileMax;
-constexpr int kPtPerThread = (kPtTileObs + kPtThreads - 1) / kPtThreads;  // observations per thread and tile
-template <int LOSS>
-__global__ void __launch_bounds__(kPtThreads, 1) k_pt_pass(IterParams p) {
-  extern __shared__ __align__(32) double pt_smem[];
-  double(*sv)[kPtTileObs] = reinterpret_cast<double(*)[kPtTileObs]>(pt_smem);  // (A, C) x 2 anchors, point-major
-  double4(*spt)[kPtTileMax] = reinterpret_cast<double4(*)[kPtTileMax]>(pt_smem + 8 * kPtTileObs);
-  const int t = threadIdx.x, half = t & 1, jo = t >> 1;  // summing: point jo of the tile, anchor `half`
-  const int T = p.n_pt_tiles, G = gridDim.x;
-  const int tb = (int)((int64_t)T * blockIdx.x / G), te = (int)((int64_t)T * (blockIdx.x + 1) / G);
-  const double* __restrict__ Cb = p.cbarb[p.roles[4]];
-  const double* __restrict__ Ck = p.cams[p.roles[1]];
-  const double4* __restrict__ Lb = p.lbar[p.roles[4]];
-  const double4* __restrict__ Lk = p.pts[p.roles[1]];
-  double qv[kPtCols] = {0, 0, 0, 0};
-  // this thread's observations of the next tile, prefetched while the current one is summed (HBM streams)
-  int64_t o_pf[kPtPerThread];
-  int32_t cam_pf[kPtPerThread];
-  double2 uv_pf[kPtPerThread];
-  int jl_pf[kPtPerThread], pos_pf[kPtPerThread];
-  auto prefetch = [&](int tile) {
-    const int64_t b = tile < te ? p.t_off[tile] : 0, e = tile < te ? p.t_off[tile + 1] : 0;
-#pragma unroll
-    for (int m = 0; m < kPtPerThread; ++m) {
-      o_pf[m] = b + t + m * kPtThreads;
-      if (o_pf[m] < e) {
-        cam_pf[m] = ld32_na(p.t_cam + o_pf[m]);
-        uv_pf[m] = ld128_na(p.t_uv + o_pf[m]);
-        jl_pf[m] = ldu16_na(p.t_jl + o_pf[m]);
-        pos_pf[m] = ldu16_na(p.t_pos + o_pf[m]);
-      } else {
-        o_pf[m] = -1;
-      }
-    }
-  };
-  prefetch(tb);
-  for (int tile = tb; tile < te; ++tile) {
-    const int64_t ob = p.t_off[tile], oe = p.t_off[tile + 1];
-    const int j0 = p.t_pt0[tile], np = p.t_pt0[tile + 1] - j0;
-    const bool single = np == 1;  // (may exceed kPtTileObs: rounds; its point-major order is the tile order)
-    if (t < np) {
-      spt[0][t] = ld256_na(Lb + j0 + t);
-      spt[1][t] = ld256_na(Lk + j0 + t);
-    }
-    const bool mine = jo < np;
-    const int jme = j0 + jo;
-    const int64_t p0 = mine ? p.p_ptr[jme] - ob : 0, p1 = mine ? p.p_ptr[jme + 1] - ob : 0;
-    double acc[4] = {0, 0, 0, 0};
-    __syncthreads();
-    for (int64_t b = ob; b < oe; b += kPtTileObs) {  // one round unless one point has more than kPtTileObs
-      const int n = (int)(oe - b < kPtTileObs ? oe - b : kPtTileObs);
-      const int64_t base = b - ob;  // point-major position of this round's first slot
-#pragma unroll
-      for (int m = 0; m < kPtPerThread; ++m) {
-        const int r = t + m * kPtThreads;
-        if (r < n) {
-          const int64_t o = b + r;
-          int32_t i;
-          double2 u;
-          int jl, pos;
-          if (o == o_pf[m]) {
-            i = cam_pf[m];
-            u = uv_pf[m];
-            jl = jl_pf[m];
-            pos = pos_pf[m];
-          } else {
-            i = ld32_na(p.t_cam + o);
-            u = ld128_na(p.t_uv + o);
-            jl = ldu16_na(p.t_jl + o);
-            pos = ldu16_na(p.t_pos + o);
-          }
-          if (single) pos = r;
-          double cam[16], v[4] = {0, 0, 0, 0};
-#if defined(DABA_PT_EXP) && (DABA_PT_EXP & 1)
-          i &= 0;  // timing experiment: every observation reads camera 0 (always an L1 hit)
-#endif
-          load_cam16<true>(Cb + (size_t)i * kCamStride, cam);
-          const double4 lb = spt[0][jl];
-          pt_terms<LOSS>(cam, lb.x, lb.y, lb.z, u, p, v[0], v[1], v[2], v[3]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) sv[k][pos] = v[k];
-          v[0] = v[1] = v[2] = v[3] = 0.0;
-          load_cam16<true>(Ck + (size_t)i * kCamStride, cam);
-          const double4 lk = spt[1][jl];
-          pt_terms<LOSS>(cam, lk.x, lk.y, lk.z, u, p, v[0], v[1], v[2], v[3]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) sv[4 + k][pos] = v[k];
-        }
-      }
-      if (b + kPtTileObs >= oe) prefetch(tile + 1);
-      __syncthreads();
-      // point jo's run of this round, in camera order
-      const int64_t lo = p0 > base ? p0 : base, hi = p1 < base + n ? p1 : base + n;
-#if !defined(DABA_PT_EXP) || !(DABA_PT_EXP & 2)
-      for (int64_t m = lo; m < hi; ++m) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] += sv[4 * half + k][m - base];
-      }
-#endif
-      __syncthreads();
-    }
-    // both anchors' sums of point jo meet in the even lane of the pair
-    double other[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) other[k] = __shfl_xor_sync(0xffffffffu, acc[k], 1);
-    if (mine && half == 0) {
-      const double4 b4 = spt[0][jo], k4 = spt[1][jo];
-      const double lb[3] = {b4.x, b4.y, b4.z}, lk[3] = {k4.x, k4.y, k4.z};
-      const double a8[8] = {acc[0], acc[1], acc[2], acc[3], other[0], other[1], other[2], other[3]};
-      double qq[kPtCols];
-      pt_finish(p, jme, lb, lk, a8, qq);
-#pragma unroll
-      for (int c = 0; c < kPtCols; ++c) qv[c] += qq[c];
-    }
-    __syncthreads();  // spt is refilled for the next tile
-  }
-  __shared__ double ws[kPtThreads / 32][kPtCols];
-#pragma unroll
-  for (int c = 0; c < kPtCols; ++c) {
-    double v = qv[c];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if ((t & 31) == 0) ws[t >> 5][c] = v;
-  }
-  __syncthreads();
-  if (t < kPtCols) {
-    double v = 0;
-    for (int w = 0; w < kPtThreads / 32; ++w) v += ws[w][t];
-    p.pt_part[(size_t)blockIdx.x * kPtCols + t] = v;
-  }
-  finish_block(p);
-}
-
 
 // ------------------------------------------------------------------ a6: camera solve
 // Sums of App. A of SURVEY.md (all in the anchor camera frame), derived from the 40 moments.
@@ -1432,24 +1258,14 @@ static void cam_launch(const IterParams& p, cudaStream_t st) {
   constexpr size_t sm = sizeof(double) * kCamSmemDoubles;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_cam_pass<LOSS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_cam_pass<LOSS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_cam_pass<LOSS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_cam_pass<LOSS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_cam_pass<LOSS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_cam_pass<LOSS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  const bool emit = p.pt_mode == 0;
-  if (p.cam_shared_ctas) {
-    if (emit)
-      k_cam_pass<LOSS, true, true><<<p.n_chunks, kCamPassThreads, sm, st>>>(p);
-    else
-      k_cam_pass<LOSS, true, false><<<p.n_chunks, kCamPassThreads, sm, st>>>(p);
-  } else {
-    if (emit)
-      k_cam_pass<LOSS, false, true><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
-    else
-      k_cam_pass<LOSS, false, false><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
-  }
+  if (p.cam_shared_ctas)
+    k_cam_pass<LOSS, true><<<p.n_chunks, kCamPassThreads, sm, st>>>(p);
+  else
+    k_cam_pass<LOSS, false><<<2 * p.n_chunks, kCamPassThreads, sm, st>>>(p);
 }
 
 int launch_cam_pass(const IterParams& p, cudaStream_t st) {
@@ -1478,28 +1294,6 @@ int launch_pt_pass(const IterParams& p, cudaStream_t st) {
 
 int launch_pt_sum(const IterParams& p, cudaStream_t st) {
   k_pt_sum<<<p.n_pt_blocks, kPtPassThreads, 0, st>>>(p);
-  return 1;
-}
-
-template <int LOSS>
-static void pt_pass_launch(const IterParams& p, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_pt_pass<LOSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPtPassSmem);
-    // shared memory only as large as the kernel needs: the rest of the 256 KB stays L1 for the camera records
-    const char* cv = getenv("DABA_PT_CARVE");
-    cudaFuncSetAttribute(k_pt_pass<LOSS>, cudaFuncAttributePreferredSharedMemoryCarveout, cv ? atoi(cv) : 60);
-    configured = true;
-  }
-  k_pt_pass<LOSS><<<p.n_pt_blocks, kPtThreads, kPtPassSmem, st>>>(p);
-}
-
-int launch_pt_recompute(const IterParams& p, cudaStream_t st) {
-  switch (p.loss) {
-    case kHuber: pt_pass_launch<kHuber>(p, st); break;
-    case kCauchy: pt_pass_launch<kCauchy>(p, st); break;
-    default: pt_pass_launch<kTrivial>(p, st); break;
-  }
   return 1;
 }
 
@@ -1677,131 +1471,6 @@ int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d
   cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, d_pt, keys_out, vals, d_src, (int)K, 0, bits, st);  // stable
   k_ptr_from_sorted<<<grid(K), 256, 0, st>>>(keys_out, K, N, d_ptr);
   return cudaStreamSynchronize(st) == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
-// ------------------------------------------------------------------ create-time point tiles (pt_mode 1)
-__global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* out) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q < n) out[q] = src[idx[q]];
-}
-__global__ void k_gather_d2(const double2* src, const int32_t* idx, int64_t n, double2* out) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q < n) out[q] = src[idx[q]];
-}
-int launch_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* out, cudaStream_t st) {
-  if (n <= 0) return 0;
-  k_gather_i32<<<grid(n), 256, 0, st>>>(src, idx, n, out);
-  return 1;
-}
-int launch_gather_d2(const double2* src, const int32_t* idx, int64_t n, double2* out, cudaStream_t st) {
-  if (n <= 0) return 0;
-  k_gather_d2<<<grid(n), 256, 0, st>>>(src, idx, n, out);
-  return 1;
-}
-// point of every point-major observation, its tile, and the (tile, camera) sort key
-__global__ void k_tile_keys(const int64_t* p_ptr, int32_t n_pts, const int32_t* t_pt0, int32_t n_tiles,
-                            const int32_t* pm_cam, int cbits, int32_t* pt, uint64_t* key) {
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_pts) return;
-  int lo = 0, hi = n_tiles;  // the tile b with t_pt0[b] <= j < t_pt0[b + 1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (t_pt0[mid] <= j) lo = mid; else hi = mid;
-  }
-  const uint64_t tl = (uint64_t)lo << cbits;
-  for (int64_t q = p_ptr[j]; q < p_ptr[j + 1]; ++q) {
-    pt[q] = j;
-    key[q] = tl | (uint64_t)(uint32_t)pm_cam[q];
-  }
-}
-__global__ void k_tile_fill(const int32_t* ord, int64_t n, const int32_t* pm_cam, const double2* pm_uv,
-                            const int32_t* pt, const uint64_t* key_sorted, int cbits, const int32_t* t_pt0,
-                            int32_t* t_cam, double2* t_uv, uint16_t* t_jl, int32_t* t_pt, int32_t* t_tile) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  const int32_t o = ord[q];
-  const int32_t tile = (int32_t)(key_sorted[q] >> cbits);
-  t_cam[q] = pm_cam[o];
-  t_uv[q] = pm_uv[o];
-  t_pt[q] = pt[o];
-  t_tile[q] = tile;
-  t_jl[q] = (uint16_t)(pt[o] - t_pt0[tile]);
-}
-__global__ void k_tile_off(const int64_t* p_ptr, const int32_t* t_pt0, int32_t n_tiles, int64_t* t_off) {
-  const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b <= n_tiles) t_off[b] = p_ptr[t_pt0[b]];
-}
-// pos[q] = tile position of the q-th observation in (point, tile position) order: its point-major position
-__global__ void k_tile_pos(const int32_t* pos, int64_t n, const int32_t* t_tile, const int64_t* t_off,
-                           uint16_t* t_pos) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q < n) t_pos[pos[q]] = (uint16_t)(q - t_off[t_tile[pos[q]]]);
-}
-
-static int nbits(int64_t n) {
-  int b = 1;
-  while ((int64_t(1) << b) < n) ++b;
-  return b;
-}
-
-// bits of the (tile, camera) sort key
-static int tile_key_bits(int32_t n_cams, int32_t n_tiles) { return nbits(n_cams) + nbits((int64_t)n_tiles + 1); }
-
-size_t point_tiles_scratch_bytes(int64_t Kp, int32_t n_pts, int32_t n_cams, int32_t n_tiles) {
-  const int n = (int)(Kp > 0 ? Kp : 1);
-  size_t t1 = 0, t2 = 0;
-  cub::DoubleBuffer<uint64_t> k64(nullptr, nullptr);
-  cub::DoubleBuffer<int32_t> v32(nullptr, nullptr), k32(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, k64, v32, n, 0, tile_key_bits(n_cams, n_tiles));
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, k32, v32, n, 0, nbits(n_pts));
-  const size_t al = 256, K = (size_t)n;
-  auto up = [&](size_t b) { return (b + al - 1) / al * al; };
-  // pt, 2 x key64, 2 x val32, t_pt, t_tile; cub temporaries
-  return up(4 * K) + 2 * up(8 * K) + 2 * up(4 * K) + 2 * up(4 * K) + up(t1 > t2 ? t1 : t2);
-}
-
-int build_point_tiles_device(const int32_t* pm_cam, const double2* pm_uv, const int64_t* p_ptr, int32_t n_pts,
-                             int64_t Kp, int32_t n_cams, const int32_t* t_pt0, int32_t n_tiles, int32_t* t_cam,
-                             double2* t_uv, uint16_t* t_jl, uint16_t* t_pos, int64_t* t_off, void* scratch,
-                             size_t scratch_bytes, cudaStream_t st) {
-  if (scratch_bytes < point_tiles_scratch_bytes(Kp, n_pts, n_cams, n_tiles)) return -1;
-  k_tile_off<<<grid((int64_t)n_tiles + 1), 256, 0, st>>>(p_ptr, t_pt0, n_tiles, t_off);
-  if (Kp > 0) {
-    const size_t K = (size_t)Kp;
-    char* sp = static_cast<char*>(scratch);
-    int32_t* pt = static_cast<int32_t*>(carve(sp, 4 * K));
-    uint64_t* ka = static_cast<uint64_t*>(carve(sp, 8 * K));
-    uint64_t* kb = static_cast<uint64_t*>(carve(sp, 8 * K));
-    int32_t* va = static_cast<int32_t*>(carve(sp, 4 * K));
-    int32_t* vb = static_cast<int32_t*>(carve(sp, 4 * K));
-    int32_t* tpt = static_cast<int32_t*>(carve(sp, 4 * K));
-    int32_t* ttile = static_cast<int32_t*>(carve(sp, 4 * K));
-    void* tmp = sp;
-    const size_t tmp_bytes = scratch_bytes - (size_t)(sp - static_cast<char*>(scratch));
-    const int cbits = nbits(n_cams);
-    // 1. tile order: point-major observations stably sorted by (tile, local camera)
-    k_tile_keys<<<grid(n_pts), 256, 0, st>>>(p_ptr, n_pts, t_pt0, n_tiles, pm_cam, cbits, pt, ka);
-    k_iota<<<grid(Kp), 256, 0, st>>>(va, Kp);
-    cub::DoubleBuffer<uint64_t> dk(ka, kb);
-    cub::DoubleBuffer<int32_t> dv(va, vb);
-    size_t tb = tmp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)Kp, 0, tile_key_bits(n_cams, n_tiles), st) !=
-        cudaSuccess)
-      return -1;
-    k_tile_fill<<<grid(Kp), 256, 0, st>>>(dv.Current(), Kp, pm_cam, pm_uv, pt, dk.Current(), cbits, t_pt0, t_cam,
-                                         t_uv, t_jl, tpt, ttile);
-    // 2. each point's observations in tile order (= ascending local camera): tile positions stably sorted by
-    //    point; their offsets are p_ptr (the same counts), and q - t_off[tile] is the point-major position
-    int32_t* pos_in = dv.Alternate();
-    k_iota<<<grid(Kp), 256, 0, st>>>(pos_in, Kp);
-    cub::DoubleBuffer<int32_t> dk2(tpt, reinterpret_cast<int32_t*>(dk.Alternate()));
-    cub::DoubleBuffer<int32_t> dv2(pos_in, pt);
-    tb = tmp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(tmp, tb, dk2, dv2, (int)Kp, 0, nbits(n_pts), st) != cudaSuccess) return -1;
-    k_tile_pos<<<grid(Kp), 256, 0, st>>>(dv2.Current(), Kp, ttile, t_off, t_pos);
-  }
-  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) return -1;
-  return 0;
 }
 
 }  // namespace daba

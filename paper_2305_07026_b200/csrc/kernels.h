@@ -20,12 +20,6 @@ constexpr int kCamWarps = kCamPassThreads / 32;
 #endif
 constexpr int kCamChunkObs = DABA_CHUNK;  // max observations per camera-pass chunk (one CTA)
 constexpr int kPtPassThreads = 256;     // point solve: threads (points) per CTA
-// point pass by recomputation (pt_mode 1): tiles of consecutive owned points with at most kPtTileMax points and
-// kPtTileObs observations (a single point with more observations is a tile of its own, taken in rounds); the
-// tile's observations in (camera, point) order; persistent CTAs (one per SM) walk contiguous tile ranges
-constexpr int kPtTileMax = 384;
-constexpr int kPtThreads = 2 * kPtTileMax;  // two threads per point when summing (one per anchor)
-constexpr int kPtTileObs = 1536;            // shared-memory slots per tile: 8 doubles each
 constexpr int kCamEvalCols = 8;   // F, dP_acc, dP_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm
 constexpr int kPtCols = 4;        // dQ_acc, dQ_mm, step2_acc, step2_mm
 constexpr int kGlobalCols = 12;   // F, dP_acc, dQ_acc, dP_mm, dQ_mm, step2_acc, step2_mm, ndeg, noacc_acc, noacc_mm,
@@ -45,7 +39,7 @@ struct CamChunk {
 // Device state of one iteration.  Role buffers: roles[0] = x^{k-1}, roles[1] = x^k, roles[2] = acc candidate,
 // roles[3] = mm candidate; x-bar buffers (three per variable kind): roles[4] = x-bar^k, roles[5] / roles[6] =
 // x-bar^{k+1} if the accelerated / MM candidate is selected.  The select kernel rotates them on the device, so
-// that the passes reading x-bar^k never share a buffer with the solves writing x-bar^{k+1}.
+// that no kernel reading x-bar^k shares a buffer with one writing x-bar^{k+1} (the solves run beside each other).
 struct IterParams {
   // sizes
   int32_t n_cams;        // local cameras (owned first, then halo)
@@ -79,17 +73,6 @@ struct IterParams {
   const int32_t* p_src;          // record of each point-side observation
   double* staging;               // 2 x n_records x 4
   int64_t n_cam_side, n_records;
-  // point pass by recomputation (pt_mode 1; no records): tile-ordered point-side observations.  Tile b holds
-  // the owned points t_pt0[b] .. t_pt0[b+1] - 1 and their observations t_off[b] .. t_off[b+1] - 1, sorted by
-  // (local camera, point); t_pos gives each one's position in the tile's point-major order (p_ptr - t_off[b]).
-  int32_t pt_mode;               // 0: records emitted by the camera pass + k_pt_sum; 1: k_pt_pass
-  int32_t n_pt_tiles;
-  const int64_t* t_off;          // n_pt_tiles + 1
-  const int32_t* t_pt0;          // n_pt_tiles + 1
-  const int32_t* t_cam;          // local camera of each tile-ordered observation
-  const double2* t_uv;
-  const uint16_t* t_jl;          // its point within the tile
-  const uint16_t* t_pos;         // its point-major position within the tile (multi-point tiles)
   // boundary observations (point owned here, camera owned elsewhere): recomputed from halo cameras
   int64_t n_boundary;
   const int32_t* b_cam;
@@ -132,7 +115,6 @@ int launch_cam_pass(const IterParams& p, cudaStream_t st);
 int launch_pt_pass(const IterParams& p, cudaStream_t st);
 int launch_cam_solve(const IterParams& p, cudaStream_t st);
 int launch_pt_sum(const IterParams& p, cudaStream_t st);  // + rank-local sums (+ select without comm)
-int launch_pt_recompute(const IterParams& p, cudaStream_t st);  // pt_mode 1: k_pt_pass (same epilogue)
 int launch_select(const IterParams& p, cudaStream_t st);
 // per-device restart: the inter-device pair terms of F^{a(k)} (before k_cam_solve); rank-local sums of them
 // into local[10..11] (create time); the allreduced trace columns after a local decision
@@ -170,18 +152,6 @@ int launch_xyz_pts(const double* src, double4* dst, int32_t n, cudaStream_t st);
 // first use)
 int64_t count_point_jumps_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int32_t N, int32_t far,
                                  void* scratch, cudaStream_t st);
-// pt_mode 1: the tile arrays of IterParams from point-major arrays on the device (pm_cam local cameras, pm_uv
-// pixels, p_ptr offsets, n_pts owned points, Kp = p_ptr[n_pts] observations) and the tiles' first points t_pt0
-// (device, n_tiles + 1; host plan_point_tiles).  Returns 0 or -1 on a CUDA error.
-// point_tiles_scratch_bytes: the scratch it needs.
-size_t point_tiles_scratch_bytes(int64_t Kp, int32_t n_pts, int32_t n_cams, int32_t n_tiles);
-int build_point_tiles_device(const int32_t* pm_cam, const double2* pm_uv, const int64_t* p_ptr, int32_t n_pts,
-                             int64_t Kp, int32_t n_cams, const int32_t* t_pt0, int32_t n_tiles, int32_t* t_cam,
-                             double2* t_uv, uint16_t* t_jl, uint16_t* t_pos, int64_t* t_off, void* scratch,
-                             size_t scratch_bytes, cudaStream_t st);
-// gathers for the light plan: out[q] = src[idx[q]]
-int launch_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* out, cudaStream_t st);
-int launch_gather_d2(const double2* src, const int32_t* idx, int64_t n, double2* out, cudaStream_t st);
 int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, void* scratch,
                            size_t scratch_bytes, cudaStream_t st);
 
