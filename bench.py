@@ -28,17 +28,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "observations/sec per DABA iteration"
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_FMA_PEAK = 17.06e12  # measured DFMA/s, profiles/r01_day0_micro.log (148 SMs, full chip, independent chains)
+# FP64 peak: DFMA/s measured on this pool's B200 (tools/dmma_micro.cu, independent chains, 148 SMs:
+# profiles/r02_fp64_micro.log, 17.71 T DFMA/s; DMMA m8n8k4 18.4 T FMA/s — no faster) -> FLOP/s = 2 x DFMA/s
+FP64_FLOPS_PEAK = 2 * 17.71e12
 
-# Algorithmic bytes per launch: what each kernel must read or write at least once.
-#   k_cam_pass (both anchors): per observation u (16 B) + point index (4 B) read, the point-side record of both
-#     anchors written (2 x 32 B); per point the two anchor states read once (2 x 32 B); cameras 2 x 128 B.
-#   k_pt_sum: per observation both records (64 B) + record index (4 B); per point read x^k and
-#     x-bar^k (64 B), write both candidates and both next x-bar (4 x 32 B), offsets (8 B).
-BYTES = {
-    "k_cam_pass": lambda K, N, M: 84 * K + 64 * N + 2 * 128 * M,
-    "k_pt_sum": lambda K, N, M: 68 * K + 200 * N,
-}
+# Algorithmic work, per iteration at K observations, N points, M cameras:
+#   bytes: K * 20 (u 16 B + point index 4 B) + N * 96 (read l^k and l^{k-1}, write l_acc and l_mm; 24 B each)
+#          + M * 500 (camera copies and moments)
+#   k_cam_pass's own share: K * 20 + N * 48 (reads the two anchors' points once) + M * 256 (the two anchor cameras)
+#   FP64: 153.1 FLOP per observation and anchor in k_cam_pass — ncu SASS opcode counts of one launch on
+#   Final-13682 (DFMA 58.43 x 2 + DMUL 23.67 + DADD 12.58 thread instructions per observation and anchor;
+#   profiles/r02_cam_pass_sass_counts.txt), i.e. 306.2 FLOP per observation and iteration.
+ALG_BYTES_ITER = lambda K, N, M: 20 * K + 96 * N + 500 * M
+ALG_BYTES = {"k_cam_pass": lambda K, N, M: 20 * K + 48 * N + 256 * M}
+FLOP_PER_ANCHOR_OBS = 153.1
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
@@ -99,6 +102,17 @@ class Clocks:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def peaks():
@@ -215,25 +229,32 @@ def main():
     s = daba.Solver(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, stream=stream.cuda_stream, comm_key=fresh_key(),
                     **kw)
     lpi = s.launches_per_iteration()
+    # three repeats of the K timed steps (the median is reported); each repeat is bracketed by
+    # a barrier and a synchronize, and its time is the max over ranks
+    reps = []
     with torch.cuda.stream(stream):
         s.iterate(a.warmup)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with Clocks(local) as clk:
             time.sleep(0.3)
-            e0.record(stream)
-            s.iterate(a.steps)
-            e1.record(stream)
-            torch.cuda.synchronize()
+            for _ in range(3):
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                s.iterate(a.steps)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                r_ms = e0.elapsed_time(e1)
+                if world > 1:
+                    t = torch.tensor([r_ms], dtype=torch.float64)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    r_ms = float(t.item())
+                reps.append(r_ms)
         if world > 1:
             dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = statistics.median(reps)
     F_end = s.objective()
     info = s.shard_info()
     s.close()
@@ -295,41 +316,49 @@ def main():
     if world == 1 and not a.no_cpu_baseline:
         spb, dt = run_oracle_sample(p, 2_000_000, 2)
         cpu = {"value": 2 * spb.K / dt, "unit": "obs/s", "cores": 1, "kind": "oracle",
-               "sample": f"{spb.name}: {spb.K} of {p.K} observations, 2 iterations, single thread"}
+               "sample": f"{spb.name}: {spb.K} of {p.K} observations, 2 iterations, single thread",
+               "host_cores": os.cpu_count(), "cpu_model": cpu_model()}
 
     value = a.steps * p.K / (ms * 1e-3)
     hbm, hbm_src = peaks()
-    # dominant kernel (of those with a byte model) and its roofline
-    dom = max(((k, v) for k, v in kt.items() if k in BYTES), key=lambda kv: kv[1][0], default=None) or \
-        max(kt.items(), key=lambda kv: kv[1][0])
-    dname, (dms, dl) = dom
-    per_launch_ms = dms / max(dl, 1)
+    K_c, K_p = info["cam_side_obs"], info["pt_side_obs"]
+    N_l, M_l = info["own_pts"] + info["halo_pts"], info["own_cams"]
     kt = {k: v for k, v in kt.items() if v[1] > 0}
     kshare = {k: round(v[0] / prof_ms, 4) for k, v in kt.items()}
-    roof = None
-    kbytes = {k: f(info["cam_side_obs"] if k == "k_cam_pass" else info["pt_side_obs"],
-                   info["own_pts"] + info["halo_pts"], info["own_cams"]) for k, f in BYTES.items()}
+    # dominant kernel: k_cam_pass (FP64-bound), timed live with events on the library's stream
+    dname = "k_cam_pass" if "k_cam_pass" in kt else max(kt.items(), key=lambda kv: kv[1][0])[0]
+    dms, dl = kt[dname]
+    per_launch_ms = dms / max(dl, 1)
     traffic, fp64_pipe = None, None
     try:
         tj = json.load(open(TRAFFIC)).get(dname, {})
         traffic, fp64_pipe = tj.get("dram_bytes_per_launch"), tj.get("fp64_pipe_pct")
     except Exception:
         pass
-    if dname in BYTES:
-        byt = kbytes[dname]
-        ach = byt / (per_launch_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": traffic, "kernel": dname, "bytes_per_launch": int(byt),
-                "kernel_ms_per_launch": round(per_launch_ms, 5), "peak_source": hbm_src,
+    roof = None
+    if dname == "k_cam_pass":
+        flop = FLOP_PER_ANCHOR_OBS * 2 * K_c
+        ach = flop / (per_launch_ms * 1e-3) / 1e12
+        kb = ALG_BYTES["k_cam_pass"](K_c, N_l, M_l)
+        it_b = ALG_BYTES_ITER(K_c, N_l, M_l)
+        it_s = ms / a.steps * 1e-3
+        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(FP64_FLOPS_PEAK / 1e12, 2), "unit": "TFLOP/s",
+                "frac": round(ach * 1e12 / FP64_FLOPS_PEAK, 4), "traffic": traffic, "kernel": dname,
+                "flop_per_launch": int(flop), "kernel_ms_per_launch": round(per_launch_ms, 5),
+                "peak_source": "measured FP64 DFMA peak (tools/dmma_micro.cu, profiles/r02_fp64_micro.log)",
                 "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)" if traffic else None,
-                "fp64_pipe_pct_ncu": fp64_pipe}
-        # whole iteration: algorithmic bytes of both passes over the device-timed step
-        tot_b = sum(kbytes.values())
-        roof["iteration"] = {"bytes": int(tot_b), "achieved": round(tot_b / (ms / a.steps * 1e-3) / 1e9, 1),
-                             "frac": round(tot_b / (ms / a.steps * 1e-3) / 1e9 / hbm, 4)}
+                "fp64_pipe_pct_ncu": fp64_pipe,
+                "hbm_algorithmic": {"bytes_per_launch": int(kb), "achieved_gbs": round(kb / (per_launch_ms * 1e-3) / 1e9, 1),
+                                    "peak_gbs": hbm, "frac": round(kb / (per_launch_ms * 1e-3) / 1e9 / hbm, 4),
+                                    "peak_source": hbm_src},
+                "iteration": {"bytes": int(it_b), "achieved_gbs": round(it_b / it_s / 1e9, 1),
+                              "hbm_frac": round(it_b / it_s / 1e9 / hbm, 4),
+                              "flop": int(FLOP_PER_ANCHOR_OBS * 2 * K_c),
+                              "fp64_frac": round(FLOP_PER_ANCHOR_OBS * 2 * K_c / it_s / FP64_FLOPS_PEAK, 4)}}
     out = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3), "higher_is_better": True,
+        "ms_per_step": ms / a.steps, "iterations_per_s": a.steps / (ms * 1e-3),
+        "repeats_ms_per_step": [round(r / a.steps, 5) for r in reps], "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": ("bal file" if os.path.isfile(a.config) else "synthetic"),
         "config": {"workload": a.config if scaling == "strong" else f"{a.config} x{world}", "cameras": p.M, "points": p.N, "observations": int(p.K),
                    "loss": ["trivial", "huber", "cauchy"][p.loss], "parallelism": f"camera-partitioned x{world}",

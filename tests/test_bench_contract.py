@@ -38,7 +38,12 @@ def test_device_arm_contract():
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
     r = d["roofline"]
-    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5 and r["peak"] > 0
+    # the dominant kernel is FP64-bound: ALU roofline in TFLOP/s, with the algorithmic-byte HBM
+    # fraction (K*20 + N*96 + M*500 per iteration) beside it
+    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1.0 and r["peak"] > 30
+    assert 0 < r["hbm_algorithmic"]["frac"] < 1.5 and r["iteration"]["bytes"] > 0
+    assert len(d["repeats_ms_per_step"]) == 3
+    assert min(d["repeats_ms_per_step"]) <= d["ms_per_step"] <= max(d["repeats_ms_per_step"])
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 3 * 5
     assert "workload" in d["config"] and d["config"]["workload"] == "small_huber"
