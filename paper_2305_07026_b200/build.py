@@ -40,6 +40,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     return lib
 
 
+def build_check(force: bool = False) -> str:
+    """The bounds-check build (-DDABA_CHECK: device-side index checks that trap) as libdaba_check.so."""
+    return build(force=force, defines=("DABA_CHECK",), out=os.path.join(HERE, "libdaba_check.so"))
+
+
 if __name__ == "__main__":
     import sys
     build(force=True, verbose="-v" in sys.argv)

@@ -28,6 +28,25 @@
 
 namespace daba {
 
+// Bounds-check build (-DDABA_CHECK, build.py check=True): every index a kernel dereferences is checked against
+// the size it indexes; a violation prints the kernel, the index and its bound and traps (a CUDA error the host
+// reports).  The pool's compute-sanitizer is closed, so this is the memory-safety check of the GPU suite
+// (tests run with DABA_LIB pointing at libdaba_check.so; profiles/r02_check_build_tests.log).
+#ifdef DABA_CHECK
+#define DCHECK(cond, what, idx, bound)                                                                      \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("DABA_CHECK %s: %s index %lld bound %lld (block %d thread %d)\n", __func__, what, (long long)(idx), \
+             (long long)(bound), (int)blockIdx.x, (int)threadIdx.x);                                        \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define DCHECK(cond, what, idx, bound) \
+  do {                                \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double sched_gamma(double s, int accelerate, double* s_next_out) {
   // eq. nesterov_scalar in Algorithm 1 line 407's order: s^{(k+1)} first, then gamma^{(k)}
   const double s_next = (sqrt(4.0 * s * s + 1.0) + 1.0) / 2.0;
@@ -294,7 +313,10 @@ __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterPar
   constexpr int G = SHARED ? kCamPassThreads / 2 : kCamPassThreads;
   const int chunk = SHARED ? blockIdx.x : blockIdx.x >> 1;
   const int grp = SHARED ? threadIdx.x / G : (blockIdx.x & 1), lane = threadIdx.x % G;
+  DCHECK(chunk < p.n_chunks, "chunk", chunk, p.n_chunks);
   const CamChunk ch = p.chunks[chunk];
+  DCHECK(ch.o0 >= 0 && ch.n <= kCamChunkObs && ch.o0 + ch.n <= p.n_cam_side, "chunk obs", ch.o0 + ch.n, p.n_cam_side);
+  DCHECK(ch.cam >= 0 && ch.cam < p.n_own_cams, "chunk camera", ch.cam, p.n_own_cams);
   double acc[kPartialStride];
 #pragma unroll
   for (int k = 0; k < kPartialStride; ++k) acc[k] = 0.0;
@@ -304,6 +326,11 @@ __global__ void __launch_bounds__(kCamPassThreads, DABA_MINB) k_cam_pass(IterPar
   if (lane < kCamStride)
     scam[grp][lane] = (grp == 0 ? p.cbarb[p.roles[4]] : p.cams[p.roles[1]])[(size_t)ch.cam * kCamStride + lane];
   stage_chunk(p, ch, sidx);
+#ifdef DABA_CHECK
+  for (int o = threadIdx.x; o < ch.n; o += kCamPassThreads)
+    DCHECK(sidx[o] >= 0 && sidx[o] < p.n_pts, "point", sidx[o], p.n_pts);
+  DCHECK(ch.o0 + ch.n <= p.n_records, "record", ch.o0 + ch.n, p.n_records);
+#endif
   __syncthreads();
   if (grp == 0)
     cam_pass_body<LOSS, true, G>(p, ch, acc, ring, sidx, lane, scam[0]);
@@ -533,6 +560,9 @@ __global__ void __launch_bounds__(256) k_pt_boundary(IterParams p) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= p.n_boundary) return;
   const int32_t i = p.b_cam[b], j = p.b_pt[b];
+  DCHECK(i >= 0 && i < p.n_cams, "boundary camera", i, p.n_cams);
+  DCHECK(j >= 0 && j < p.n_own_pts, "boundary point", j, p.n_own_pts);
+  DCHECK(p.n_cam_side + b < p.n_records, "boundary record", p.n_cam_side + b, p.n_records);
   const double2 u = p.b_uv[b];
   const double4 lk = ld256(p.pts[p.roles[1]] + j), lb = ld256(p.lbar[p.roles[4]] + j);
   double cb[16], ck[16];
@@ -636,6 +666,8 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
       int32_t r[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) r[i] = o + i < o1 ? p.p_src[o + i] : -1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) DCHECK(r[i] < p.n_records && (r[i] >= 0 || o + i >= o1), "record", r[i], p.n_records);
       double4 A[4], B[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -825,6 +857,8 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
   double dP_acc = 0.0;
   const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
   if (valid) {
+    DCHECK(p.cam_chunk_ptr[i] <= p.cam_chunk_ptr[i + 1] && p.cam_chunk_ptr[i + 1] <= p.n_chunks, "camera chunks",
+           p.cam_chunk_ptr[i + 1], p.n_chunks);
     for (int c = p.cam_chunk_ptr[i]; c < p.cam_chunk_ptr[i + 1]; ++c) {
       const double* src = p.partial + ((size_t)c * 2 + a) * kPartialStride;
       for (int k = 0; k < kPartialStride; ++k) m[k] += src[k];
@@ -1044,6 +1078,8 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(IterParams p) {
   const int64_t b = blockIdx.x * (int64_t)kInterThreads + threadIdx.x;
   if (b < p.n_inter) {
     const int32_t i = p.i_cam[b], j = p.i_pt[b];
+    DCHECK(i >= 0 && i < p.n_cams, "inter camera", i, p.n_cams);
+    DCHECK(j >= 0 && j < p.n_pts, "inter point", j, p.n_pts);
     const double sg = (double)p.i_sign[b];
     const double2 u = p.i_uv[b];
     const double* ck = p.cams[p.roles[1]] + (size_t)i * kCamStride;
@@ -1155,6 +1191,7 @@ __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_
   const int n_cam_threads = 64 * n_cam;
   if (t < n_cam_threads) {  // two warps per camera: lanes 0..61 copy one double each
     const int e = t >> 6, c = t & 63;
+    DCHECK(cam_idx[e] >= 0 && cam_idx[e] < p.n_own_cams, "send camera", cam_idx[e], p.n_own_cams);
     const size_t i = (size_t)cam_idx[e] * kCamStride;
     double v = 0.0;
     if (c < 15)
@@ -1168,6 +1205,7 @@ __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_
     if (c < kHaloCam) buf[cam_off[e] + c] = v;
   } else if (t < n_cam_threads + n_pt) {
     const int q = t - n_cam_threads;
+    DCHECK(pt_idx[q] >= 0 && pt_idx[q] < p.n_own_pts, "send point", pt_idx[q], p.n_own_pts);
     const double4 la = p.pts[ra][pt_idx[q]], lm = p.pts[rm][pt_idx[q]];
     double* b = buf + pt_off[q];
     b[0] = la.x;
@@ -1205,6 +1243,7 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
     gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
   }
   if (t < n_cam) {  // x^{k+1} and its x-bar^{k+1} as the owner computed them
+    DCHECK(cam_idx[t] >= p.n_own_cams && cam_idx[t] < p.n_cams, "halo camera", cam_idx[t], p.n_cams);
     const size_t i = (size_t)cam_idx[t] * kCamStride;
     const double* src = buf + cam_off[t];
     double v[15], xb[16];
@@ -1221,6 +1260,7 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
     for (int k = 0; k < 16; ++k) cb[k] = xb[k];
   } else if (t < n_cam + n_pt) {
     const int q = t - n_cam;
+    DCHECK(pt_idx[q] >= p.n_own_pts && pt_idx[q] < p.n_pts, "halo point", pt_idx[q], p.n_pts);
     const double* b = buf + pt_off[q] + 3 * sel;
     const double4 lp = p.pts[r_old][pt_idx[q]];
     p.pts[r_new][pt_idx[q]] = make_double4(b[0], b[1], b[2], 0.0);

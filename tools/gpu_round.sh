@@ -11,6 +11,11 @@ for w in $what; do
     tests)
       timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${tag}_gputests.log 2>&1
       echo "tests rc=$?" >> gpurun_out/${tag}_rc.log ;;
+    check)
+      DABA_LIB=$PWD/paper_2305_07026_b200/libdaba_check.so timeout 2400 python -m pytest tests/test_gpu_parity.py \
+        tests/test_gpu_bal.py tests/test_gpu_coarse.py -q --timeout 900 -p no:cacheprovider \
+        > gpurun_out/${tag}_check_tests.log 2>&1
+      echo "check rc=$?" >> gpurun_out/${tag}_rc.log ;;
     bench)
       python bench.py --steps 100 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
       echo "bench rc=$?" >> gpurun_out/${tag}_rc.log ;;
