@@ -210,8 +210,10 @@ int daba_pixel_residuals(daba_ctx* ctx, double* resid_out);
  * obs_uv (K x 2) sorted by camera, with camera i's observations at [cam_off[i], cam_off[i+1]) (int64, M+1 entries).
  * A pair with |l - t| <= eps (Assumption 2) adds nothing and gets W[k] = 0.  V / gl are zeroed and then
  * accumulated with fp64 atomics (summation order not fixed); U / gc / F_cam are written in a fixed order.
- * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).  Returns 0, DABA_E_INVALID_ARG (-1) for
- * bad sizes / NULL buffers / unknown loss, DABA_E_CUDA (-3) if a launch fails. */
+ * The indices are checked on the device first (obs_pt in [0, N), cam_off monotone from 0 to K): DABA_E_INVALID_ARG
+ * before anything is written (this synchronises `stream`).  Then asynchronous on `stream` (a cudaStream_t; NULL =
+ * legacy default stream).  Returns 0, DABA_E_INVALID_ARG (-1) for bad sizes / NULL buffers / unknown loss / bad
+ * indices, DABA_E_CUDA (-3) if a launch fails. */
 int daba_coarse_blocks(const double* cams, int64_t M, const double* pts, int64_t N, const int32_t* obs_pt,
                        const double* obs_uv, const int64_t* cam_off, int64_t K, int loss, double scale, double eps,
                        double* U, double* gc, double* V, double* gl, double* W, double* F_cam, void* stream);
@@ -243,11 +245,49 @@ int daba_coarse_solve(const double* U, const double* gc, const double* V, const 
  * obs_cam / obs_pt (int32), obs_uv (K x 2) DEVICE, sorted by camera with offsets cam_off (int64, M + 1, DEVICE).
  * trace (HOST, n_iters x 5, nullable): F(x^k), F-bar^k, E(x_acc | x^k), restart flag, E(x_mm | x^k).
  * Host-driven and blocking (scalars read back per LM trial); scratch is allocated stream-ordered and freed.
+ * = daba_coarse_run_part with one device, mm_always = 1, keep_scratch = 1.
  * Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3), DABA_E_OOM (-5). */
 int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam, const int32_t* obs_pt,
                     const double* obs_uv, const int64_t* cam_off, int64_t K, int loss, double scale, double eps,
                     double xi, double eta, double mu0, double mu_up, int lm_trials, int accelerate, int pcg_max_iter,
                     double pcg_tol, int n_iters, double* trace, void* stream);
+
+/* Algorithm 1 with the coarse-partition surrogate over a DEVICE PARTITION (eq. Ealpha):
+ * cam_dev (M) / pt_dev (N) give each camera / point a device in [0, ndev) (int32, DEVICE; both NULL = one device,
+ * ndev = 1; ndev <= 8).  A pair whose camera and point share a device (E') is kept exactly in that device's
+ * subproblem; a pair across devices (E'') is majorized (Prop. 1): P_ij on the camera's device, Q_ij on the point's.
+ * Each device's subproblem (eqs. update_amm / update_mm) is one successful LM step on the device's variables
+ * (readings R-N3a..d): the devices' systems are block diagonal, so one Schur-complement PCG solves them
+ * all; each device accepts its first trial (mu = mu0 mu_up^tau) that strictly decreases ITS E^a, the others keep
+ * trying.  The restart test is the global one of reading D2: E(x_acc | x^k) = F(x^k) + sum_a [E^a(x_acc | x^k) -
+ * E^a(x^k | x^k)] > F-bar^k.  All buffers as daba_coarse_run.  trace (HOST, n_iters x 5, nullable): F(x^k),
+ * F-bar^k, E(x_acc | x^k), restart flag, E(x_mm | x^k) (NaN when mm_always = 0 and no restart fired: the MM
+ * subproblem is then not solved, Alg. 1).  trials (HOST, n_iters x 2 ndev int32, nullable): per iteration
+ * the accepted trial of every device for the accelerated then the MM subproblem (-1: none / not solved).
+ * The inputs are checked on the device first (indices in range, cam_off monotone from 0 to K, obs_cam inside its
+ * camera's segment, device ids in range): DABA_E_INVALID_ARG before anything is written.  The calling thread's
+ * current device is switched to the one holding `cams` for the call.  The PCG's point sums and scalars use fp64
+ * atomics: results are reproducible to rounding, not bitwise.  Scratch comes from the library's stream-ordered
+ * pool; keep_scratch = 0 trims the pool back afterwards.  Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3),
+ * DABA_E_OOM (-5). */
+typedef struct {
+  int loss;          /* 0 trivial, 1 Huber, 2 Cauchy */
+  double scale, eps; /* loss scale delta (> 0); Assumption 2 threshold */
+  double xi, eta;    /* proximal weight (> 0), restart averaging in (0, 1] */
+  double mu0, mu_up; /* LM damping schedule */
+  int lm_trials;     /* >= 1 */
+  int accelerate;    /* 0: plain MM (DUBA) */
+  int pcg_max_iter;  /* >= 1 */
+  double pcg_tol;    /* preconditioned residual ratio */
+  int mm_always;     /* 1: solve the MM subproblem every iteration (oracle parity); 0: only when the restart fires */
+  int keep_scratch;  /* 1: keep the scratch in the pool for the next call */
+} daba_coarse_options;
+void daba_coarse_default_options(daba_coarse_options* o); /* trivial, 1, 1e-8, xi 1e-4, eta 0.1, 1e-3, 10, 5, 1,
+                                                              PCG <= 10 to 1e-2, mm_always 0, keep_scratch 0 */
+int daba_coarse_run_part(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
+                         const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
+                         const int32_t* cam_dev, const int32_t* pt_dev, int ndev, const daba_coarse_options* opt,
+                         int n_iters, double* trace, int32_t* trials, void* stream);
 
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations

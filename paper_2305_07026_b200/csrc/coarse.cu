@@ -14,12 +14,49 @@
 #include <algorithm>
 
 #include "device_math.cuh"
+#include "../../include/daba.h"
 
 namespace daba {
 namespace {
 
 constexpr int kCoarseThreads = 128;
 constexpr int kUCols = 45 + 9;  // packed lower triangle of U_i and g_c,i
+constexpr int kMaxDev = 8;      // devices of a coarse partition (eq. Ealpha's alpha) handled in one run
+
+// A device partition: cam_dev (M) and pt_dev (N) device ids in [0, ndev), or null (one device: every
+// pair intra-device).  An intra-device pair (E') enters its device's LM system exactly (Gauss-Newton, R-N3a); an
+// inter-device pair (E'') is majorized by Prop. 1: P_ij on the camera's device, Q_ij on the point's (eq. Ealpha).
+struct Part {
+  const int32_t* cam_dev;
+  const int32_t* pt_dev;
+  int ndev;
+};
+__device__ __forceinline__ int cdev(const Part& P, int64_t i) { return P.cam_dev ? P.cam_dev[i] : 0; }
+__device__ __forceinline__ int pdev(const Part& P, int64_t j) { return P.pt_dev ? P.pt_dev[j] : 0; }
+__device__ __forceinline__ bool intra(const Part& P, int64_t i, int64_t j) {
+  return !P.cam_dev || P.cam_dev[i] == P.pt_dev[j];
+}
+
+// Anchor coefficients of pair (c_hat, l_hat, u) in the world frame (eqs. ray, lambdaij, error, w; P:L111-141,
+// L216-224): q = R p, v = l - t, lam, R e = q - lam v, w = rho'(|e|^2), rho; false if Assumption 2 fails.
+template <int LOSS>
+__device__ __forceinline__ bool pair_coef(const double* __restrict__ cam, const double* __restrict__ l, double2 u,
+                                          double eps2, double delta, double q[3], double v[3], double* lam,
+                                          double Re[3], double* w, double* rho) {
+  const double s = u.x * u.x + u.y * u.y;
+  const double pz = cam[12] + cam[13] * s + cam[14] * s * s;
+  for (int a = 0; a < 3; ++a) {
+    q[a] = cam[3 * a] * u.x + cam[3 * a + 1] * u.y + cam[3 * a + 2] * pz;
+    v[a] = l[a] - cam[9 + a];
+  }
+  const double nv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  if (!(nv > eps2)) return false;
+  *lam = (v[0] * q[0] + v[1] * q[1] + v[2] * q[2]) / nv;
+  for (int a = 0; a < 3; ++a) Re[a] = q[a] - *lam * v[a];
+  const double d2 = delta * delta;
+  *w = loss_eval<LOSS, true>(Re[0] * Re[0] + Re[1] * Re[1] + Re[2] * Re[2], delta, d2, 1.0 / d2, rho);
+  return true;
+}
 
 __device__ __forceinline__ int tri9(int r, int c) { return r * (r + 1) / 2 + c; }  // r >= c
 
@@ -65,11 +102,15 @@ __device__ bool pair_jacobians(const double* __restrict__ cam, const double* __r
 
 // One CTA per camera (observations sorted by camera): each thread sums its observations' w J_c^T J_c and
 // w J_c^T r in registers, the CTA reduces them in a fixed order; the point blocks go out by fp64 atomics.
+// Inter-device pairs (a partition): the camera side adds the Gauss-Newton system of P_ij = w |R p + lam t - g|^2
+// (exact: P is quadratic in the residual), 2 w J^T J and 2 w J^T (R e / 2) with J = [-[q]x, lam I, R e3 b^T]; the
+// point side adds Q_ij's, 2 w lam^2 I and -w lam R e (eq. Q: Q = w |lam l - g|^2 + a/2, lam l_hat - g = -R e / 2);
+// W_k = 0 (the pair couples no two variables of one device).
 template <int LOSS>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
     const double* __restrict__ cams, const double* __restrict__ pts, const int32_t* __restrict__ obs_pt,
-    const double2* __restrict__ uv, const int64_t* __restrict__ cam_off, double delta, double eps2, double* U,
-    double* gc, double* V, double* gl, double* W, double* Fpart) {
+    const double2* __restrict__ uv, const int64_t* __restrict__ cam_off, double delta, double eps2, Part part,
+    double* U, double* gc, double* V, double* gl, double* W, double* Fpart) {
   const int i = blockIdx.x;
   __shared__ double scam[15];
   if (threadIdx.x < 15) scam[threadIdx.x] = cams[(size_t)i * 15 + threadIdx.x];
@@ -84,6 +125,35 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
     const double l[3] = {pts[3 * (size_t)j], pts[3 * (size_t)j + 1], pts[3 * (size_t)j + 2]};
     double r[3], Jc[27], Jl[9];
     double* Wk = W ? W + (size_t)k * 27 : nullptr;
+    if (!intra(part, i, j)) {  // E'': majorized (Prop. 1)
+      if (Wk)
+        for (int e = 0; e < 27; ++e) Wk[e] = 0.0;
+      double q[3], v[3], lam, Re[3], w, rho;
+      if (!pair_coef<LOSS>(scam, l, uv[k], eps2, delta, q, v, &lam, Re, &w, &rho)) continue;  // R-N3d
+      Fsum += 0.5 * rho;  // P + Q = F at the anchor (Prop. 1)
+      const double s = uv[k].x * uv[k].x + uv[k].y * uv[k].y;
+      const double b[3] = {1.0, s, s * s};
+      // J = [-[q]x, lam I, R e3 b^T] (3 x 9, row-major)
+      double J[27];
+      const double mq[9] = {0, q[2], -q[1], -q[2], 0, q[0], q[1], -q[0], 0};
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) {
+          J[9 * a + c] = mq[3 * a + c];
+          J[9 * a + 3 + c] = a == c ? lam : 0.0;
+          J[9 * a + 6 + c] = scam[3 * a + 2] * b[c];
+        }
+#pragma unroll
+      for (int a = 0; a < 9; ++a) {
+#pragma unroll
+        for (int c = 0; c <= a; ++c) acc[tri9(a, c)] += 2.0 * w * (J[a] * J[c] + J[9 + a] * J[9 + c] + J[18 + a] * J[18 + c]);
+        acc[45 + a] += w * (J[a] * Re[0] + J[9 + a] * Re[1] + J[18 + a] * Re[2]);
+      }
+      for (int a = 0; a < 3; ++a) {
+        atomicAdd(V + 9 * (size_t)j + 4 * a, 2.0 * w * lam * lam);
+        atomicAdd(gl + 3 * (size_t)j + a, -w * lam * Re[a]);
+      }
+      continue;
+    }
     if (!pair_jacobians(scam, l, uv[k], eps2, r, Jc, Jl)) {  // R-N3d: the pair contributes nothing
       if (Wk)
         for (int e = 0; e < 27; ++e) Wk[e] = 0.0;
@@ -159,6 +229,67 @@ __global__ void k_coarse_mirror(double* V, int64_t N) {
 }  // namespace
 }  // namespace daba
 
+namespace daba {
+namespace {
+// Input checks on the device before any kernel writes (round-1 advisor: bad indices must not reach the atomics):
+// obs_pt in [0, N); obs_cam (when given) in [0, M) and inside its camera's cam_off segment; cam_off monotone from 0
+// to K; device ids in [0, ndev).  err (device int) receives a bit mask.
+__global__ void k_coarse_validate(const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M,
+                                  int64_t N, int64_t K, Part part, int* err) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < K) {
+    if (obs_pt[t] < 0 || obs_pt[t] >= N) atomicOr(err, 1);
+    if (obs_cam) {
+      const int32_t i = obs_cam[t];
+      if (i < 0 || i >= M)
+        atomicOr(err, 2);
+      else if (t < cam_off[i] || t >= cam_off[i + 1])
+        atomicOr(err, 4);
+    }
+  }
+  if (t < M && cam_off[t] > cam_off[t + 1]) atomicOr(err, 8);
+  if (t == 0 && (cam_off[0] != 0 || cam_off[M] != K)) atomicOr(err, 16);
+  if (t < M && part.cam_dev && (part.cam_dev[t] < 0 || part.cam_dev[t] >= part.ndev)) atomicOr(err, 32);
+  if (t < N && part.pt_dev && (part.pt_dev[t] < 0 || part.pt_dev[t] >= part.ndev)) atomicOr(err, 32);
+}
+
+// 0 if the inputs are consistent, -1 if not, -3 on a CUDA error (synchronises the stream)
+int validate(const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N, int64_t K,
+             Part part, cudaStream_t st) {
+  int* d = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int), st) != cudaSuccess) return -3;
+  cudaMemsetAsync(d, 0, sizeof(int), st);
+  const int64_t n = std::max<int64_t>(std::max<int64_t>(K, M + 1), N);
+  if (n > 0) k_coarse_validate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(obs_cam, obs_pt, cam_off, M, N, K, part, d);
+  int h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -3;
+  return h ? -1 : 0;
+}
+
+int coarse_blocks_impl(const double* cams, int64_t M, const double* pts, int64_t N, const int32_t* obs_pt,
+                       const double2* uv, const int64_t* cam_off, int loss, double scale, double eps2, Part part,
+                       double* U, double* gc, double* V, double* gl, double* W, double* F_cam, cudaStream_t st) {
+  if (N > 0) {
+    if (cudaMemsetAsync(V, 0, (size_t)N * 9 * sizeof(double), st) != cudaSuccess) return -3;
+    if (cudaMemsetAsync(gl, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
+  }
+  if (M > 0) {
+    const dim3 g((unsigned)M), b(kCoarseThreads);
+    if (loss == kHuber)
+      k_coarse_blocks<kHuber><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+    else if (loss == kCauchy)
+      k_coarse_blocks<kCauchy><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+    else
+      k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+  }
+  if (N > 0) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+}  // namespace
+}  // namespace daba
+
 extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* pts, int64_t N,
                                   const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
                                   int loss, double scale, double eps, double* U, double* gc, double* V, double* gl,
@@ -169,23 +300,11 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
       (K > 0 && (!obs_pt || !obs_uv)))
     return -1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (N > 0) {
-    if (cudaMemsetAsync(V, 0, (size_t)N * 9 * sizeof(double), st) != cudaSuccess) return -3;
-    if (cudaMemsetAsync(gl, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
-  }
-  if (M > 0) {
-    const double2* uv = reinterpret_cast<const double2*>(obs_uv);
-    const double eps2 = eps * eps;
-    const dim3 g((unsigned)M), b(kCoarseThreads);
-    if (loss == kHuber)
-      k_coarse_blocks<kHuber><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, U, gc, V, gl, W, F_cam);
-    else if (loss == kCauchy)
-      k_coarse_blocks<kCauchy><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, U, gc, V, gl, W, F_cam);
-    else
-      k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, U, gc, V, gl, W, F_cam);
-  }
-  if (N > 0) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  const Part one{nullptr, nullptr, 1};
+  int rc = M > 0 ? validate(nullptr, obs_pt, cam_off, M, N, K, one, st) : 0;
+  if (rc) return rc;
+  return coarse_blocks_impl(cams, M, pts, N, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, loss, scale,
+                            eps * eps, one, U, gc, V, gl, W, F_cam, st);
 }
 
 // ------------------------------------------------------------------ the damped LM direction by Schur complement + PCG
@@ -247,6 +366,7 @@ struct WSrc {
   const double2* uv;
   int loss;
   double delta, eps2;
+  Part part;  // inter-device pairs have W_k = 0
 };
 
 __device__ __forceinline__ void get_W(const WSrc& s, int64_t k, const double* cam, int32_t j, double Wk[27]) {
@@ -287,14 +407,14 @@ __device__ __forceinline__ bool get_J(const WSrc& s, int64_t k, const double* ca
 }
 
 __global__ void k_cs_points(const double* __restrict__ V, const double* __restrict__ gl, int64_t N, double xi,
-                            double mu, CS w, int* bad) {
+                            double mu, CS w, int* bad, Part part) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= N) return;
   double A[9], Ai[9];
   for (int e = 0; e < 9; ++e) A[e] = V[9 * j + e];
   for (int a = 0; a < 3; ++a) A[4 * a] = (A[4 * a] + xi) * (1.0 + mu);
   if (!spd_inverse<3>(A, Ai)) {
-    atomicAdd(bad, 1);
+    atomicAdd(bad + pdev(part, j), 1);  // a failed trial of that device (R-N3c)
     for (int e = 0; e < 9; ++e) Ai[e] = 0.0;
   }
   for (int e = 0; e < 9; ++e) w.Vinv[9 * j + e] = Ai[e];
@@ -316,6 +436,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_cs_cams(const double* __rest
   for (int k = 0; k < kUCols; ++k) acc[k] = 0.0;
   for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
     const int32_t j = obs_pt[k];
+    if (!intra(ws.part, i, j)) continue;  // W_k = 0
     double Wk[27];
     get_W(ws, k, scam, j, Wk);
     const double* Vi = w.Vinv + 9 * (size_t)j;
@@ -362,13 +483,13 @@ __global__ void __launch_bounds__(kCoarseThreads) k_cs_cams(const double* __rest
 }
 
 // In-place inverse of each camera's 9x9 diagonal block of S (the block-Jacobi preconditioner), one thread each.
-__global__ void k_cs_inv(int64_t M, CS w, int* bad) {
+__global__ void k_cs_inv(int64_t M, CS w, int* bad, Part part) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M) return;
   double D[81], Di[81];
   for (int e = 0; e < 81; ++e) D[e] = w.Pinv[i * 81 + e];
   if (!spd_inverse<9>(D, Di)) {
-    atomicAdd(bad, 1);
+    atomicAdd(bad + cdev(part, i), 1);
     for (int e = 0; e < 81; ++e) Di[e] = 0.0;
   }
   for (int e = 0; e < 81; ++e) w.Pinv[i * 81 + e] = Di[e];
@@ -409,6 +530,7 @@ __global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
   const int32_t i = obs_cam[k], j = obs_pt[k];
+  if (!intra(ws.part, i, j)) return;  // W_k = 0
   const double* vi = v + 9 * (size_t)i;
   if (!ws.W) {  // w J_l^T (J_c v)
     double Jc[27], Jl[9], w;
@@ -446,6 +568,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 4) k_cs_pass2(const double* __
   for (int a = 0; a < 9; ++a) acc[a] = 0.0;
   for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
     const int32_t j = obs_pt[k];
+    if (!intra(ws.part, i, j)) continue;  // W_k = 0
     const double* Vi = w.Vinv + 9 * (size_t)j;
     const double* tj = w.t + 3 * (size_t)j;
     double u[3];
@@ -556,10 +679,12 @@ extern "C" int64_t daba_coarse_solve_workspace(int64_t M, int64_t N) {
 
 namespace daba {
 namespace {
+// bad_dev (host, kMaxDev): per device, how many damped blocks were not positive definite (a failed trial of that
+// device, R-N3c); the system is block diagonal over the devices, so the other devices' directions are unaffected.
 int coarse_solve_impl(const double* U, const double* gc, const double* V, const double* gl, WSrc ws,
                       const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N,
                       int64_t K, double xi, double mu, int max_iter, double tol, double* dc, double* dl, double* work,
-                      double info[2], void* stream) {
+                      double info[2], int bad_dev[kMaxDev], void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CS w;
   double* o = work;
@@ -578,10 +703,10 @@ int coarse_solve_impl(const double* U, const double* gc, const double* V, const 
   const unsigned gM = (unsigned)((M + T - 1) / T), gN = (unsigned)((N + T - 1) / T), gK = (unsigned)((K + T - 1) / T),
                  g9M = (unsigned)((9 * M + T - 1) / T);
   if (cudaMemsetAsync(w.s, 0, (S_COLS + 8) * sizeof(double), st) != cudaSuccess) return -3;
-  if (N > 0) k_cs_points<<<gN, T, 0, st>>>(V, gl, N, xi, mu, w, bad);
+  if (N > 0) k_cs_points<<<gN, T, 0, st>>>(V, gl, N, xi, mu, w, bad, ws.part);
   if (M > 0) {
     k_cs_cams<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, gc, ws, obs_pt, cam_off, xi, mu, w, bad);
-    k_cs_inv<<<(unsigned)((M + 63) / 64), 64, 0, st>>>(M, w, bad);
+    k_cs_inv<<<(unsigned)((M + 63) / 64), 64, 0, st>>>(M, w, bad, ws.part);
     k_cs_init<<<gM, T, 0, st>>>(M, w);
   }
   k_cs_start<<<1, 1, 0, st>>>(w);
@@ -600,14 +725,12 @@ int coarse_solve_impl(const double* U, const double* gc, const double* V, const 
     if (K > 0 && M > 0) k_cs_pass1<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, dc, w.t, w.s, 0);
     k_cs_backsub<<<gN, T, 0, st>>>(gl, N, w, dl);
   }
-  double s[S_COLS + 1];
-  if (cudaMemcpyAsync(s, w.s, (S_COLS + 1) * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -3;
+  double s[S_COLS + 4];
+  if (cudaMemcpyAsync(s, w.s, (S_COLS + 4) * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -3;
   if (cudaStreamSynchronize(st) != cudaSuccess) return -3;
-  int nbad;
-  memcpy(&nbad, &s[S_COLS], sizeof nbad);
+  memcpy(bad_dev, &s[S_COLS], sizeof(int) * kMaxDev);
   info[0] = s[S_ITERS];
   info[1] = s[S_RZ0] > 0 ? sqrt(s[S_RZ] / s[S_RZ0]) : 0.0;
-  if (nbad) return -6;  // a damped block is not positive definite: a failed LM trial (R-N3c)
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 }  // namespace
@@ -623,9 +746,15 @@ extern "C" int daba_coarse_solve(const double* U, const double* gc, const double
   if ((M > 0 && (!U || !gc || !cam_off || !dc || !work)) || (N > 0 && (!V || !gl || !dl || !work)) ||
       (K > 0 && (!W || !obs_cam || !obs_pt)))
     return -1;
-  WSrc ws{W, nullptr, nullptr, nullptr, 0, 1.0, 0.0};
-  return coarse_solve_impl(U, gc, V, gl, ws, obs_cam, obs_pt, cam_off, M, N, K, xi, mu, max_iter, tol, dc, dl, work,
-                           info, stream);
+  WSrc ws{W, nullptr, nullptr, nullptr, 0, 1.0, 0.0, Part{nullptr, nullptr, 1}};
+  if (M > 0) {
+    const int v = validate(obs_cam, obs_pt, cam_off, M, N, K, ws.part, static_cast<cudaStream_t>(stream));
+    if (v) return v;
+  }
+  int bad[kMaxDev];
+  const int rc = coarse_solve_impl(U, gc, V, gl, ws, obs_cam, obs_pt, cam_off, M, N, K, xi, mu, max_iter, tol, dc, dl,
+                                   work, info, bad, stream);
+  return rc ? rc : (bad[0] ? -6 : 0);  // a damped block not positive definite: a failed LM trial (R-N3c)
 }
 
 namespace daba {
@@ -777,6 +906,125 @@ __global__ void k_cr_retract(const double* ch, const double* lh, const double* d
   if (e < 3 * N) l[e] = lh[e] + dl[e];
 }
 
+// Per camera: the camera's share of E^a(x | x_hat) - E^a(x_hat | x_hat) for every device a (eq. Ealpha): intra-
+// device pairs F_k(x) - F_k(x_hat) (E', exact) and the camera's proximal term on its device; inter-device pairs by
+// the anchor-relative forms of eqs. P / Q (reading Q21) — dP = w dr.(dr + R e) with dr = R'p(d') - R_hat p(d_hat)
+// + lam (t' - t_hat) on the camera's device, dQ = w (lam dl).(lam dl - R e) on the point's.  The terms of device a
+// depend on device a's variables only.  One CTA per camera, fixed-order reduction -> dEc[i * kMaxDev + a].
+template <int LOSS>
+__global__ void __launch_bounds__(kCoarseThreads) k_cr_dE(const double* __restrict__ c, const double* __restrict__ l,
+                                                          const double* __restrict__ ch, const double* __restrict__ lh,
+                                                          const int32_t* __restrict__ obs_pt,
+                                                          const double2* __restrict__ uv,
+                                                          const int64_t* __restrict__ cam_off, double delta,
+                                                          double eps2, double xi, Part part, double* dEc) {
+  const int i = blockIdx.x;
+  __shared__ double sc[15], sh[15];
+  if (threadIdx.x < 15) {
+    sc[threadIdx.x] = c[(size_t)i * 15 + threadIdx.x];
+    sh[threadIdx.x] = ch[(size_t)i * 15 + threadIdx.x];
+  }
+  __syncthreads();
+  const int di = cdev(part, i);
+  const double d2 = delta * delta, id2 = 1.0 / d2;
+  double acc[kMaxDev];
+#pragma unroll
+  for (int a = 0; a < kMaxDev; ++a) acc[a] = 0.0;
+  for (int64_t k = cam_off[i] + threadIdx.x; k < cam_off[i + 1]; k += kCoarseThreads) {
+    const int32_t j = obs_pt[k];
+    const double lx[3] = {l[3 * (size_t)j], l[3 * (size_t)j + 1], l[3 * (size_t)j + 2]};
+    const double lhx[3] = {lh[3 * (size_t)j], lh[3 * (size_t)j + 1], lh[3 * (size_t)j + 2]};
+    const double2 u = uv[k];
+    if (intra(part, i, j)) {  // E': F_k(x) - F_k(x_hat) (eq. Fij; a degenerate pair contributes 0, Q17)
+      double r[3], rho1 = 0.0, rho0 = 0.0;
+      if (pair_residual(sc, lx, u, eps2, r)) loss_eval<LOSS, true>(r[0] * r[0] + r[1] * r[1] + r[2] * r[2], delta, d2, id2, &rho1);
+      if (pair_residual(sh, lhx, u, eps2, r)) loss_eval<LOSS, true>(r[0] * r[0] + r[1] * r[1] + r[2] * r[2], delta, d2, id2, &rho0);
+      acc[di] += 0.5 * rho1 - 0.5 * rho0;
+      continue;
+    }
+    double q[3], v[3], lam, Re[3], w, rho;
+    if (!pair_coef<LOSS>(sh, lhx, u, eps2, delta, q, v, &lam, Re, &w, &rho)) continue;  // R-N3d
+    const double s = u.x * u.x + u.y * u.y;
+    const double pz = sc[12] + sc[13] * s + sc[14] * s * s;
+    double dP = 0.0, dQ = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      const double qn = sc[3 * a] * u.x + sc[3 * a + 1] * u.y + sc[3 * a + 2] * pz;
+      const double dr = (qn - q[a]) + lam * (sc[9 + a] - sh[9 + a]);
+      dP += dr * (dr + Re[a]);
+      const double m = lam * (lx[a] - lhx[a]);
+      dQ += m * (m - Re[a]);
+    }
+    acc[di] += w * dP;
+    acc[pdev(part, j)] += w * dQ;
+  }
+  __shared__ double red[kCoarseThreads / 32][kMaxDev];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < kMaxDev; ++a) {
+    double x = acc[a];
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    if (lane == 0) red[warp][a] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < part.ndev) {
+    const int a = threadIdx.x;
+    double x = 0.0;
+    for (int v = 0; v < kCoarseThreads / 32; ++v) x += red[v][a];
+    if (a == di) {  // the camera's proximal term (reading Q7: |R - R_hat|_F^2 + |t - t_hat|^2 + |d - d_hat|^2)
+      double pr = 0.0;
+      for (int e = 0; e < 15; ++e) pr += (sc[e] - sh[e]) * (sc[e] - sh[e]);
+      x += 0.5 * xi * pr;
+    }
+    dEc[(size_t)i * kMaxDev + a] = x;
+  }
+}
+
+// The points' proximal terms per device: per-block partials over grid-stride ranges (fixed order).
+__global__ void __launch_bounds__(256) k_cr_dE_pts(const double* __restrict__ l, const double* __restrict__ lh,
+                                                   int64_t N, double xi, Part part, double* part_out) {
+  double acc[kMaxDev];
+#pragma unroll
+  for (int a = 0; a < kMaxDev; ++a) acc[a] = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int a = 0; a < 3; ++a) d += (l[3 * j + a] - lh[3 * j + a]) * (l[3 * j + a] - lh[3 * j + a]);
+    acc[pdev(part, j)] += 0.5 * xi * d;
+  }
+  __shared__ double red[8][kMaxDev];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < kMaxDev; ++a) {
+    double x = acc[a];
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    if (lane == 0) red[warp][a] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxDev) {
+    double x = 0.0;
+    for (int v = 0; v < (int)blockDim.x / 32; ++v) x += red[v][threadIdx.x];
+    part_out[(size_t)blockIdx.x * kMaxDev + threadIdx.x] = x;
+  }
+}
+
+// out[a] = sum_i dEc[i][a] + sum_b pp[b][a], fixed order (one block, a per warp)
+__global__ void k_cr_dE_final(const double* dEc, int64_t M, const double* pp, int nb, int ndev, double* out) {
+  const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a >= ndev) return;
+  double x = 0.0;
+  for (int64_t i = lane; i < M; i += 32) x += dEc[(size_t)i * kMaxDev + a];
+  for (int b = lane; b < nb; b += 32) x += pp[(size_t)b * kMaxDev + a];
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+  if (lane == 0) out[a] = x;
+}
+
+// co/lo take the trial's value of every variable whose device bit is set in mask
+__global__ void k_cr_take(const double* ct, const double* lt, int64_t M, int64_t N, Part part, unsigned mask,
+                          double* co, double* lo) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < 15 * M && (mask >> cdev(part, e / 15) & 1u)) co[e] = ct[e];
+  if (e < 3 * N && (mask >> pdev(part, e / 3) & 1u)) lo[e] = lt[e];
+}
+
 struct Run {
   int64_t M, N, K;
   const int32_t *oc, *op;
@@ -786,11 +1034,14 @@ struct Run {
   double scale, eps2, eps, xi, mu0, mu_up;
   int trials, pcg_iter;
   double pcg_tol;
-  double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal;
+  Part part;
+  double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal, *dEc;
   cudaStream_t st;
 };
+constexpr int kDEBlocks = 148;
 
-int run_F(const Run& R, const double* c, const double* l, const double* ch, const double* lh, double* out) {
+// F(x) = sum_k F_k (eq. Fobj), fixed order
+int run_F(const Run& R, const double* c, const double* l, double* out) {
   if (R.M > 0) {
     if (R.loss == kHuber)
       k_cr_F<kHuber><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
@@ -799,139 +1050,258 @@ int run_F(const Run& R, const double* c, const double* l, const double* ch, cons
     else
       k_cr_F<kTrivial><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
   }
-  k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, c, ch, R.N, l, lh, R.scal + 8);
+  k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, c, nullptr, R.N, l, nullptr, R.scal + 8);
   k_cr_eval_final<<<1, 256, 0, R.st>>>(R.scal + 8, kEvalBlocks, R.xi, R.scal);
   if (cudaMemcpyAsync(out, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess) return -3;
   return cudaStreamSynchronize(R.st) == cudaSuccess ? 0 : -3;
 }
 
-// One successful LM step on E(. | anchor) = F + xi/2 |. - anchor|^2 from the anchor (R-N3c); out = the accepted
-// trial or the anchor.  *trial = accepted trial index or -1.
-// E0_known: E(anchor | anchor) = F(anchor) if the caller has it (the x^k anchor: F(x^k)), else NaN — then it is
-// summed from the blocks kernel's per-camera F.  *E_out: E of the accepted trial (E0 if none), i.e. E(x_new | anchor).
-int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
-            int* trial, double E0_known, double* E_out) {
-  int rc = daba_coarse_blocks(ca, R.M, la, R.N, R.op, reinterpret_cast<const double*>(R.uv), R.off, R.K, R.loss,
-                              R.scale, R.eps, R.U, R.gc, R.V, R.gl, nullptr, R.Fc, R.st);  // W recomputed in the PCG
-  if (rc) return rc;
-  double E0 = E0_known;
-  if (!(E0 == E0)) {  // NaN: sum the anchor's per-camera F written by the blocks kernel
-    k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, nullptr, nullptr, R.N, nullptr, nullptr, R.scal + 8);
-    k_cr_eval_final<<<1, 256, 0, R.st>>>(R.scal + 8, kEvalBlocks, R.xi, R.scal);
-    if (cudaMemcpyAsync(&E0, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess ||
-        cudaStreamSynchronize(R.st) != cudaSuccess)
-      return -3;
+// dE[a] = E^a(x | x_hat) - E^a(x_hat | x_hat) for every device a (host, kMaxDev)
+int run_dE(const Run& R, const double* c, const double* l, const double* ch, const double* lh, double dE[kMaxDev]) {
+  if (R.M > 0) {
+    if (R.loss == kHuber)
+      k_cr_dE<kHuber><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, ch, lh, R.op, R.uv, R.off, R.scale, R.eps2, R.xi, R.part, R.dEc);
+    else if (R.loss == kCauchy)
+      k_cr_dE<kCauchy><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, ch, lh, R.op, R.uv, R.off, R.scale, R.eps2, R.xi, R.part, R.dEc);
+    else
+      k_cr_dE<kTrivial><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, ch, lh, R.op, R.uv, R.off, R.scale, R.eps2, R.xi, R.part, R.dEc);
   }
-  *E_out = E0;
-  *trial = -1;
-  double mu = R.mu0;
-  const unsigned g = (unsigned)((std::max(R.M, 3 * R.N) + 255) / 256);
-  for (int tau = 0; tau < R.trials; ++tau, mu *= R.mu_up) {
-    double info[2];
-    const WSrc ws{nullptr, ca, la, R.uv, R.loss, R.scale, R.eps2};
-    rc = coarse_solve_impl(R.U, R.gc, R.V, R.gl, ws, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter, R.pcg_tol,
-                           R.dcv, R.dlv, R.work, info, R.st);
-    if (rc == -6) continue;  // a damped block not positive definite: a failed trial
-    if (rc) return rc;
-    if (g) k_cr_retract<<<g, 256, 0, R.st>>>(ca, la, R.dcv, R.dlv, R.M, R.N, ct, lt);
-    double E;
-    if ((rc = run_F(R, ct, lt, ca, la, &E))) return rc;
-    if (E - E0 < 0) {
-      *trial = tau;
-      *E_out = E;
-      break;
-    }
-  }
-  const double* cs = *trial >= 0 ? ct : ca;
-  const double* ls = *trial >= 0 ? lt : la;
-  if (R.M && cudaMemcpyAsync(co, cs, R.M * 15 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
-    return -3;
-  if (R.N && cudaMemcpyAsync(lo, ls, R.N * 3 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
-    return -3;
+  double* pp = R.scal + 8 + 2 * kEvalBlocks;
+  k_cr_dE_pts<<<kDEBlocks, 256, 0, R.st>>>(l, lh, R.N, R.xi, R.part, pp);
+  k_cr_dE_final<<<1, 32 * kMaxDev, 0, R.st>>>(R.dEc, R.M, pp, kDEBlocks, R.part.ndev, R.scal);
+  double h[kMaxDev];
+  if (cudaMemcpyAsync(h, R.scal, sizeof(double) * R.part.ndev, cudaMemcpyDeviceToHost, R.st) != cudaSuccess) return -3;
+  if (cudaStreamSynchronize(R.st) != cudaSuccess) return -3;
+  for (int a = 0; a < kMaxDev; ++a) dE[a] = a < R.part.ndev ? h[a] : 0.0;
   return 0;
 }
 
-}  // namespace
-}  // namespace daba
+// One successful LM step per device from the anchor (ca, la) (readings R-N3a..d): the devices' systems are
+// block diagonal (E'' pairs couple no two variables of one device), so one PCG solves all of them; a trial round
+// uses mu = mu0 mu_up^tau for every device still without an accepted trial (each device's own schedule).  co/lo:
+// every device's accepted trial (its own variables) or the anchor; trial[a]: the accepted trial index or -1;
+// dE[a] = E^a(x_new | anchor) - E^a(anchor | anchor) (0 if none accepted).
+int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
+            int trial[kMaxDev], double dE[kMaxDev]) {
+  int rc = coarse_blocks_impl(ca, R.M, la, R.N, R.op, R.uv, R.off, R.loss, R.scale, R.eps2, R.part, R.U, R.gc, R.V,
+                              R.gl, nullptr, R.Fc, R.st);  // W recomputed in the PCG passes
+  if (rc) return rc;
+  if (R.M && cudaMemcpyAsync(co, ca, R.M * 15 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    return -3;
+  if (R.N && cudaMemcpyAsync(lo, la, R.N * 3 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    return -3;
+  for (int a = 0; a < kMaxDev; ++a) {
+    trial[a] = -1;
+    dE[a] = 0.0;
+  }
+  double mu = R.mu0;
+  const unsigned g = (unsigned)((std::max(15 * R.M, 3 * R.N) + 255) / 256);
+  for (int tau = 0; tau < R.trials; ++tau, mu *= R.mu_up) {
+    double info[2], dEt[kMaxDev];
+    int bad[kMaxDev];
+    const WSrc ws{nullptr, ca, la, R.uv, R.loss, R.scale, R.eps2, R.part};
+    rc = coarse_solve_impl(R.U, R.gc, R.V, R.gl, ws, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter,
+                           R.pcg_tol, R.dcv, R.dlv, R.work, info, bad, R.st);
+    if (rc) return rc;
+    if (g) k_cr_retract<<<g, 256, 0, R.st>>>(ca, la, R.dcv, R.dlv, R.M, R.N, ct, lt);
+    if ((rc = run_dE(R, ct, lt, ca, la, dEt))) return rc;
+    unsigned mask = 0;
+    bool open = false;
+    for (int a = 0; a < R.part.ndev; ++a) {
+      if (trial[a] >= 0) continue;
+      if (!bad[a] && dEt[a] < 0) {  // strict decrease of E^a: accepted ("one successful inner LM step")
+        trial[a] = tau;
+        dE[a] = dEt[a];
+        mask |= 1u << a;
+      } else {
+        open = true;
+      }
+    }
+    if (mask && g) k_cr_take<<<g, 256, 0, R.st>>>(ct, lt, R.M, R.N, R.part, mask, co, lo);
+    if (!open) break;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
 
-extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
-                               const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
-                               int loss, double scale, double eps, double xi, double eta, double mu0, double mu_up,
-                               int lm_trials, int accelerate, int pcg_max_iter, double pcg_tol, int n_iters,
-                               double* trace, void* stream) {
-  using namespace daba;
-  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || n_iters < 0 || !(scale > 0) || !(eps >= 0) || !(xi > 0) ||
-      !(eta > 0 && eta <= 1) || !(mu0 >= 0) || !(mu_up >= 1) || lm_trials < 1 || pcg_max_iter < 1 ||
-      !(pcg_tol >= 0) || loss < 0 || loss > 2)
-    return -1;
-  if ((M > 0 && (!cams || !cam_off)) || (N > 0 && !pts) || (K > 0 && (!obs_cam || !obs_pt || !obs_uv)))
-    return -1;
-  Run R{M, N, K, obs_cam, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, loss, scale, eps * eps, eps, xi,
-        mu0, mu_up, lm_trials, pcg_max_iter, pcg_tol};
-  R.st = static_cast<cudaStream_t>(stream);
+int coarse_run_impl(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam, const int32_t* obs_pt,
+                    const double* obs_uv, const int64_t* cam_off, int64_t K, Part part, const daba_coarse_options& o,
+                    int n_iters, double* trace, int32_t* trials_out, cudaStream_t st) {
+  Run R{M, N, K, obs_cam, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, o.loss, o.scale,
+        o.eps * o.eps, o.eps, o.xi, o.mu0, o.mu_up, o.lm_trials, o.pcg_max_iter, o.pcg_tol, part};
+  R.st = st;
   const size_t nc = (size_t)M * 15, nl = (size_t)N * 3;
-  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9) + (size_t)N * (9 + 3 + 3) +
-                       (size_t)daba_coarse_solve_workspace(M, N) + 8 + 2 * kEvalBlocks;
+  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)N * (9 + 3 + 3) +
+                       (size_t)daba_coarse_solve_workspace(M, N) + 8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev;
   double* base = nullptr;
-  // scratch from the retained pool: mapping ~1.6 GB afresh on every call (Final-13682) cost more than an iteration
+  // scratch from the retained pool (mapping ~1.6 GB afresh per call at Final-13682 cost ~300 ms); unless
+  // keep_scratch, the pool is trimmed back to its previous reservation afterwards
   int device = 0;
   cudaGetDevice(&device);
   cudaMemPool_t pool = shared_pool(device);
-  if ((pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, R.st)
-            : cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), R.st)) != cudaSuccess)
+  uint64_t reserved0 = 0;
+  if (pool) cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved0);
+  if ((pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, st)
+            : cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), st)) != cudaSuccess)
     return -5;
-  double* o = base;
-  auto take = [&](size_t n) { double* p = o; o += n; return p; };
+  double* op = base;
+  auto take = [&](size_t n) { double* p = op; op += n; return p; };
   double *cp = take(nc), *lp = take(nl), *cb = take(nc), *lb = take(nl), *ca = take(nc), *la = take(nl),
          *cm = take(nc), *lm = take(nl), *ct = take(nc), *lt = take(nl);
   R.U = take((size_t)M * 81);
   R.gc = take((size_t)M * 9);
   R.Fc = take((size_t)M);
   R.dcv = take((size_t)M * 9);
+  R.dEc = take((size_t)M * kMaxDev);
   R.V = take((size_t)N * 9);
   R.gl = take((size_t)N * 3);
   R.dlv = take((size_t)N * 3);
   R.W = nullptr;
   R.work = take((size_t)daba_coarse_solve_workspace(M, N));
-  R.scal = take(8 + 2 * kEvalBlocks);
+  R.scal = take(8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev);
   int rc = 0;
   // x^{-1} = x^0 (eq. Fainit); F-bar^{-1} = F(x^0) (A18, global form); s^0 = 1
-  if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
-      cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+  if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     rc = -3;
   double Fbar = 0.0, s = 1.0;
-  if (!rc) rc = run_F(R, cams, pts, nullptr, nullptr, &Fbar);
+  if (!rc) rc = run_F(R, cams, pts, &Fbar);
   const unsigned g = (unsigned)((std::max(M, 3 * N) + 255) / 256);
   for (int it = 0; it < n_iters && !rc; ++it) {
     const double s_next = (sqrt(4.0 * s * s + 1.0) + 1.0) / 2.0;  // eq. nesterov_scalar, Alg. 1
-    const double gamma = accelerate ? (s - 1.0) / s_next : 0.0;
-    if (g) k_cr_extrapolate<<<g, 256, 0, R.st>>>(cams, cp, pts, lp, M, N, gamma, cb, lb);
-    double Fk, Eacc, Emm;
-    int ta, tm;
-    if ((rc = run_F(R, cams, pts, nullptr, nullptr, &Fk))) break;
-    Fbar = (1.0 - eta) * Fbar + eta * Fk;  // eq. lFak
-    double Ebar;
-    if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, &ta, NAN, &Ebar))) break;  // eq. update_amm
-    if ((rc = lm_step(R, cams, pts, cm, lm, ct, lt, &tm, Fk, &Emm))) break;  // eq. update_mm; Emm = E(x_mm | x^k)
-    if ((rc = run_F(R, ca, la, cams, pts, &Eacc))) break;                   // E(x_acc | x^k), eq. Eak
-    const bool restart = accelerate ? (Eacc > Fbar) : true;         // Alg. 1, strict ">"
+    const double gamma = o.accelerate ? (s - 1.0) / s_next : 0.0;
+    double Fk;
+    if ((rc = run_F(R, cams, pts, &Fk))) break;
+    Fbar = (1.0 - o.eta) * Fbar + o.eta * Fk;  // eq. lFak
+    int ta[kMaxDev], tm[kMaxDev];
+    double dEa[kMaxDev], dEm[kMaxDev], Eacc = NAN, Emm = NAN;
+    bool restart = true;
+    for (int a = 0; a < kMaxDev; ++a) ta[a] = tm[a] = -1;
+    if (o.accelerate) {
+      if (g) k_cr_extrapolate<<<g, 256, 0, st>>>(cams, cp, pts, lp, M, N, gamma, cb, lb);
+      if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, ta, dEa))) break;  // eq. update_amm
+      if ((rc = run_dE(R, ca, la, cams, pts, dEa))) break;           // E(x_acc | x^k) - F(x^k), eq. Eak
+      Eacc = Fk;
+      for (int a = 0; a < part.ndev; ++a) Eacc += dEa[a];
+      restart = Eacc > Fbar;  // Alg. 1, strict ">"
+    }
+    if (restart || o.mm_always) {  // eq. update_mm: only needed when the restart fires (Alg. 1)
+      if ((rc = lm_step(R, cams, pts, cm, lm, ct, lt, tm, dEm))) break;
+      Emm = Fk;
+      for (int a = 0; a < part.ndev; ++a) Emm += dEm[a];  // E(x_mm | x^k)
+    }
+    if (!o.accelerate) Eacc = Emm;  // gamma = 0: x-bar = x^k, the two subproblems coincide
     if (trace) {
       double* t = trace + 5 * (size_t)it;
       t[0] = Fk;
       t[1] = Fbar;
       t[2] = Eacc;
-      t[3] = (accelerate && restart) ? 1.0 : 0.0;
+      t[3] = (o.accelerate && restart) ? 1.0 : 0.0;
       t[4] = Emm;
     }
+    if (trials_out)
+      for (int a = 0; a < part.ndev; ++a) {
+        trials_out[(size_t)it * 2 * part.ndev + a] = ta[a];
+        trials_out[(size_t)it * 2 * part.ndev + part.ndev + a] = tm[a];
+      }
     // x^{k-1} <- x^k, x^k <- x^{k+1}
-    if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
-        cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
-        cudaMemcpyAsync(cams, restart ? cm : ca, nc * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess ||
-        cudaMemcpyAsync(pts, restart ? lm : la, nl * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
+    if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(cams, restart ? cm : ca, nc * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(pts, restart ? lm : la, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       rc = -3;
     s = s_next;
   }
-  cudaFreeAsync(base, R.st);
-  if (cudaStreamSynchronize(R.st) != cudaSuccess && !rc) rc = -3;
+  cudaFreeAsync(base, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = -3;
+  if (pool && !o.keep_scratch) cudaMemPoolTrimTo(pool, (size_t)reserved0);
   return rc;
+}
+
+}  // namespace
+}  // namespace daba
+
+extern "C" void daba_coarse_default_options(daba_coarse_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->loss = DABA_LOSS_TRIVIAL;
+  o->scale = 1.0;
+  o->eps = 1e-8;
+  o->xi = 1e-4;
+  o->eta = 0.1;
+  o->mu0 = 1e-3;
+  o->mu_up = 10.0;
+  o->lm_trials = 5;
+  o->accelerate = 1;
+  o->pcg_max_iter = 10;
+  o->pcg_tol = 1e-2;
+  o->mm_always = 0;
+  o->keep_scratch = 0;
+}
+
+// The device the caller's arrays live on becomes current for the call (round-1 advisor): pools, scratch and launches
+// then all belong to it; the previous device is restored.
+namespace {
+struct DeviceOf {
+  int prev = -1;
+  explicit DeviceOf(const void* ptr) {
+    cudaPointerAttributes at{};
+    if (ptr && cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+      cudaGetDevice(&prev);
+      if (prev == at.device) prev = -1;
+      else cudaSetDevice(at.device);
+    }
+    cudaGetLastError();
+  }
+  ~DeviceOf() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+extern "C" int daba_coarse_run_part(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
+                                    const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
+                                    const int32_t* cam_dev, const int32_t* pt_dev, int ndev,
+                                    const daba_coarse_options* opt, int n_iters, double* trace, int32_t* trials,
+                                    void* stream) {
+  using namespace daba;
+  if (!opt) return -1;
+  const daba_coarse_options& o = *opt;
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || n_iters < 0 || !(o.scale > 0) || !(o.eps >= 0) || !(o.xi > 0) ||
+      !(o.eta > 0 && o.eta <= 1) || !(o.mu0 >= 0) || !(o.mu_up >= 1) || o.lm_trials < 1 || o.pcg_max_iter < 1 ||
+      !(o.pcg_tol >= 0) || o.loss < 0 || o.loss > 2 || ndev < 1 || ndev > kMaxDev || (!cam_dev != !pt_dev) ||
+      (ndev > 1 && !cam_dev))
+    return -1;
+  if ((M > 0 && (!cams || !cam_off)) || (N > 0 && !pts) || (K > 0 && (!obs_cam || !obs_pt || !obs_uv))) return -1;
+  DeviceOf on(cams ? static_cast<const void*>(cams) : static_cast<const void*>(pts));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Part part{cam_dev, pt_dev, ndev};
+  if (M > 0) {
+    const int v = validate(obs_cam, obs_pt, cam_off, M, N, K, part, st);
+    if (v) return v;
+  }
+  return coarse_run_impl(cams, M, pts, N, obs_cam, obs_pt, obs_uv, cam_off, K, part, o, n_iters, trace, trials, st);
+}
+
+extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
+                               const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
+                               int loss, double scale, double eps, double xi, double eta, double mu0, double mu_up,
+                               int lm_trials, int accelerate, int pcg_max_iter, double pcg_tol, int n_iters,
+                               double* trace, void* stream) {
+  daba_coarse_options o;
+  daba_coarse_default_options(&o);
+  o.loss = loss;
+  o.scale = scale;
+  o.eps = eps;
+  o.xi = xi;
+  o.eta = eta;
+  o.mu0 = mu0;
+  o.mu_up = mu_up;
+  o.lm_trials = lm_trials;
+  o.accelerate = accelerate;
+  o.pcg_max_iter = pcg_max_iter;
+  o.pcg_tol = pcg_tol;
+  o.mm_always = 1;  // the one-device entry keeps its trace: E(x_mm | x^k) every iteration
+  o.keep_scratch = 1;
+  return daba_coarse_run_part(cams, M, pts, N, obs_cam, obs_pt, obs_uv, cam_off, K, nullptr, nullptr, 1, &o, n_iters,
+                              trace, nullptr, stream);
 }

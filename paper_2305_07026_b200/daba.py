@@ -44,7 +44,16 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_reset_kernel_times", "daba_launches_per_iteration", "daba_last_error", "daba_destroy",
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
-           "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve", "daba_coarse_run"]
+           "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve", "daba_coarse_run",
+           "daba_coarse_default_options", "daba_coarse_run_part"]
+
+
+class CoarseOptions(ctypes.Structure):
+    """daba_coarse_options (include/daba.h)."""
+    _fields_ = [("loss", ctypes.c_int), ("scale", ctypes.c_double), ("eps", ctypes.c_double), ("xi", ctypes.c_double),
+                ("eta", ctypes.c_double), ("mu0", ctypes.c_double), ("mu_up", ctypes.c_double),
+                ("lm_trials", ctypes.c_int), ("accelerate", ctypes.c_int), ("pcg_max_iter", ctypes.c_int),
+                ("pcg_tol", ctypes.c_double), ("mm_always", ctypes.c_int), ("keep_scratch", ctypes.c_int)]
 
 
 def lib():
@@ -97,6 +106,10 @@ def lib():
                                         ctypes.c_double, V, V, V, V, V]
         D = ctypes.c_double
         L.daba_coarse_run.argtypes = [V, I64, V, I64, V, V, V, V, I64, I32, D, D, D, D, D, D, I32, I32, I32, D, I32, V, V]
+        L.daba_coarse_default_options.argtypes = [ctypes.POINTER(CoarseOptions)]
+        L.daba_coarse_default_options.restype = None
+        L.daba_coarse_run_part.argtypes = [V, I64, V, I64, V, V, V, V, I64, V, V, I32, ctypes.POINTER(CoarseOptions),
+                                           I32, V, V, V]
         L.daba_bal_read.argtypes = [ctypes.c_char_p, V, V, V, V, V, V]
         L.daba_bal_write.argtypes = [ctypes.c_char_p, V, I64, V, I64, V, V, V, I64]
         L.daba_bal_last_error.argtypes = []
@@ -191,6 +204,25 @@ def paper_to_bal(cams, obs_uv):
     return _convert(lib().daba_paper_to_bal, cams, obs_uv)
 
 
+def _coarse_check(what, cams=None, pts=None, obs_cam=None, obs_pt=None, obs_uv=None, cam_off=None, extra=()):
+    """Argument marshalling checks of the coarse entry points: contiguous CUDA tensors of the documented dtypes and
+    shapes (the C side checks the index VALUES on the device)."""
+    import torch
+    f64, i32, i64 = torch.float64, torch.int32, torch.int64
+    M = cams.shape[0] if cams is not None else None
+    K = obs_pt.shape[0] if obs_pt is not None else None
+    spec = [(cams, f64, (M, 15)), (pts, f64, (pts.shape[0], 3) if pts is not None else None),
+            (obs_cam, i32, (K,)), (obs_pt, i32, (K,)), (obs_uv, f64, (K, 2)),
+            (cam_off, i64, (M + 1,) if M is not None else None)] + list(extra)
+    for t, dt, shape in spec:
+        if t is None:
+            continue
+        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+            raise DabaError(-1, f"{what}: contiguous CUDA tensors of the documented dtypes required")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise DabaError(-1, f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
 def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1.0, eps=1e-8, stream=None):
     """daba_coarse_blocks (include/daba.h): the Gauss-Newton blocks of the intra-device penalties.
     Inputs are CUDA tensors already on the device (torch: device memory only): cams (M, 15) fp64 native layout,
@@ -199,18 +231,16 @@ def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1
     asynchronous on `stream` (default: torch's current stream)."""
     import torch
     M, N, K = cams.shape[0], pts.shape[0], obs_pt.shape[0]
-    for t, dt in ((cams, torch.float64), (pts, torch.float64), (obs_uv, torch.float64), (obs_pt, torch.int32),
-                  (cam_off, torch.int64)):
-        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
-            raise DabaError(-1, "coarse_blocks: contiguous CUDA tensors of the documented dtypes required")
+    _coarse_check("coarse_blocks", cams=cams, pts=pts, obs_pt=obs_pt, obs_uv=obs_uv, cam_off=cam_off)
     dev, f64 = cams.device, torch.float64
     U, gc = torch.empty((M, 9, 9), dtype=f64, device=dev), torch.empty((M, 9), dtype=f64, device=dev)
     V, gl = torch.empty((N, 3, 3), dtype=f64, device=dev), torch.empty((N, 3), dtype=f64, device=dev)
     W, F = torch.empty((K, 9, 3), dtype=f64, device=dev), torch.empty((M,), dtype=f64, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    rc = lib().daba_coarse_blocks(cams.data_ptr(), M, pts.data_ptr(), N, obs_pt.data_ptr(), obs_uv.data_ptr(),
-                                  cam_off.data_ptr(), K, int(loss), float(scale), float(eps), U.data_ptr(),
-                                  gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(), F.data_ptr(), st)
+    with torch.cuda.device(dev):
+        rc = lib().daba_coarse_blocks(cams.data_ptr(), M, pts.data_ptr(), N, obs_pt.data_ptr(), obs_uv.data_ptr(),
+                                      cam_off.data_ptr(), K, int(loss), float(scale), float(eps), U.data_ptr(),
+                                      gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(), F.data_ptr(), st)
     if rc != 0:
         raise DabaError(rc, "daba_coarse_blocks")
     return U, gc, V, gl, W, F
@@ -222,19 +252,23 @@ def coarse_solve(blocks, obs_cam, obs_pt, cam_off, xi=1e-4, mu=1e-3, max_iter=50
     import torch
     U, gc, V, gl, W, _ = blocks
     M, N, K = U.shape[0], V.shape[0], W.shape[0]
-    for t, dt in ((obs_cam, torch.int32), (obs_pt, torch.int32), (cam_off, torch.int64)):
-        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
-            raise DabaError(-1, "coarse_solve: contiguous CUDA tensors of the documented dtypes required")
+    f64 = torch.float64
+    _coarse_check("coarse_solve", obs_cam=obs_cam, obs_pt=obs_pt,
+                  extra=[(cam_off, torch.int64, (M + 1,)), (U, f64, (M, 9, 9)), (gc, f64, (M, 9)), (V, f64, (N, 3, 3)),
+                         (gl, f64, (N, 3)), (W, f64, (K, 9, 3))])
+    if obs_pt.shape[0] != K:
+        raise DabaError(-1, "coarse_solve: obs_pt and W disagree on K")
     dev = U.device
     dc = torch.zeros((M, 9), dtype=torch.float64, device=dev)
     dl = torch.zeros((N, 3), dtype=torch.float64, device=dev)
     work = torch.empty((max(1, lib().daba_coarse_solve_workspace(M, N)),), dtype=torch.float64, device=dev)
     info = np.zeros(2)
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    rc = lib().daba_coarse_solve(U.data_ptr(), gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(),
-                                 obs_cam.data_ptr(), obs_pt.data_ptr(), cam_off.data_ptr(), M, N, K, float(xi), float(mu),
-                                 int(max_iter), float(tol), dc.data_ptr(), dl.data_ptr(), work.data_ptr(),
-                                 info.ctypes.data, st)
+    with torch.cuda.device(dev):
+        rc = lib().daba_coarse_solve(U.data_ptr(), gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(),
+                                     obs_cam.data_ptr(), obs_pt.data_ptr(), cam_off.data_ptr(), M, N, K, float(xi),
+                                     float(mu), int(max_iter), float(tol), dc.data_ptr(), dl.data_ptr(), work.data_ptr(),
+                                     info.ctypes.data, st)
     if rc != 0:
         raise DabaError(rc, "daba_coarse_solve")
     return dc, dl, (int(info[0]), float(info[1]))
@@ -246,20 +280,58 @@ def coarse_run(cams, pts, obs_cam, obs_pt, obs_uv, cam_off, n_iters, loss=LOSS_T
     """daba_coarse_run (include/daba.h; SURVEY NEXT-3 at one device): n_iters DABA iterations with the coarse
     surrogate.  cams (M, 15) / pts (N, 3) CUDA fp64 tensors are updated in place; returns the (n_iters, 5) trace."""
     import torch
-    for t, dt in ((cams, torch.float64), (pts, torch.float64), (obs_uv, torch.float64), (obs_cam, torch.int32),
-                  (obs_pt, torch.int32), (cam_off, torch.int64)):
-        if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
-            raise DabaError(-1, "coarse_run: contiguous CUDA tensors of the documented dtypes required")
+    _coarse_check("coarse_run", cams=cams, pts=pts, obs_cam=obs_cam, obs_pt=obs_pt, obs_uv=obs_uv, cam_off=cam_off)
     tr = np.zeros((n_iters, 5))
     st = stream if stream is not None else torch.cuda.current_stream(cams.device).cuda_stream
-    rc = lib().daba_coarse_run(cams.data_ptr(), cams.shape[0], pts.data_ptr(), pts.shape[0], obs_cam.data_ptr(),
-                               obs_pt.data_ptr(), obs_uv.data_ptr(), cam_off.data_ptr(), obs_pt.shape[0], int(loss),
-                               float(scale), float(eps), float(xi), float(eta), float(mu0), float(mu_up),
-                               int(lm_trials), int(accelerate), int(pcg_max_iter), float(pcg_tol), int(n_iters),
-                               tr.ctypes.data, st)
+    with torch.cuda.device(cams.device):
+        rc = lib().daba_coarse_run(cams.data_ptr(), cams.shape[0], pts.data_ptr(), pts.shape[0], obs_cam.data_ptr(),
+                                   obs_pt.data_ptr(), obs_uv.data_ptr(), cam_off.data_ptr(), obs_pt.shape[0],
+                                   int(loss), float(scale), float(eps), float(xi), float(eta), float(mu0), float(mu_up),
+                                   int(lm_trials), int(accelerate), int(pcg_max_iter), float(pcg_tol), int(n_iters),
+                                   tr.ctypes.data, st)
     if rc != 0:
         raise DabaError(rc, "daba_coarse_run")
     return tr
+
+
+def coarse_options(**kw):
+    """daba_coarse_options with the library defaults (daba_coarse_default_options) overridden by kw."""
+    o = CoarseOptions()
+    lib().daba_coarse_default_options(ctypes.byref(o))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown coarse option {k}")
+        setattr(o, k, v)
+    return o
+
+
+def coarse_run_part(cams, pts, obs_cam, obs_pt, obs_uv, cam_off, n_iters, cam_dev=None, pt_dev=None, ndev=None,
+                    stream=None, **opts):
+    """daba_coarse_run_part (include/daba.h): n_iters DABA iterations with the coarse surrogate over
+    the device partition (cam_dev (M,), pt_dev (N,) int32 CUDA tensors, or None for one device).  cams / pts are
+    updated in place; returns (trace (n_iters, 5), accepted trials (n_iters, 2, ndev))."""
+    import torch
+    M, N = cams.shape[0], pts.shape[0]
+    _coarse_check("coarse_run_part", cams=cams, pts=pts, obs_cam=obs_cam, obs_pt=obs_pt, obs_uv=obs_uv,
+                  cam_off=cam_off,
+                  extra=[(cam_dev, torch.int32, (M,)), (pt_dev, torch.int32, (N,))])
+    if (cam_dev is None) != (pt_dev is None):
+        raise DabaError(-1, "coarse_run_part: cam_dev and pt_dev go together")
+    if ndev is None:
+        ndev = 1 if cam_dev is None else int(max(cam_dev.max().item() if M else 0, pt_dev.max().item() if N else 0)) + 1
+    o = coarse_options(**opts)
+    tr = np.zeros((n_iters, 5))
+    trials = np.zeros((n_iters, 2, ndev), np.int32)
+    st = stream if stream is not None else torch.cuda.current_stream(cams.device).cuda_stream
+    with torch.cuda.device(cams.device):
+        rc = lib().daba_coarse_run_part(cams.data_ptr(), M, pts.data_ptr(), N, obs_cam.data_ptr(), obs_pt.data_ptr(),
+                                        obs_uv.data_ptr(), cam_off.data_ptr(), obs_pt.shape[0],
+                                        cam_dev.data_ptr() if cam_dev is not None else None,
+                                        pt_dev.data_ptr() if pt_dev is not None else None, int(ndev), ctypes.byref(o),
+                                        int(n_iters), tr.ctypes.data, trials.ctypes.data, st)
+    if rc != 0:
+        raise DabaError(rc, "daba_coarse_run_part")
+    return tr, trials
 
 
 class Plan:

@@ -210,3 +210,132 @@ def test_coarse_run_isolated_camera_and_point():
     # unchanged up to the rounding of ProjRot3D in the extrapolation (x-bar of a variable with x^k = x^{k-1})
     np.testing.assert_allclose(c1[-1], cams[-1], rtol=0, atol=1e-13 * np.abs(cams[-1]).max())
     np.testing.assert_array_equal(l1[-1], pts[-1])
+
+
+# ---------------------------------------------------------------- NEXT-3 over a device partition
+def _run_part_gpu(cp, iters, cam_dev=None, pt_dev=None, **opts):
+    import paper_2305_07026_b200 as daba
+    dev = torch.device("cuda:0")
+    order = np.argsort(cp.oc, kind="stable")
+    cam_off = np.concatenate([[0], np.cumsum(np.bincount(cp.oc, minlength=cp.M))]).astype(np.int64)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
+    cams, pts = t(cp.cams0, torch.float64), t(cp.pts0, torch.float64)
+    cd = t(cam_dev, torch.int32) if cam_dev is not None else None
+    pd = t(pt_dev, torch.int32) if pt_dev is not None else None
+    kw = dict(loss=cp.opt.kind, scale=cp.opt.scale, xi=cp.opt.xi, eta=cp.opt.eta, pcg_max_iter=2000, pcg_tol=1e-15,
+              mm_always=1)
+    kw.update(opts)
+    tr, trials = daba.coarse_run_part(cams, pts, t(cp.oc[order], torch.int32), t(cp.op[order], torch.int32),
+                                      t(cp.uv[order], torch.float64), t(cam_off, torch.int64), iters, cam_dev=cd,
+                                      pt_dev=pd, **kw)
+    return tr, trials, cams.cpu().numpy(), pts.cpu().numpy()
+
+
+def _partition(p, ndev, kind, seed=0):
+    rng = np.random.default_rng(seed)
+    if kind == "random":
+        return rng.integers(0, ndev, p.M), rng.integers(0, ndev, p.N)
+    # contiguous camera ranges; each point with the device owning most of its observations (ties: lowest)
+    cam_dev = (np.arange(p.M) * ndev) // p.M
+    cnt = np.zeros((p.N, ndev), int)
+    np.add.at(cnt, (p.obs_pt, cam_dev[p.obs_cam]), 1)
+    return cam_dev, cnt.argmax(axis=1)
+
+
+@pytest.mark.parametrize("ndev,kind,loss,eta", [(2, "contiguous", oracle.LOSS_HUBER, 0.1),
+                                                (3, "random", oracle.LOSS_CAUCHY, 1.0),
+                                                (2, "random", oracle.LOSS_TRIVIAL, 1.0)])
+def test_coarse_run_partitioned_matches_the_oracle(ndev, kind, loss, eta):
+    """daba_coarse_run_part (eq. Ealpha: E' pairs exact in their device's LM step, E'' pairs majorized by P on the
+    camera's device and Q on the point's; each device accepts its own first decreasing trial) against
+    oracle/coarse.run with the same device assignment: restart flags identical, F / F-bar / E traces within 1e-9,
+    states within 1e-7 of their scale after 8 iterations."""
+    p = gen.generate("tiny_seq", loss=loss, outlier_frac=0.05 if loss else 0.0)
+    cam_dev, pt_dev = _partition(p, ndev, kind, seed=ndev)
+    cp = coarse.Problem(p, cam_dev, pt_dev, eta=eta)
+    assert 0 < cp.intra.sum() < cp.K  # both kinds of pairs occur
+    tr_ref, c_ref, l_ref = coarse.run(cp, 8)
+    tr, trials, c, l = _run_part_gpu(cp, 8, cam_dev, pt_dev)
+    np.testing.assert_array_equal(tr[:, 3], tr_ref[:, 3])
+    for col in (0, 1, 2, 4):
+        np.testing.assert_allclose(tr[:, col], tr_ref[:, col], rtol=1e-9)
+    assert np.abs(c - c_ref).max() <= 1e-7 * np.abs(c_ref).max()
+    assert np.abs(l - l_ref).max() <= 1e-7 * np.abs(l_ref).max()
+    assert trials.shape == (8, 2, ndev) and (trials[:, 1] >= 0).any()
+    assert tr[-1, 0] < tr[0, 0]
+
+
+def test_coarse_run_one_device_entries_agree():
+    """daba_coarse_run is daba_coarse_run_part with one device (mm_always = 1)."""
+    import paper_2305_07026_b200 as daba
+    p = gen.generate("tiny_seq", loss=oracle.LOSS_HUBER, outlier_frac=0.05)
+    cp = coarse.Problem(p, np.zeros(p.M, int), np.zeros(p.N, int))
+    tr1, _, c1, l1 = _run_part_gpu(cp, 6)
+    dev = torch.device("cuda:0")
+    order = np.argsort(cp.oc, kind="stable")
+    cam_off = np.concatenate([[0], np.cumsum(np.bincount(cp.oc, minlength=cp.M))]).astype(np.int64)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
+    cams, pts = t(cp.cams0, torch.float64), t(cp.pts0, torch.float64)
+    tr0 = daba.coarse_run(cams, pts, t(cp.oc[order], torch.int32), t(cp.op[order], torch.int32),
+                          t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 6, loss=cp.opt.kind,
+                          scale=cp.opt.scale, pcg_max_iter=2000, pcg_tol=1e-15)
+    # (the PCG sums with fp64 atomics: two runs agree to rounding, not bitwise — include/daba.h)
+    np.testing.assert_array_equal(tr1[:, 3], tr0[:, 3])
+    np.testing.assert_allclose(tr1, tr0, rtol=1e-10)
+    np.testing.assert_allclose(c1, cams.cpu().numpy(), rtol=0, atol=1e-10 * np.abs(c1).max())
+
+
+@pytest.mark.parametrize("ndev", [1, 2])
+def test_coarse_run_mm_only_on_restart(ndev):
+    """mm_always = 0 solves the MM subproblem only when the restart fires (Alg. 1): the same iterates as
+    solving it every iteration, E(x_mm | x^k) reported only on restarts."""
+    p = gen.generate("tiny_seq", loss=oracle.LOSS_HUBER, outlier_frac=0.05)
+    cam_dev, pt_dev = _partition(p, ndev, "contiguous")
+    cp = coarse.Problem(p, cam_dev, pt_dev, eta=1.0)
+    kw = dict(cam_dev=cam_dev, pt_dev=pt_dev) if ndev > 1 else {}
+    tra, _, ca, la = _run_part_gpu(cp, 10, mm_always=1, **kw)
+    trb, trials_b, cb, lb = _run_part_gpu(cp, 10, mm_always=0, **kw)
+    rs = tra[:, 3] == 1
+    assert rs.any() and (~rs).any()
+    np.testing.assert_array_equal(trb[:, 3], tra[:, 3])
+    np.testing.assert_allclose(trb[:, :3], tra[:, :3], rtol=1e-10)  # (rounding: fp64 atomics in the PCG)
+    np.testing.assert_allclose(trb[rs, 4], tra[rs, 4], rtol=1e-10)
+    assert np.all(np.isnan(trb[~rs, 4])) and np.all(trials_b[~rs, 1] == -1)
+    np.testing.assert_allclose(cb, ca, rtol=0, atol=1e-10 * np.abs(ca).max())
+    np.testing.assert_allclose(lb, la, rtol=0, atol=1e-10 * np.abs(la).max())
+
+
+def test_coarse_entries_reject_bad_indices_before_writing():
+    """Index values are checked on the device before any kernel writes: an out-of-range point index, a camera
+    segment table that does not end at K, a device id out of range -> DABA_E_INVALID_ARG, state untouched."""
+    import paper_2305_07026_b200 as daba
+    p = gen.generate("tiny_seq")
+    cp = coarse.Problem(p, np.zeros(p.M, int), np.zeros(p.N, int))
+    dev = torch.device("cuda:0")
+    order = np.argsort(cp.oc, kind="stable")
+    cam_off = np.concatenate([[0], np.cumsum(np.bincount(cp.oc, minlength=cp.M))]).astype(np.int64)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
+    op_bad = cp.op[order].copy()
+    op_bad[3] = cp.N
+    off_bad = cam_off.copy()
+    off_bad[-1] -= 1
+    cases = [(op_bad, cam_off, None), (cp.op[order], off_bad, None),
+             (cp.op[order], cam_off, (np.full(cp.M, 2), np.zeros(cp.N, int)))]
+    for op, off, part in cases:
+        cams, pts = t(cp.cams0, torch.float64), t(cp.pts0, torch.float64)
+        kw = {}
+        if part is not None:
+            kw = dict(cam_dev=t(part[0], torch.int32), pt_dev=t(part[1], torch.int32), ndev=2)
+        with pytest.raises(daba.DabaError) as e:
+            daba.coarse_run_part(cams, pts, t(cp.oc[order], torch.int32), t(op, torch.int32),
+                                 t(cp.uv[order], torch.float64), t(off, torch.int64), 2, **kw)
+        assert e.value.code == -1
+        np.testing.assert_array_equal(cams.cpu().numpy(), cp.cams0)
+        np.testing.assert_array_equal(pts.cpu().numpy(), cp.pts0)
+    with pytest.raises(daba.DabaError) as e:
+        daba.coarse_blocks(t(cp.cams0, torch.float64), t(cp.pts0, torch.float64), t(op_bad, torch.int32),
+                           t(cp.uv[order], torch.float64), t(cam_off, torch.int64))
+    assert e.value.code == -1
+    with pytest.raises(daba.DabaError):  # BAL-layout (M, 9) cameras: caught by the shape check
+        daba.coarse_run_part(t(p.cams, torch.float64), t(cp.pts0, torch.float64), t(cp.oc[order], torch.int32),
+                             t(cp.op[order], torch.int32), t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 1)
