@@ -270,6 +270,11 @@ int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32
  * atomics: results are reproducible to rounding, not bitwise.  Scratch comes from the library's stream-ordered
  * pool; keep_scratch = 0 trims the pool back afterwards.  Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3),
  * DABA_E_OOM (-5). */
+/* The native camera layout of the coarse entry points from the ABI's BAL layout (host arrays, M x 9 -> M x 15:
+ * R = Exp(aa)^T camera->world row-major, t = -R t_w2c the centre, d = (f, f k1, f k2); reading D4 — the conversion
+ * daba_create applies).  0 or DABA_E_INVALID_ARG. */
+int daba_bal_to_native(const double* cameras_bal, int64_t M, double* cameras_native);
+
 typedef struct {
   int loss;          /* 0 trivial, 1 Huber, 2 Cauchy */
   double scale, eps; /* loss scale delta (> 0); Assumption 2 threshold */

@@ -498,6 +498,16 @@ void native_to_bal(const double* c, double* b) {
 }  // namespace daba
 
 // ====================================================================== C-ABI
+extern "C" int daba_bal_to_native(const double* cameras_bal, int64_t M, double* cameras_native) {
+  if (M < 0 || (M > 0 && (!cameras_bal || !cameras_native))) return DABA_E_INVALID_ARG;
+  for (int64_t i = 0; i < M; ++i) {
+    double tmp[16];
+    daba::bal_to_native(cameras_bal + 9 * i, tmp);
+    std::memcpy(cameras_native + 15 * i, tmp, 15 * sizeof(double));
+  }
+  return DABA_OK;
+}
+
 extern "C" void daba_default_options(daba_options* o) {
   if (!o) return;
   std::memset(o, 0, sizeof *o);

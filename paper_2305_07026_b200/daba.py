@@ -45,7 +45,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
            "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve", "daba_coarse_run",
-           "daba_coarse_default_options", "daba_coarse_run_part"]
+           "daba_coarse_default_options", "daba_coarse_run_part", "daba_bal_to_native"]
 
 
 class CoarseOptions(ctypes.Structure):
@@ -106,6 +106,7 @@ def lib():
                                         ctypes.c_double, V, V, V, V, V]
         D = ctypes.c_double
         L.daba_coarse_run.argtypes = [V, I64, V, I64, V, V, V, V, I64, I32, D, D, D, D, D, D, I32, I32, I32, D, I32, V, V]
+        L.daba_bal_to_native.argtypes = [V, I64, V]
         L.daba_coarse_default_options.argtypes = [ctypes.POINTER(CoarseOptions)]
         L.daba_coarse_default_options.restype = None
         L.daba_coarse_run_part.argtypes = [V, I64, V, I64, V, V, V, V, I64, V, V, I32, ctypes.POINTER(CoarseOptions),
@@ -292,6 +293,16 @@ def coarse_run(cams, pts, obs_cam, obs_pt, obs_uv, cam_off, n_iters, loss=LOSS_T
     if rc != 0:
         raise DabaError(rc, "daba_coarse_run")
     return tr
+
+
+def bal_to_native(cams):
+    """BAL cameras (M, 9) -> the native layout (M, 15) of the coarse entry points (daba_bal_to_native)."""
+    c = _c(cams, np.float64).reshape(-1, 9)
+    out = np.empty((c.shape[0], 15))
+    rc = lib().daba_bal_to_native(c.ctypes.data, c.shape[0], out.ctypes.data)
+    if rc:
+        raise DabaError(rc, "daba_bal_to_native")
+    return out
 
 
 def coarse_options(**kw):
