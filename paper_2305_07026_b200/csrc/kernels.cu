@@ -146,7 +146,7 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   const double rx = fma(c[0], u.x, fma(c[1], u.y, c[2] * pz));
   const double ry = fma(c[3], u.x, fma(c[4], u.y, c[5] * pz));
   const double rz = fma(c[6], u.x, fma(c[7], u.y, c[8] * pz));
-  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * __drcp_rn(nv);  // eq. gamma
+  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * rcp_d(nv);  // eq. gamma
   const double ex = fma(-lam, vx, rx), ey = fma(-lam, vy, ry), ez = fma(-lam, vz, rz);  // R e (eq. error)
   const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
   double rho = 0;
@@ -492,7 +492,7 @@ __device__ __forceinline__ void pt_terms(const double* cam, double lx, double ly
   const double vx = lx - cam[9], vy = ly - cam[10], vz = lz - cam[11];
   const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
   if (!(nv > p.eps2)) return;
-  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * __drcp_rn(nv);  // eq. gamma
+  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * rcp_d(nv);  // eq. gamma
   const double ex = fma(-lam, vx, rx), ey = fma(-lam, vy, ry), ez = fma(-lam, vz, rz);  // R e (eq. error)
   const double w = loss_eval<LOSS, false>(fma(ex, ex, fma(ey, ey, ez * ez)), p.delta, p.delta2, p.idelta2, nullptr);
   const double wl = w * lam;
