@@ -556,7 +556,13 @@ def test_long_trace_spans_the_device_ring():
         trg = s.iterate_trace(1300)
     rel = np.abs(trg[:, 0] - tro[:, 0]) / np.abs(tro[:, 0])
     assert rel.max() <= 1e-9, (rel.max(), int(rel.argmax()))
-    np.testing.assert_array_equal(trg[:, D.daba.TR_RESTART][:200], tro[:, oracle.TR_RESTART][:200])
+    # Restart decisions: identical wherever the oracle's test E_acc > F-bar is not a near tie (reading Q23).  Near
+    # convergence (F falls ~1e4x on this noiseless-ish problem) E_acc and F-bar agree to ~1e-10 and both
+    # candidates are within rounding of each other, so a flipped near-tie decision does not move the trajectory.
+    Eacc, Fb = tro[:, oracle.TR_EACC], tro[:, oracle.TR_FBAR]
+    tie = np.abs(Eacc - Fb) <= 1e-9 * np.abs(Fb)
+    np.testing.assert_array_equal(trg[~tie, D.daba.TR_RESTART], tro[~tie, oracle.TR_RESTART])
+    assert (~tie[:200]).all()  # the first 200 decisions are all clear-cut
 
 
 @pytest.mark.parametrize("name", ["small_cauchy", "small_seq_huber"])
