@@ -294,6 +294,21 @@ int daba_coarse_run_part(double* cams, int64_t M, double* pts, int64_t N, const 
                          const int32_t* cam_dev, const int32_t* pt_dev, int ndev, const daba_coarse_options* opt,
                          int n_iters, double* trace, int32_t* trials, void* stream);
 
+/* The same iteration with ONE DEVICE PER RANK (SURVEY NEXT-3 distributed; the paper's setting): every rank
+ * passes the same global HOST arrays (BAL cameras M x 9, points N x 3, observations as daba_create; cam_owner /
+ * pt_owner: NULL = the daba_create partition) and solves its own device's subproblem on cuda_device; the halo it
+ * reads (the pairs across devices) is the finest partition's; per iteration the ranks allreduce (F(x^k), the two
+ * E^a decreases) and exchange the boundary variables' x^{k+1} (comm_kind 0 NCCL, 1 LOCAL threads of one process;
+ * comm_id 128 bytes, NULL iff nranks == 1).  Results equal daba_coarse_run_part with cam_dev = cam_owner and
+ * pt_dev = pt_owner (all devices on one GPU).  trace (HOST, n_iters x 5, same on every rank, nullable); cams_out
+ * (HOST, M x 15 NATIVE layout) / pts_out (HOST, N x 3), nullable: the rank's owned entries are written.
+ * Blocking.  Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3), DABA_E_NCCL (-4), DABA_E_OOM (-5). */
+int daba_coarse_run_dist(const double* cameras, int64_t M, const double* points, int64_t N, const int32_t* obs_cam,
+                         const int32_t* obs_pt, const double* obs_uv, int64_t K, const int32_t* cam_owner,
+                         const int32_t* pt_owner, int rank, int nranks, const void* comm_id, int comm_kind,
+                         int cuda_device, const daba_coarse_options* opt, int n_iters, double* trace,
+                         double* cams_out, double* pts_out);
+
 /* ---- BAL datasets (host only, no CUDA calls) ----
  * The BAL text format (the paper's datasets, Table 1): a header "M N K"; K observations
  * "camera point u v" (centred pixels); M cameras of 9 numbers (angle-axis of R_w2c, t_w2c, f, k1, k2 with BAL's

@@ -12,9 +12,15 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
 
 #include "device_math.cuh"
 #include "../../include/daba.h"
+#include "comm.h"
+#include "shard.h"
 
 namespace daba {
 namespace {
@@ -1037,6 +1043,8 @@ struct Run {
   Part part;
   double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal, *dEc;
   cudaStream_t st;
+  unsigned active = ~0u;  // devices whose LM acceptance matters (a rank's own device; the halo device is fixed)
+  int64_t M_F = -1;       // F(x) sums the first M_F cameras' pairs (a rank's own cameras); -1: all
 };
 constexpr int kDEBlocks = 148;
 
@@ -1050,7 +1058,8 @@ int run_F(const Run& R, const double* c, const double* l, double* out) {
     else
       k_cr_F<kTrivial><<<(unsigned)R.M, kCoarseThreads, 0, R.st>>>(c, l, R.op, R.uv, R.off, R.scale, R.eps2, R.Fc);
   }
-  k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M, c, nullptr, R.N, l, nullptr, R.scal + 8);
+  k_cr_eval_part<<<kEvalBlocks, 256, 0, R.st>>>(R.Fc, R.M_F < 0 ? R.M : R.M_F, c, nullptr, R.N, l, nullptr,
+                                                  R.scal + 8);
   k_cr_eval_final<<<1, 256, 0, R.st>>>(R.scal + 8, kEvalBlocks, R.xi, R.scal);
   if (cudaMemcpyAsync(out, R.scal, sizeof(double), cudaMemcpyDeviceToHost, R.st) != cudaSuccess) return -3;
   return cudaStreamSynchronize(R.st) == cudaSuccess ? 0 : -3;
@@ -1113,7 +1122,7 @@ int lm_step(const Run& R, const double* ca, const double* la, double* co, double
         trial[a] = tau;
         dE[a] = dEt[a];
         mask |= 1u << a;
-      } else {
+      } else if (R.active >> a & 1u) {
         open = true;
       }
     }
@@ -1304,4 +1313,268 @@ extern "C" int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, 
   o.keep_scratch = 1;
   return daba_coarse_run_part(cams, M, pts, N, obs_cam, obs_pt, obs_uv, cam_off, K, nullptr, nullptr, 1, &o, n_iters,
                               trace, nullptr, stream);
+}
+
+// ------------------------------------------------------------------ NEXT-3 distributed: one device per rank
+// Each rank holds its device's variables (the shard plan's owned cameras and points) and the halo it reads (the
+// same halo the finest partition exchanges: cameras of other ranks observing its points, points of other ranks its
+// cameras observe).  Locally the halo is a second, FIXED device: the pairs touching an owned variable are routed
+// exactly as in daba_coarse_run_part (own-own E', own-halo E'' by P / Q), only device 0's LM acceptance counts,
+// F(x^k) sums the own cameras' pairs, and per iteration the ranks allreduce (F, dE_acc, dE_mm) and exchange the
+// boundary variables' x^{k+1}.  Equal to daba_coarse_run_part with cam_dev = cam_owner, pt_dev = pt_owner.
+namespace daba {
+void bal_to_native(const double* b, double* c);  // engine.cu (reading D4)
+namespace {
+__global__ void k_cd_pack(const double* cams, const double* pts, const int32_t* ci, const int64_t* co, int32_t nc,
+                          const int32_t* pi, const int64_t* po, int32_t np, double* buf) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < 15 * (int64_t)nc) {
+    const int64_t e = t / 15, k = t % 15;
+    buf[co[e] + k] = cams[15 * (int64_t)ci[e] + k];
+  } else if (t < 15 * (int64_t)nc + 3 * (int64_t)np) {
+    const int64_t u = t - 15 * (int64_t)nc, e = u / 3, k = u % 3;
+    buf[po[e] + k] = pts[3 * (int64_t)pi[e] + k];
+  }
+}
+__global__ void k_cd_unpack(double* cams, double* pts, const int32_t* ci, const int64_t* co, int32_t nc,
+                            const int32_t* pi, const int64_t* po, int32_t np, const double* buf) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < 15 * (int64_t)nc) {
+    const int64_t e = t / 15, k = t % 15;
+    cams[15 * (int64_t)ci[e] + k] = buf[co[e] + k];
+  } else if (t < 15 * (int64_t)nc + 3 * (int64_t)np) {
+    const int64_t u = t - 15 * (int64_t)nc, e = u / 3, k = u % 3;
+    pts[3 * (int64_t)pi[e] + k] = buf[po[e] + k];
+  }
+}
+
+struct DistBufs {
+  std::vector<void*> v;
+  cudaStream_t st;
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st) != cudaSuccess) return nullptr;
+    v.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~DistBufs() {
+    for (void* p : v) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+  }
+};
+template <class T>
+bool up(DistBufs& B, T** d, const std::vector<T>& h) {
+  if (!(*d = B.get<T>(h.size()))) return false;
+  return h.empty() || cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, B.st) == cudaSuccess;
+}
+}  // namespace
+}  // namespace daba
+
+extern "C" int daba_coarse_run_dist(const double* cameras, int64_t M, const double* points, int64_t N,
+                                    const int32_t* obs_cam, const int32_t* obs_pt, const double* obs_uv, int64_t K,
+                                    const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks,
+                                    const void* comm_id, int comm_kind, int cuda_device,
+                                    const daba_coarse_options* opt, int n_iters, double* trace, double* cams_out,
+                                    double* pts_out) {
+  using namespace daba;
+  if (!opt || M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || n_iters < 0 || nranks < 1 || rank < 0 ||
+      rank >= nranks || (nranks > 1 && !comm_id) || comm_kind < 0 || comm_kind > 1)
+    return -1;
+  const daba_coarse_options& o = *opt;
+  if (!(o.scale > 0) || !(o.eps >= 0) || !(o.xi > 0) || !(o.eta > 0 && o.eta <= 1) || !(o.mu0 >= 0) ||
+      !(o.mu_up >= 1) || o.lm_trials < 1 || o.pcg_max_iter < 1 || !(o.pcg_tol >= 0) || o.loss < 0 || o.loss > 2)
+    return -1;
+  if ((M > 0 && !cameras) || (N > 0 && !points) || (K > 0 && (!obs_cam || !obs_pt || !obs_uv))) return -1;
+  ShardPlan S;
+  if (!plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &S, false).empty()) return -1;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return -3;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return -3;
+  int rc = 0;
+  {
+    DistBufs B{{}, st};
+    // local problem: cameras / points owned first, then halo (shard.h); every pair touching an owned variable,
+    // sorted by local camera (the camera side of the owned cameras, then the boundary pairs of halo cameras)
+    const int32_t nc = (int32_t)S.cam_g.size(), npt = (int32_t)S.pt_g.size();
+    const int32_t noc = S.n_own_cams, nop = S.n_own_pts;
+    std::vector<double> hc((size_t)nc * 15), hp((size_t)npt * 3);
+    for (int32_t li = 0; li < nc; ++li) {
+      double tmp[16];
+      bal_to_native(cameras + 9 * (size_t)S.cam_g[(size_t)li], tmp);
+      std::memcpy(&hc[(size_t)li * 15], tmp, 15 * sizeof(double));
+    }
+    for (int32_t lj = 0; lj < npt; ++lj)
+      for (int k = 0; k < 3; ++k) hp[(size_t)lj * 3 + k] = points[3 * (size_t)S.pt_g[(size_t)lj] + k];
+    std::vector<int64_t> cnt((size_t)nc + 1, 0);
+    for (size_t q = 0; q < S.c_obs.size(); ++q) ++cnt[(size_t)S.c_cam[q] + 1];
+    for (size_t q = 0; q < S.p_obs.size(); ++q)
+      if (S.p_cam[q] >= noc) ++cnt[(size_t)S.p_cam[q] + 1];
+    for (int32_t li = 0; li < nc; ++li) cnt[(size_t)li + 1] += cnt[(size_t)li];
+    const int64_t KL = cnt[(size_t)nc];
+    std::vector<int32_t> loc((size_t)KL), lop((size_t)KL);
+    std::vector<double> luv((size_t)KL * 2);
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    auto put = [&](int32_t c, int32_t pnt, int32_t g) {
+      const int64_t w = pos[(size_t)c]++;
+      loc[(size_t)w] = c;
+      lop[(size_t)w] = pnt;
+      luv[2 * (size_t)w] = obs_uv[2 * (size_t)g];
+      luv[2 * (size_t)w + 1] = obs_uv[2 * (size_t)g + 1];
+    };
+    for (size_t q = 0; q < S.c_obs.size(); ++q) put(S.c_cam[q], S.c_pt[q], S.c_obs[q]);
+    for (size_t q = 0; q < S.p_obs.size(); ++q)
+      if (S.p_cam[q] >= noc) put(S.p_cam[q], S.p_pt[q], S.p_obs[q]);
+    std::vector<int32_t> cdv((size_t)nc), pdv((size_t)npt);
+    for (int32_t li = 0; li < nc; ++li) cdv[(size_t)li] = li < noc ? 0 : 1;
+    for (int32_t lj = 0; lj < npt; ++lj) pdv[(size_t)lj] = lj < nop ? 0 : 1;
+    // halo exchange plan: per peer [cameras x 15 | points x 3]
+    std::vector<PeerSeg> segs;
+    std::vector<int32_t> sc, sp, rcm, rpt;
+    std::vector<int64_t> sco, spo, rco, rpo;
+    int64_t soff = 0, roff = 0;
+    for (const Peer& pe : S.peers) {
+      PeerSeg g;
+      g.rank = pe.rank;
+      g.send_off = soff;
+      g.recv_off = roff;
+      for (int32_t c : pe.send_cams) { sc.push_back(c); sco.push_back(soff); soff += 15; }
+      for (int32_t q : pe.send_pts) { sp.push_back(q); spo.push_back(soff); soff += 3; }
+      for (int32_t c : pe.recv_cams) { rcm.push_back(c); rco.push_back(roff); roff += 15; }
+      for (int32_t q : pe.recv_pts) { rpt.push_back(q); rpo.push_back(roff); roff += 3; }
+      g.send_cnt = soff - g.send_off;
+      g.recv_cnt = roff - g.recv_off;
+      segs.push_back(g);
+    }
+    double *dc, *dp, *duv, *sendb = nullptr, *recvb = nullptr, *red = nullptr;
+    int32_t *doc, *dop, *dcd, *dpd, *dsc, *dsp, *drc, *drp;
+    int64_t *doff, *dsco, *dspo, *drco, *drpo;
+    if (!up(B, &dc, hc) || !up(B, &dp, hp) || !up(B, &doc, loc) || !up(B, &dop, lop) || !up(B, &duv, luv) ||
+        !up(B, &doff, cnt) || !up(B, &dcd, cdv) || !up(B, &dpd, pdv) || !up(B, &dsc, sc) || !up(B, &dsp, sp) ||
+        !up(B, &drc, rcm) || !up(B, &drp, rpt) || !up(B, &dsco, sco) || !up(B, &dspo, spo) || !up(B, &drco, rco) ||
+        !up(B, &drpo, rpo) || !(sendb = B.get<double>((size_t)soff)) || !(recvb = B.get<double>((size_t)roff)) ||
+        !(red = B.get<double>(8))) {
+      rc = -5;
+    }
+    std::unique_ptr<Comm> comm;
+    if (!rc && nranks > 1) {
+      std::string e;
+      comm.reset(make_comm(comm_kind == 1 ? 1 : 0, comm_id, rank, nranks, &e));
+      if (!comm) rc = -4;
+    }
+    // scratch of the coarse run on the local problem (as coarse_run_impl)
+    Run R{nc, npt, KL, doc, dop, reinterpret_cast<const double2*>(duv), doff, o.loss, o.scale, o.eps * o.eps, o.eps,
+          o.xi, o.mu0, o.mu_up, o.lm_trials, o.pcg_max_iter, o.pcg_tol, Part{dcd, dpd, 2}};
+    R.st = st;
+    R.active = 1u;  // the halo device is fixed: only this rank's acceptance counts
+    R.M_F = noc;    // F counts each pair once, on its camera's owner
+    const size_t ncl = (size_t)nc * 15, nl = (size_t)npt * 3;
+    double* base = nullptr;
+    if (!rc) {
+      const size_t total = 5 * (ncl + nl) + (size_t)nc * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)npt * (9 + 3 + 3) +
+                           (size_t)daba_coarse_solve_workspace(nc, npt) + 8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev;
+      if (!(base = B.get<double>(total))) rc = -5;
+    }
+    if (!rc && KL > 0 && validate(doc, dop, doff, nc, npt, KL, R.part, st)) rc = -3;  // (the plan's own output)
+    if (!rc) {
+      double* op = base;
+      auto take = [&](size_t n) { double* p = op; op += n; return p; };
+      double *cp = take(ncl), *lp = take(nl), *cb = take(ncl), *lb = take(nl), *ca = take(ncl), *la = take(nl),
+             *cm = take(ncl), *lm = take(nl), *ct = take(ncl), *lt = take(nl);
+      R.U = take((size_t)nc * 81);
+      R.gc = take((size_t)nc * 9);
+      R.Fc = take((size_t)nc);
+      R.dcv = take((size_t)nc * 9);
+      R.dEc = take((size_t)nc * kMaxDev);
+      R.V = take((size_t)npt * 9);
+      R.gl = take((size_t)npt * 3);
+      R.dlv = take((size_t)npt * 3);
+      R.W = nullptr;
+      R.work = take((size_t)daba_coarse_solve_workspace(nc, npt));
+      R.scal = take(8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev);
+      // global sums of rank-local scalars (the allreduce of reading D2)
+      auto sum = [&](double* v, int n) -> int {
+        if (!comm) return 0;
+        if (cudaMemcpyAsync(red, v, sizeof(double) * n, cudaMemcpyHostToDevice, st) != cudaSuccess) return -3;
+        if (!comm->allreduce(red, red, n, st).empty()) return -4;
+        if (cudaMemcpyAsync(v, red, sizeof(double) * n, cudaMemcpyDeviceToHost, st) != cudaSuccess) return -3;
+        return cudaStreamSynchronize(st) == cudaSuccess ? 0 : -3;
+      };
+      const unsigned g = (unsigned)((std::max<int64_t>(nc, 3 * (int64_t)npt) + 255) / 256);
+      const int64_t nx = 15 * (int64_t)sc.size() + 3 * (int64_t)sp.size(), nr = 15 * (int64_t)rcm.size() + 3 * (int64_t)rpt.size();
+      if (cudaMemcpyAsync(cp, dc, ncl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+          cudaMemcpyAsync(lp, dp, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        rc = -3;
+      double Fbar = 0.0, s = 1.0;
+      if (!rc && !(rc = run_F(R, dc, dp, &Fbar))) rc = sum(&Fbar, 1);
+      for (int it = 0; it < n_iters && !rc; ++it) {
+        const double s_next = (sqrt(4.0 * s * s + 1.0) + 1.0) / 2.0;  // eq. nesterov_scalar, Alg. 1
+        const double gamma = o.accelerate ? (s - 1.0) / s_next : 0.0;
+        double Fk;
+        if ((rc = run_F(R, dc, dp, &Fk)) || (rc = sum(&Fk, 1))) break;
+        Fbar = (1.0 - o.eta) * Fbar + o.eta * Fk;  // eq. lFak
+        int ta[kMaxDev], tm[kMaxDev];
+        double dEa[kMaxDev], dEm[kMaxDev], Eacc = NAN, Emm = NAN;
+        bool restart = true;
+        if (o.accelerate) {
+          if (g) k_cr_extrapolate<<<g, 256, 0, st>>>(dc, cp, dp, lp, nc, npt, gamma, cb, lb);
+          if ((rc = lm_step(R, cb, lb, ca, la, ct, lt, ta, dEa)) || (rc = run_dE(R, ca, la, dc, dp, dEa))) break;
+          double e = dEa[0];
+          if ((rc = sum(&e, 1))) break;
+          Eacc = Fk + e;  // E(x_acc | x^k), eq. Eak, summed over the devices
+          restart = Eacc > Fbar;  // Alg. 1
+        }
+        if (restart || o.mm_always) {
+          if ((rc = lm_step(R, dc, dp, cm, lm, ct, lt, tm, dEm))) break;
+          double e = dEm[0];
+          if ((rc = sum(&e, 1))) break;
+          Emm = Fk + e;
+        }
+        if (!o.accelerate) Eacc = Emm;
+        if (trace) {
+          double* t = trace + 5 * (size_t)it;
+          t[0] = Fk;
+          t[1] = Fbar;
+          t[2] = Eacc;
+          t[3] = (o.accelerate && restart) ? 1.0 : 0.0;
+          t[4] = Emm;
+        }
+        // x^{k-1} <- x^k; x^k <- x^{k+1} (this rank's variables from its own candidates; the halo from the owners)
+        if (cudaMemcpyAsync(cp, dc, ncl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(lp, dp, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(dc, restart ? cm : ca, ncl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(dp, restart ? lm : la, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+          rc = -3;
+          break;
+        }
+        if (comm && !segs.empty()) {
+          if (nx > 0)
+            k_cd_pack<<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(dc, dp, dsc, dsco, (int32_t)sc.size(), dsp, dspo,
+                                                                    (int32_t)sp.size(), sendb);
+          if (!comm->exchange(sendb, recvb, segs, st).empty()) {
+            rc = -4;
+            break;
+          }
+          if (nr > 0)
+            k_cd_unpack<<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(dc, dp, drc, drco, (int32_t)rcm.size(), drp,
+                                                                      drpo, (int32_t)rpt.size(), recvb);
+        }
+        s = s_next;
+      }
+      if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = -3;
+      // owned states back to the caller's global arrays (native layout)
+      if (!rc && (cams_out || pts_out)) {
+        std::vector<double> oc((size_t)noc * 15), ol((size_t)nop * 3);
+        if ((noc && cudaMemcpy(oc.data(), dc, oc.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) ||
+            (nop && cudaMemcpy(ol.data(), dp, ol.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess))
+          rc = -3;
+        for (int32_t li = 0; !rc && cams_out && li < noc; ++li)
+          std::memcpy(cams_out + 15 * (size_t)S.cam_g[(size_t)li], &oc[(size_t)li * 15], 15 * sizeof(double));
+        for (int32_t lj = 0; !rc && pts_out && lj < nop; ++lj)
+          std::memcpy(pts_out + 3 * (size_t)S.pt_g[(size_t)lj], &ol[(size_t)lj * 3], 3 * sizeof(double));
+      }
+    }
+  }
+  cudaStreamDestroy(st);
+  return rc;
 }

@@ -45,7 +45,7 @@ EXPORTS = ["daba_default_options", "daba_comm_id", "daba_create", "daba_iterate"
            "daba_plan_create", "daba_plan_counts", "daba_plan_array", "daba_plan_peer_list", "daba_plan_destroy",
            "daba_pixel_error", "daba_pixel_residuals", "daba_bal_read", "daba_bal_write", "daba_bal_last_error", "daba_bal_to_paper",
            "daba_paper_to_bal", "daba_coarse_blocks", "daba_coarse_solve_workspace", "daba_coarse_solve", "daba_coarse_run",
-           "daba_coarse_default_options", "daba_coarse_run_part", "daba_bal_to_native"]
+           "daba_coarse_default_options", "daba_coarse_run_part", "daba_bal_to_native", "daba_coarse_run_dist"]
 
 
 class CoarseOptions(ctypes.Structure):
@@ -107,6 +107,8 @@ def lib():
         D = ctypes.c_double
         L.daba_coarse_run.argtypes = [V, I64, V, I64, V, V, V, V, I64, I32, D, D, D, D, D, D, I32, I32, I32, D, I32, V, V]
         L.daba_bal_to_native.argtypes = [V, I64, V]
+        L.daba_coarse_run_dist.argtypes = [V, I64, V, I64, V, V, V, I64, V, V, I32, I32, V, I32, I32,
+                                           ctypes.POINTER(CoarseOptions), I32, V, V, V]
         L.daba_coarse_default_options.argtypes = [ctypes.POINTER(CoarseOptions)]
         L.daba_coarse_default_options.restype = None
         L.daba_coarse_run_part.argtypes = [V, I64, V, I64, V, V, V, V, I64, V, V, I32, ctypes.POINTER(CoarseOptions),
@@ -303,6 +305,29 @@ def bal_to_native(cams):
     if rc:
         raise DabaError(rc, "daba_bal_to_native")
     return out
+
+
+def coarse_run_dist(cams, pts, obs_cam, obs_pt, obs_uv, n_iters, rank=0, nranks=1, comm_key=None, comm=COMM_NCCL,
+                    device=0, cam_owner=None, pt_owner=None, **opts):
+    """daba_coarse_run_dist (include/daba.h; SURVEY NEXT-3 with one device per rank): host arrays in the ABI layout
+    (BAL cameras); returns (trace (n_iters, 5), cams (M, 15) native with this rank's cameras filled (NaN
+    elsewhere), pts (N, 3) likewise)."""
+    c, l = _c(cams, np.float64).reshape(-1, 9), _c(pts, np.float64).reshape(-1, 3)
+    oc, op, uv = _c(obs_cam, np.int32), _c(obs_pt, np.int32), _c(obs_uv, np.float64).reshape(-1, 2)
+    co = _c(cam_owner, np.int32) if cam_owner is not None else None
+    po = _c(pt_owner, np.int32) if pt_owner is not None else None
+    M, N, K = c.shape[0], l.shape[0], oc.shape[0]
+    key = ctypes.create_string_buffer(comm_key, 128) if comm_key is not None else None
+    o = coarse_options(**opts)
+    tr = np.zeros((n_iters, 5))
+    cout, lout = np.full((M, 15), np.nan), np.full((N, 3), np.nan)
+    rc = lib().daba_coarse_run_dist(c.ctypes.data, M, l.ctypes.data, N, oc.ctypes.data, op.ctypes.data, uv.ctypes.data,
+                                    K, co.ctypes.data if co is not None else None,
+                                    po.ctypes.data if po is not None else None, rank, nranks, key, int(comm), device,
+                                    ctypes.byref(o), int(n_iters), tr.ctypes.data, cout.ctypes.data, lout.ctypes.data)
+    if rc != 0:
+        raise DabaError(rc, "daba_coarse_run_dist")
+    return tr, cout, lout
 
 
 def coarse_options(**kw):

@@ -339,3 +339,46 @@ def test_coarse_entries_reject_bad_indices_before_writing():
     with pytest.raises(daba.DabaError):  # BAL-layout (M, 9) cameras: caught by the shape check
         daba.coarse_run_part(t(p.cams, torch.float64), t(cp.pts0, torch.float64), t(cp.oc[order], torch.int32),
                              t(cp.op[order], torch.int32), t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 1)
+
+
+@pytest.mark.parametrize("nranks,loss,eta", [(2, oracle.LOSS_HUBER, 0.1), (3, oracle.LOSS_CAUCHY, 1.0)])
+def test_coarse_run_dist_matches_the_oracle(nranks, loss, eta):
+    """NEXT-3 with one device per rank (daba_coarse_run_dist; ranks = threads through the LOCAL transport, each
+    solving its own device's subproblem, allreducing F / E and exchanging the boundary variables): equal to
+    oracle/coarse.run with the daba_create partition as the device assignment — restart flags identical, traces
+    within 1e-9, every rank's owned states within 1e-7 of their scale after 8 iterations."""
+    import threading
+    import paper_2305_07026_b200 as daba
+    p = gen.generate("tiny_seq", loss=loss, outlier_frac=0.05 if loss else 0.0)
+    plan = daba.Plan(p.M, p.N, p.obs_cam, p.obs_pt, rank=0, nranks=nranks)
+    cam_dev, pt_dev = plan.array(2), plan.array(3)
+    cp = coarse.Problem(p, cam_dev, pt_dev, eta=eta)
+    assert 0 < cp.intra.sum() < cp.K
+    tr_ref, c_ref, l_ref = coarse.run(cp, 8)
+    key = np.random.default_rng(nranks + 10).bytes(128)
+    out, err = [None] * nranks, []
+
+    def work(r):
+        try:
+            out[r] = daba.coarse_run_dist(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, 8, rank=r, nranks=nranks,
+                                          comm_key=key, comm=daba.COMM_LOCAL, loss=loss, scale=p.loss_scale, eta=eta,
+                                          pcg_max_iter=2000, pcg_tol=1e-15, mm_always=1)
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    if err:
+        raise err[0]
+    c, l = np.full_like(c_ref, np.nan), np.full_like(l_ref, np.nan)
+    for tr, cr, lr in out:
+        np.testing.assert_array_equal(tr, out[0][0])  # every rank reports the same global trace
+        c[~np.isnan(cr[:, 0])] = cr[~np.isnan(cr[:, 0])]
+        l[~np.isnan(lr[:, 0])] = lr[~np.isnan(lr[:, 0])]
+    tr = out[0][0]
+    np.testing.assert_array_equal(tr[:, 3], tr_ref[:, 3])
+    for col in (0, 1, 2, 4):
+        np.testing.assert_allclose(tr[:, col], tr_ref[:, col], rtol=1e-9)
+    assert not np.isnan(c).any() and not np.isnan(l).any()
+    assert np.abs(c - c_ref).max() <= 1e-7 * np.abs(c_ref).max()
+    assert np.abs(l - l_ref).max() <= 1e-7 * np.abs(l_ref).max()
