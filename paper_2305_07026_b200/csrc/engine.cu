@@ -160,6 +160,19 @@ int dalloc(daba_ctx* c, T** p, size_t n) {
   return DABA_OK;
 }
 
+// Release one dalloc'd buffer before destroy (create-time buffers whose job is done).
+void dfree(daba_ctx* c, void* p, size_t bytes) {
+  if (!p) return;
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+  if (it == c->allocs.end()) return;
+  c->allocs.erase(it);
+  c->dev_bytes -= bytes;
+  if (c->pooled)
+    cudaFreeAsync(p, c->stream);
+  else
+    cudaFree(p);
+}
+
 // Host -> device copy on the context's stream.  Small or page-locked sources go directly; large pageable ones
 // through a process-wide page-locked staging buffer (two 32 MB halves: the host threads fill one half while
 // the copy engine drains the other).  Returns once the source may be reused.
@@ -564,24 +577,8 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   const int32_t point_far = (int32_t)env_int("DABA_POINT_FAR", 1024);  // "far apart" in camera ids
   // one rank with input sorted by (camera, point): a light host plan, the point side built on the device
   const bool defer = nranks == 1 && point_order != 2 && env_int("DABA_DEVICE_PLAN", 1) != 0;
-  std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, defer);
-  if (!e.empty()) {
-    *out = nullptr;
-    return DABA_E_INVALID_ARG;
-  }
-  timer.mark("plan_shard");
-  if (!C->plan.point_side_deferred && point_order != 0)
-    order_owned_points(&C->plan, obs_cam, point_order == 2, point_far);
-  timer.mark("point order");
-  // native cameras (Assumption 2 at x^0, P:L944, is checked on the device by the first objective evaluation)
-  std::vector<double> nat((size_t)M * 15);
-  for (int64_t i = 0; i < M; ++i) {
-    double tmp[16];
-    bal_to_native(cameras + 9 * i, tmp);
-    std::memcpy(&nat[(size_t)i * 15], tmp, 15 * sizeof(double));
-  }
-  timer.mark("native cameras");
-  // device and stream
+  // device, stream and communicator first: with one rank the observations go to the device anyway, and their
+  // validation (indices in range, sorted by (camera, point), each camera's offset) runs there
   if (cudaSetDevice(cuda_device) != cudaSuccess) return DABA_E_CUDA;
   if (o.stream) {
     C->stream = static_cast<cudaStream_t>(o.stream);
@@ -619,13 +616,10 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     g_create_err = why;
     return code;
   };
-  // light plan: decide on the device whether the input point numbering follows the cameras; if not, fall back
-  // to the full host plan with the locality renumbering.  d_opt (the observations' points on the device)
-  // becomes the camera side's point index.
   int32_t* d_opt = nullptr;
-  if (C->plan.point_side_deferred) {
-    // the record staging buffer (64 B per observation) is allocated now and lends its memory to the setup
-    // temporaries (no allocate / free churn at create)
+  bool pre = false;  // a light plan from the device check; the observations are already on the device
+  if (defer && !cam_owner && !pt_owner && K > 0 && M > 0 && env_int("DABA_DEVICE_VALIDATE", 1) != 0 &&
+      ((4 * (size_t)K + 255) / 256 * 256 + 8 * ((size_t)M + 1) + 1024 <= 64 * (size_t)K)) {
     IterParams& Q = C->P;
     Q.n_records = std::max<int64_t>(K, 1);
     if ((rc = dalloc(C, &Q.staging, 8 * (size_t)Q.n_records)) || (rc = dalloc(C, &d_opt, (size_t)Q.n_records)))
@@ -634,6 +628,63 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
         h2d(C, d_ocam, obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess)
       return g_bail_line = __LINE__, bail(DABA_E_CUDA);
+    std::vector<int64_t> cptr((size_t)M + 1);
+    int64_t bad = K;
+    bool sorted = false;
+    if (validate_sorted_device(d_ocam, d_opt, K, M, N,
+                               reinterpret_cast<char*>(Q.staging) + (4 * (size_t)K + 255) / 256 * 256, &bad, &sorted,
+                               cptr.data(), C->stream) != 0)
+      return g_bail_line = __LINE__, bail(DABA_E_CUDA);
+    if (bad < K) {
+      fail(C, DABA_E_INVALID_ARG, "observation " + std::to_string(bad) + " has an index out of range");
+      return g_bail_line = __LINE__, bail(DABA_E_INVALID_ARG);
+    }
+    if (sorted) {
+      plan_light(M, N, K, std::move(cptr), &C->plan);
+      pre = true;
+    } else {  // the host plan sorts and checks for duplicates
+      dfree(C, Q.staging, 64 * (size_t)Q.n_records);
+      dfree(C, d_opt, 4 * (size_t)Q.n_records);
+      Q.staging = nullptr;
+      d_opt = nullptr;
+    }
+    timer.mark("device validation");
+  }
+  if (!pre) {
+    std::string e = plan_shard(M, N, K, obs_cam, obs_pt, cam_owner, pt_owner, rank, nranks, &C->plan, defer);
+    if (!e.empty()) {
+      fail(C, DABA_E_INVALID_ARG, e);
+      return g_bail_line = __LINE__, bail(DABA_E_INVALID_ARG);
+    }
+    timer.mark("plan_shard");
+    if (!C->plan.point_side_deferred && point_order != 0)
+      order_owned_points(&C->plan, obs_cam, point_order == 2, point_far);
+    timer.mark("point order");
+  }
+  // native cameras (Assumption 2 at x^0, P:L944, is checked on the device by the first objective evaluation)
+  std::vector<double> nat((size_t)M * 15);
+  for (int64_t i = 0; i < M; ++i) {
+    double tmp[16];
+    bal_to_native(cameras + 9 * i, tmp);
+    std::memcpy(&nat[(size_t)i * 15], tmp, 15 * sizeof(double));
+  }
+  timer.mark("native cameras");
+  // light plan: decide on the device whether the input point numbering follows the cameras; if not, fall back
+  // to the full host plan with the locality renumbering.  d_opt (the observations' points on the device)
+  // becomes the camera side's point index.
+  if (C->plan.point_side_deferred) {
+    // the record staging buffer (64 B per observation) is allocated now and lends its memory to the setup
+    // temporaries (no allocate / free churn at create)
+    IterParams& Q = C->P;
+    if (!pre) {
+      Q.n_records = std::max<int64_t>(K, 1);
+      if ((rc = dalloc(C, &Q.staging, 8 * (size_t)Q.n_records)) || (rc = dalloc(C, &d_opt, (size_t)Q.n_records)))
+        return g_bail_line = __LINE__, bail(rc);
+      if (h2d(C, d_opt, obs_pt, sizeof(int32_t) * (size_t)K) != cudaSuccess ||
+          h2d(C, reinterpret_cast<int32_t*>(Q.staging), obs_cam, sizeof(int32_t) * (size_t)K) != cudaSuccess)
+        return g_bail_line = __LINE__, bail(DABA_E_CUDA);
+    }
+    int32_t* d_ocam = reinterpret_cast<int32_t*>(Q.staging);
     // scratch after the K camera ids: N int32 keys + a counter; with more points than the buffer holds (isolated
     // points) or no observations the check is skipped (nothing to gather, the numbering is kept)
     const bool fits = K > 0 && sizeof(int32_t) * ((size_t)K + 8 + (size_t)N) + 64 <= 64 * (size_t)Q.n_records;
@@ -683,6 +734,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
     if ((rc = upload(C, &P.roles, roles))) return g_bail_line = __LINE__, bail(rc);
   }
   timer.mark("device, stream, comm");
+  bool uv_on_side = false;  // the pixels' upload runs on the side stream (joined before the first objective)
   // camera side + chunks
   const int64_t chunk_obs = std::max<int64_t>(64, std::min<int64_t>(kCamChunkObs, env_int("DABA_CHUNK_OBS", kCamChunkObs)));
   {
@@ -696,8 +748,19 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       CUDA_OR(C, h2d(C, dpt, S.c_pt.data(), kc * sizeof(int32_t)));
     }
     if (S.cam_side_identity) {
-      // one rank, input sorted by (camera, point): the camera-side pixels are the input itself (no host copy)
-      CUDA_OR(C, h2d(C, duv, obs_uv, kc * sizeof(double2)));
+      // one rank, input sorted by (camera, point): the camera-side pixels are the input itself (no host copy).
+      // From page-locked memory the copy runs on the side stream, beside the device sort of the point side; the
+      // main stream waits for it before the first objective evaluation.
+      if (kc * sizeof(double2) >= (8u << 20) && is_pinned(obs_uv)) {
+        CUDA_OR(C, cudaEventRecord(C->ev_fork0, C->stream));  // (after duv's stream-ordered allocation)
+        CUDA_OR(C, cudaStreamWaitEvent(C->side, C->ev_fork0, 0) == cudaSuccess
+                       ? cudaMemcpyAsync(duv, obs_uv, kc * sizeof(double2), cudaMemcpyHostToDevice, C->side)
+                       : cudaErrorUnknown);
+        CUDA_OR(C, cudaEventRecord(C->ev_join0, C->side));
+        uv_on_side = true;
+      } else {
+        CUDA_OR(C, h2d(C, duv, obs_uv, kc * sizeof(double2)));
+      }
     } else {
       hvec<double2> uv(kc);
       parallel_for((int64_t)kc, [&](int64_t a, int64_t b) {
@@ -939,6 +1002,7 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
   timer.mark("states");
   // s^{(0)} = 1, F-bar^{(-1)} = F(x^0) (eq. Fainit, global form), k = 0
   double F0 = 0, nd = 0;
+  if (uv_on_side) CUDA_OR(C, cudaStreamWaitEvent(C->stream, C->ev_join0, 0));
   if ((rc = compute_objective(C, &F0, &nd))) return g_bail_line = __LINE__, bail(rc);
   if (nd > 0) return g_bail_line = __LINE__, bail(DABA_E_DEGENERATE);  // Assumption 2: ||l_j - t_i|| <= eps for some pair
   if (P.restart_scope == 1) {

@@ -1513,4 +1513,49 @@ int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d
   return cudaStreamSynchronize(st) == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+
+// Create time, one rank: the observations' indices checked on the device (the arrays go there anyway), whether
+// they are sorted by (camera, point) strictly (so also free of duplicate pairs), and — when they are — each
+// camera's first observation.  bad_min: smallest k with an index out of range (K if none).
+__global__ void k_validate_sorted(const int32_t* cam, const int32_t* pt, int64_t K, int64_t M, int64_t N,
+                                  unsigned long long* bad_min, int* unsorted, int64_t* cptr) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int32_t c = cam[k], j = pt[k];
+  if (c < 0 || c >= M || j < 0 || j >= N) {
+    atomicMin(bad_min, (unsigned long long)k);
+    return;
+  }
+  int32_t prev = -1;
+  if (k > 0) {
+    prev = cam[k - 1];
+    const int32_t jp = pt[k - 1];
+    if (!(prev < c || (prev == c && jp < j))) atomicOr(unsorted, 1);
+  }
+  for (int64_t i = prev + 1 > 0 ? prev + 1 : 0; i <= c; ++i) cptr[i] = k;  // cameras starting at k
+  if (k == K - 1)
+    for (int64_t i = (int64_t)c + 1; i <= M; ++i) cptr[i] = K;
+}
+
+int validate_sorted_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int64_t M, int64_t N, void* scratch,
+                           int64_t* bad_k, bool* sorted, int64_t* cam_ptr_host, cudaStream_t st) {
+  char* sp = static_cast<char*>(scratch);
+  unsigned long long* bad = static_cast<unsigned long long*>(carve(sp, sizeof(unsigned long long)));
+  int* uns = static_cast<int*>(carve(sp, sizeof(int)));
+  int64_t* cptr = static_cast<int64_t*>(carve(sp, sizeof(int64_t) * (size_t)(M + 1)));
+  const unsigned long long kk = (unsigned long long)K;
+  cudaMemcpyAsync(bad, &kk, sizeof kk, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(uns, 0, sizeof(int), st);
+  if (K > 0) k_validate_sorted<<<grid(K), 256, 0, st>>>(d_cam, d_pt, K, M, N, bad, uns, cptr);
+  unsigned long long hb = 0;
+  int hu = 0;
+  cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hu, uns, sizeof hu, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(cam_ptr_host, cptr, sizeof(int64_t) * (size_t)(M + 1), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) return -1;
+  *bad_k = (int64_t)hb;
+  *sorted = hu == 0;
+  return 0;
+}
+
 }  // namespace daba

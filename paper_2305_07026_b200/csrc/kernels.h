@@ -152,6 +152,12 @@ int launch_xyz_pts(const double* src, double4* dst, int32_t n, cudaStream_t st);
 // first use)
 int64_t count_point_jumps_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int32_t N, int32_t far,
                                  void* scratch, cudaStream_t st);
+// Create time, one rank (device copies of the observations' cameras and points, K > 0): *bad_k = the first
+// observation with an index out of range (K if none); *sorted = strictly sorted by (camera, point); when sorted and
+// valid, cam_ptr_host (HOST, M + 1) = each camera's first observation.  scratch: 16 + 8 (M + 1) bytes + 512.
+// 0 or -1 on a CUDA error.
+int validate_sorted_device(const int32_t* d_cam, const int32_t* d_pt, int64_t K, int64_t M, int64_t N, void* scratch,
+                           int64_t* bad_k, bool* sorted, int64_t* cam_ptr_host, cudaStream_t st);
 int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, void* scratch,
                            size_t scratch_bytes, cudaStream_t st);
 

@@ -110,6 +110,29 @@ struct Tm {
 
 }  // namespace
 
+void plan_light(int64_t M, int64_t N, int64_t K, std::vector<int64_t> cam_ptr, ShardPlan* out) {
+  ShardPlan& P = *out;
+  P = ShardPlan();
+  P.M = M;
+  P.N = N;
+  P.K = K;
+  P.cam_owner.assign((size_t)M, 0);
+  P.pt_owner.assign((size_t)N, 0);
+  P.cam_g.resize((size_t)M);
+  P.pt_g.resize((size_t)N);
+  pfor(M, [&](int64_t a, int64_t b, int) {
+    for (int64_t i = a; i < b; ++i) P.cam_g[(size_t)i] = (int32_t)i;
+  });
+  pfor(N, [&](int64_t a, int64_t b, int) {
+    for (int64_t j = a; j < b; ++j) P.pt_g[(size_t)j] = (int32_t)j;
+  });
+  P.n_own_cams = (int32_t)M;
+  P.n_own_pts = (int32_t)N;
+  P.cam_ptr = std::move(cam_ptr);
+  P.cam_side_identity = true;
+  P.point_side_deferred = true;
+}
+
 std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, const int32_t* obs_pt,
                        const int32_t* cam_owner_in, const int32_t* pt_owner_in, int rank, int nranks,
                        ShardPlan* out, bool defer_point_side) {

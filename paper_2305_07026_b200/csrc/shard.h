@@ -85,4 +85,8 @@ std::string plan_shard(int64_t M, int64_t N, int64_t K, const int32_t* obs_cam, 
                        const int32_t* cam_owner, const int32_t* pt_owner, int rank, int nranks, ShardPlan* out,
                        bool defer_point_side = false);
 
+// The light plan of one rank whose observations are sorted by (camera, point) (checked by the caller): identity
+// numbering, every camera and point owned, camera offsets cam_ptr (M + 1); the point side is left to the engine.
+void plan_light(int64_t M, int64_t N, int64_t K, std::vector<int64_t> cam_ptr, ShardPlan* out);
+
 }  // namespace daba
