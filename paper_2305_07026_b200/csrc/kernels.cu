@@ -1222,7 +1222,7 @@ __global__ void k_pack(IterParams p, const int32_t* cam_idx, const int64_t* cam_
 __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* cam_off, int32_t n_cam,
                          const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf,
                          int select_inside) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // after the decision: x^{k+1} = roles[1], x^k = roles[0], x-bar buffer roles[4], gamma^{(k+1)} from s^{(k+1)};
   // with select_inside the decision is still to be committed: every thread derives the same outcome
   // (sel: which half of the received record; without select_inside both halves carry x^{k+1})
@@ -1242,24 +1242,16 @@ __global__ void k_unpack(IterParams p, const int32_t* cam_idx, const int64_t* ca
     xbuf = p.roles[4];
     gamma = sched_gamma(p.sched[0], p.accelerate, nullptr);
   }
-  if (t < n_cam) {  // x^{k+1} and its x-bar^{k+1} as the owner computed them
-    DCHECK(cam_idx[t] >= p.n_own_cams && cam_idx[t] < p.n_cams, "halo camera", cam_idx[t], p.n_cams);
-    const size_t i = (size_t)cam_idx[t] * kCamStride;
-    const double* src = buf + cam_off[t];
-    double v[15], xb[16];
-#pragma unroll
-    for (int k = 0; k < 15; ++k) v[k] = src[15 * sel + k];  // all loads in flight before any store
-#pragma unroll
-    for (int k = 0; k < 16; ++k) xb[k] = src[30 + 16 * sel + k];
-    double* c = p.cams[r_new] + i;
-    double* cb = p.cbarb[xbuf] + i;
-#pragma unroll
-    for (int k = 0; k < 15; ++k) c[k] = v[k];
-    c[15] = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) cb[k] = xb[k];
-  } else if (t < n_cam + n_pt) {
-    const int q = t - n_cam;
+  const int64_t n_cam_thr = (int64_t)n_cam * 32;  // one warp per halo camera: lane k < 15 copies x_k, 16 + k x-bar_k
+  if (t < n_cam_thr) {  // x^{k+1} and its x-bar^{k+1} as the owner computed them (coalesced 31-double records)
+    const int e = t >> 5, lane = t & 31;
+    DCHECK(cam_idx[e] >= p.n_own_cams && cam_idx[e] < p.n_cams, "halo camera", cam_idx[e], p.n_cams);
+    const size_t i = (size_t)cam_idx[e] * kCamStride;
+    const double* src = buf + cam_off[e];
+    if (lane < 16) p.cams[r_new][i + lane] = lane < 15 ? src[15 * sel + lane] : 0.0;
+    else p.cbarb[xbuf][i + lane - 16] = src[30 + 16 * sel + lane - 16];
+  } else if (t < n_cam_thr + n_pt) {
+    const int q = (int)(t - n_cam_thr);
     DCHECK(pt_idx[q] >= p.n_own_pts && pt_idx[q] < p.n_pts, "halo point", pt_idx[q], p.n_pts);
     const double* b = buf + pt_off[q] + 3 * sel;
     const double4 lp = p.pts[r_old][pt_idx[q]];
@@ -1406,7 +1398,7 @@ int launch_unpack(const IterParams& p, const int32_t* cam_idx, const int64_t* ca
                   const int32_t* pt_idx, const int64_t* pt_off, int32_t n_pt, const double* buf, int select_inside,
                   cudaStream_t st) {
   if (n_cam + n_pt == 0) return 0;
-  k_unpack<<<blocks(n_cam + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
+  k_unpack<<<blocks((int64_t)n_cam * 32 + n_pt, 256), 256, 0, st>>>(p, cam_idx, cam_off, n_cam, pt_idx, pt_off, n_pt, buf,
                                                       select_inside);
   return 1;
 }
