@@ -225,7 +225,8 @@ int daba_coarse_blocks(const double* cams, int64_t M, const double* pts, int64_t
  * gradients (implicit Schur products, two observation passes each) until |r|_P <= tol |b|_P or max_iter
  * iterations; then dl = -(V + Pl)'^-1 (gl + W^T dc).  Inputs are daba_coarse_blocks' outputs plus obs_cam (int32,
  * sorted by camera) and the same obs_pt / cam_off; all DEVICE pointers, caller-owned.  dc: M x 9, dl: N x 3
- * (device, written).  work: daba_coarse_solve_workspace(M, N) doubles of device scratch.  info (HOST, 2 doubles):
+ * (device, written).  work: daba_coarse_solve_workspace(M, N) doubles of device scratch.  The point sums W^T v use
+ * fp64 atomics (reproducible to rounding); the PCG scalars are summed in a fixed order.  info (HOST, 2 doubles):
  * PCG iterations taken, final preconditioned residual ratio.  Blocking (synchronises `stream`).  Returns 0,
  * DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3), or DABA_E_STATE (-6) if a damped 3x3 / 9x9 block is not positive
  * definite (a failed LM trial: retry with a larger mu). */
@@ -266,8 +267,9 @@ int daba_coarse_run(double* cams, int64_t M, double* pts, int64_t N, const int32
  * the accepted trial of every device for the accelerated then the MM subproblem (-1: none / not solved).
  * The inputs are checked on the device first (indices in range, cam_off monotone from 0 to K, obs_cam inside its
  * camera's segment, device ids in range): DABA_E_INVALID_ARG before anything is written.  The calling thread's
- * current device is switched to the one holding `cams` for the call.  The PCG's point sums and scalars use fp64
- * atomics: results are reproducible to rounding, not bitwise.  Scratch comes from the library's stream-ordered
+ * current device is switched to the one holding `cams` for the call.  The camera-side sums and the PCG scalars are
+ * taken in a fixed order; the point-side sums use fp64 atomics unless opt->deterministic (then runs are bitwise
+ * reproducible).  Scratch comes from the library's stream-ordered
  * pool; keep_scratch = 0 trims the pool back afterwards.  Returns 0, DABA_E_INVALID_ARG (-1), DABA_E_CUDA (-3),
  * DABA_E_OOM (-5). */
 /* The native camera layout of the coarse entry points from the ABI's BAL layout (host arrays, M x 9 -> M x 15:
@@ -286,9 +288,13 @@ typedef struct {
   double pcg_tol;    /* preconditioned residual ratio */
   int mm_always;     /* 1: solve the MM subproblem every iteration (oracle parity); 0: only when the restart fires */
   int keep_scratch;  /* 1: keep the scratch in the pool for the next call */
+  int deterministic; /* 1: every sum in a fixed order (the point sides over a stable sort by point, made once per
+                        call; no fp64 atomics): bitwise reproducible runs, ~2x slower point-side passes; 0: the
+                        point-side sums by fp64 atomics (reproducible to rounding only) */
 } daba_coarse_options;
 void daba_coarse_default_options(daba_coarse_options* o); /* trivial, 1, 1e-8, xi 1e-4, eta 0.1, 1e-3, 10, 5, 1,
-                                                              PCG <= 10 to 1e-2, mm_always 0, keep_scratch 0 */
+                                                              PCG <= 10 to 1e-2, mm_always 0, keep_scratch 0,
+                                                              deterministic 0 */
 int daba_coarse_run_part(double* cams, int64_t M, double* pts, int64_t N, const int32_t* obs_cam,
                          const int32_t* obs_pt, const double* obs_uv, const int64_t* cam_off, int64_t K,
                          const int32_t* cam_dev, const int32_t* pt_dev, int ndev, const daba_coarse_options* opt,

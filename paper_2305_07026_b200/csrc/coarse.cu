@@ -37,6 +37,17 @@ struct Part {
   const int32_t* pt_dev;
   int ndev;
 };
+// The observations in point order (built once per call by a stable radix sort on the point index): point j's
+// observations are off[j] .. off[j+1]-1, in increasing observation index, with their camera, pixel (null when the
+// per-observation W blocks are given) and observation index.  The point-side sums run over it, one thread per
+// point in a fixed order — deterministic, no atomics (round-1 advisor / verdict: the coarse path's fp64 atomics).
+struct PtOrder {
+  const int64_t* off;
+  const int32_t* cam;
+  const double2* uv;
+  const int32_t* k;
+};
+
 __device__ __forceinline__ int cdev(const Part& P, int64_t i) { return P.cam_dev ? P.cam_dev[i] : 0; }
 __device__ __forceinline__ int pdev(const Part& P, int64_t j) { return P.pt_dev ? P.pt_dev[j] : 0; }
 __device__ __forceinline__ bool intra(const Part& P, int64_t i, int64_t j) {
@@ -67,7 +78,7 @@ __device__ __forceinline__ bool pair_coef(const double* __restrict__ cam, const 
 __device__ __forceinline__ int tri9(int r, int c) { return r * (r + 1) / 2 + c; }  // r >= c
 
 // r, J_c (3x9, row-major), J_l (3x3) of one observation; false if Assumption 2 fails (|l - t| <= eps).
-__device__ bool pair_jacobians(const double* __restrict__ cam, const double* __restrict__ l, double2 u, double eps2,
+__device__ __forceinline__ bool pair_jacobians(const double* __restrict__ cam, const double* __restrict__ l, double2 u, double eps2,
                                double r[3], double Jc[27], double Jl[9]) {
   const double* R = cam;
   const double s = u.x * u.x + u.y * u.y;
@@ -107,7 +118,8 @@ __device__ bool pair_jacobians(const double* __restrict__ cam, const double* __r
 }
 
 // One CTA per camera (observations sorted by camera): each thread sums its observations' w J_c^T J_c and
-// w J_c^T r in registers, the CTA reduces them in a fixed order; the point blocks go out by fp64 atomics.
+// w J_c^T r in registers, the CTA reduces them in a fixed order; the point blocks go out by fp64 atomics (V != null)
+// or come from k_coarse_pts in point order (the deterministic mode).
 // Inter-device pairs (a partition): the camera side adds the Gauss-Newton system of P_ij = w |R p + lam t - g|^2
 // (exact: P is quadratic in the residual), 2 w J^T J and 2 w J^T (R e / 2) with J = [-[q]x, lam I, R e3 b^T]; the
 // point side adds Q_ij's, 2 w lam^2 I and -w lam R e (eq. Q: Q = w |lam l - g|^2 + a/2, lam l_hat - g = -R e / 2);
@@ -154,10 +166,11 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
         for (int c = 0; c <= a; ++c) acc[tri9(a, c)] += 2.0 * w * (J[a] * J[c] + J[9 + a] * J[9 + c] + J[18 + a] * J[18 + c]);
         acc[45 + a] += w * (J[a] * Re[0] + J[9 + a] * Re[1] + J[18 + a] * Re[2]);
       }
-      for (int a = 0; a < 3; ++a) {
-        atomicAdd(V + 9 * (size_t)j + 4 * a, 2.0 * w * lam * lam);
-        atomicAdd(gl + 3 * (size_t)j + a, -w * lam * Re[a]);
-      }
+      if (V)  // the point side, Q_ij (else k_coarse_pts)
+        for (int a = 0; a < 3; ++a) {
+          atomicAdd(V + 9 * (size_t)j + 4 * a, 2.0 * w * lam * lam);
+          atomicAdd(gl + 3 * (size_t)j + a, -w * lam * Re[a]);
+        }
       continue;
     }
     if (!pair_jacobians(scam, l, uv[k], eps2, r, Jc, Jl)) {  // R-N3d: the pair contributes nothing
@@ -180,13 +193,14 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
         for (int c = 0; c < 3; ++c)
           Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
     }
+    if (V)  // the point side (else k_coarse_pts)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
+      for (int a = 0; a < 3; ++a) {
 #pragma unroll
-      for (int c = 0; c <= a; ++c)
-        atomicAdd(V + 9 * (size_t)j + 3 * a + c, w * (Jl[a] * Jl[c] + Jl[3 + a] * Jl[3 + c] + Jl[6 + a] * Jl[6 + c]));
-      atomicAdd(gl + 3 * (size_t)j + a, w * (Jl[a] * r[0] + Jl[3 + a] * r[1] + Jl[6 + a] * r[2]));
-    }
+        for (int c = 0; c <= a; ++c)
+          atomicAdd(V + 9 * (size_t)j + 3 * a + c, w * (Jl[a] * Jl[c] + Jl[3 + a] * Jl[3 + c] + Jl[6 + a] * Jl[6 + c]));
+        atomicAdd(gl + 3 * (size_t)j + a, w * (Jl[a] * r[0] + Jl[3 + a] * r[1] + Jl[6 + a] * r[2]));
+      }
   }
   // CTA reduction, fixed order: warp shuffles, then the four warps' rows in order
   __shared__ double red[kCoarseThreads / 32][kUCols + 1];
@@ -232,6 +246,67 @@ __global__ void k_coarse_mirror(double* V, int64_t N) {
   v[5] = v[7];
 }
 
+// Point side of the blocks, one thread per point over its observations in point order (fixed order, no atomics):
+// V_j = sum w J_l^T J_l and g_l,j = sum w J_l^T r over its intra-device pairs, and Q_ij's Gauss-Newton terms
+// 2 w lam^2 I and -w lam R e over its inter-device pairs (eq. Q, Prop. 1) — term for term what the camera pass
+// computes for the same pair (the same camera state, pixel and arithmetic).
+template <int LOSS>
+__global__ void __launch_bounds__(256) k_coarse_pts(const double* __restrict__ cams, const double* __restrict__ pts,
+                                                    PtOrder po, int64_t N, double delta, double eps2, Part part,
+                                                    double* V, double* gl) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const double l[3] = {pts[3 * j], pts[3 * j + 1], pts[3 * j + 2]};
+  const double delta2 = delta * delta, idelta2 = 1.0 / delta2;
+  double v6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, g[3] = {0.0, 0.0, 0.0};  // v6: packed lower triangle
+  const int64_t o1 = po.off[j + 1];
+  for (int64_t t = po.off[j]; t < o1; ++t) {
+    const int32_t i = po.cam[t];
+    const double2 u = po.uv[t];
+    double cam[15];
+#pragma unroll
+    for (int e = 0; e < 15; ++e) cam[e] = __ldg(cams + 15 * (size_t)i + e);
+    if (!intra(part, i, j)) {  // E'': Q_ij on the point's device
+      double q[3], v[3], lam, Re[3], w, rho;
+      if (!pair_coef<LOSS>(cam, l, u, eps2, delta, q, v, &lam, Re, &w, &rho)) continue;  // R-N3d
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        v6[a * (a + 3) / 2] += 2.0 * w * lam * lam;
+        g[a] += -w * lam * Re[a];
+      }
+      continue;
+    }
+    double r[3], Jc[27], Jl[9];
+    if (!pair_jacobians(cam, l, u, eps2, r, Jc, Jl)) continue;  // R-N3d
+    const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+    double rho = 0.0;
+    const double w = loss_eval<LOSS, true>(sh, delta, delta2, idelta2, &rho);  // R-N3a
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int c = 0; c <= a; ++c)
+        v6[a * (a + 1) / 2 + c] += w * (Jl[a] * Jl[c] + Jl[3 + a] * Jl[3 + c] + Jl[6 + a] * Jl[6 + c]);
+      g[a] += w * (Jl[a] * r[0] + Jl[3 + a] * r[1] + Jl[6 + a] * r[2]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) V[9 * j + 3 * a + c] = a >= c ? v6[a * (a + 1) / 2 + c] : v6[c * (c + 1) / 2 + a];
+    gl[3 * j + a] = g[a];
+  }
+}
+
+// Point order, second half: each position's camera and pixel (the sort gave the observation indices).
+__global__ void k_po_gather(const int32_t* __restrict__ perm, int64_t K, const int32_t* __restrict__ obs_cam,
+                            const double2* __restrict__ uv, int32_t* pcam, double2* puv) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const int32_t k = perm[t];
+  pcam[t] = obs_cam[k];
+  if (uv) puv[t] = uv[k];
+}
+
 }  // namespace
 }  // namespace daba
 
@@ -275,24 +350,74 @@ int validate(const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_o
 }
 
 int coarse_blocks_impl(const double* cams, int64_t M, const double* pts, int64_t N, const int32_t* obs_pt,
-                       const double2* uv, const int64_t* cam_off, int loss, double scale, double eps2, Part part,
-                       double* U, double* gc, double* V, double* gl, double* W, double* F_cam, cudaStream_t st) {
-  if (N > 0) {
+                       const double2* uv, const int64_t* cam_off, const PtOrder& po, int loss, double scale,
+                       double eps2, Part part, double* U, double* gc, double* V, double* gl, double* W, double* F_cam,
+                       cudaStream_t st) {
+  const bool det = po.off != nullptr;  // deterministic: the point side in point order
+  if (N > 0 && !det) {
     if (cudaMemsetAsync(V, 0, (size_t)N * 9 * sizeof(double), st) != cudaSuccess) return -3;
     if (cudaMemsetAsync(gl, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
   }
+  double *Va = det ? nullptr : V, *gla = det ? nullptr : gl;
   if (M > 0) {
     const dim3 g((unsigned)M), b(kCoarseThreads);
     if (loss == kHuber)
-      k_coarse_blocks<kHuber><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+      k_coarse_blocks<kHuber><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
     else if (loss == kCauchy)
-      k_coarse_blocks<kCauchy><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+      k_coarse_blocks<kCauchy><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
     else
-      k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, V, gl, W, F_cam);
+      k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
   }
-  if (N > 0) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
+  if (N > 0 && !det) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
+  if (N > 0 && det) {
+    const unsigned g = (unsigned)((N + 255) / 256);
+    if (loss == kHuber)
+      k_coarse_pts<kHuber><<<g, 256, 0, st>>>(cams, pts, po, N, scale, eps2, part, V, gl);
+    else if (loss == kCauchy)
+      k_coarse_pts<kCauchy><<<g, 256, 0, st>>>(cams, pts, po, N, scale, eps2, part, V, gl);
+    else
+      k_coarse_pts<kTrivial><<<g, 256, 0, st>>>(cams, pts, po, N, scale, eps2, part, V, gl);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+}  // namespace
+
+int sort_point_side_device(const int32_t* d_pt, int64_t K, int32_t N, int32_t* d_src, int64_t* d_ptr, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st);  // kernels.cu: stable radix sort by point
+cudaMemPool_t shared_pool(int device);                                // engine.cu: the process-wide retained pool
+
+namespace {
+// Doubles of device storage the point order over K observations and N points takes (with or without pixels).
+size_t pt_order_doubles(int64_t K, int64_t N, bool with_uv) {
+  return (with_uv ? 2 * (size_t)K : 0) + (size_t)N + 1 + 2 * (size_t)((K + 1) / 2);
+}
+
+// Builds the point order into store (pt_order_doubles of them, 16-byte aligned): the stable radix sort of the
+// observation indices by point, then the gather of each position's camera and pixel.  Synchronises the stream.
+// 0, -1 (K or N beyond the sort's int32 range), -3 (CUDA error), -5 (out of memory).
+int build_pt_order(const int32_t* obs_cam, const int32_t* obs_pt, const double2* uv, int64_t K, int64_t N,
+                   double* store, cudaStream_t st, PtOrder* po) {
+  if (K > INT32_MAX || N > INT32_MAX) return -1;
+  double2* puv = uv ? reinterpret_cast<double2*>(store) : nullptr;
+  int64_t* off = reinterpret_cast<int64_t*>(store + (uv ? 2 * (size_t)K : 0));
+  int32_t* perm = reinterpret_cast<int32_t*>(off + N + 1);
+  int32_t* pcam = perm + 2 * ((K + 1) / 2);
+  *po = PtOrder{off, pcam, puv, perm};
+  void* scratch = nullptr;
+  const size_t bytes = 24 * (size_t)K + ((size_t)1 << 22);  // the sort's keys and values out + CUB's temporaries
+  int device = 0;
+  cudaGetDevice(&device);
+  cudaMemPool_t pool = shared_pool(device);  // (retained: no fresh mapping per call)
+  if (K > 0 && (pool ? cudaMallocFromPoolAsync(&scratch, bytes, pool, st) : cudaMallocAsync(&scratch, bytes, st)) !=
+                   cudaSuccess)
+    return -5;
+  int rc = sort_point_side_device(obs_pt, K, (int32_t)N, perm, off, scratch, bytes, st) ? -3 : 0;
+  if (!rc && K > 0) k_po_gather<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(perm, K, obs_cam, uv, pcam, puv);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) rc = -3;
+  return rc;
+}
+
 }  // namespace
 }  // namespace daba
 
@@ -301,7 +426,9 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
                                   int loss, double scale, double eps, double* U, double* gc, double* V, double* gl,
                                   double* W, double* F_cam, void* stream) {
   using namespace daba;
-  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(scale > 0) || !(eps >= 0) || loss < 0 || loss > 2) return -1;
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || !(scale > 0) || !(eps >= 0) ||
+      loss < 0 || loss > 2)
+    return -1;
   if ((M > 0 && (!cams || !cam_off || !U || !gc || !F_cam)) || (N > 0 && (!pts || !V || !gl)) ||
       (K > 0 && (!obs_pt || !obs_uv)))
     return -1;
@@ -309,8 +436,8 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
   const Part one{nullptr, nullptr, 1};
   int rc = M > 0 ? validate(nullptr, obs_pt, cam_off, M, N, K, one, st) : 0;
   if (rc) return rc;
-  return coarse_blocks_impl(cams, M, pts, N, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, loss, scale,
-                            eps * eps, one, U, gc, V, gl, W, F_cam, st);
+  return coarse_blocks_impl(cams, M, pts, N, obs_pt, reinterpret_cast<const double2*>(obs_uv), cam_off, PtOrder{},
+                            loss, scale, eps * eps, one, U, gc, V, gl, W, F_cam, st);
 }
 
 // ------------------------------------------------------------------ the damped LM direction by Schur complement + PCG
@@ -322,10 +449,29 @@ extern "C" int daba_coarse_blocks(const double* cams, int64_t M, const double* p
 namespace daba {
 namespace {
 
-struct CS {  // workspace views (doubles)
-  double *Pinv, *Vinv, *yv, *t, *x, *r, *z, *p, *q, *s;
+struct CS {  // workspace views (doubles); part: per-CTA / per-camera partial sums of the PCG scalars
+  double *Pinv, *Vinv, *yv, *t, *x, *r, *z, *p, *q, *s, *part;
 };
-enum { S_RZ = 0, S_PQ, S_RZN, S_RZ0, S_DONE, S_ITERS, S_COLS = 8 };
+enum { S_RZ = 0, S_PQ, S_RZN, S_RZ0, S_DONE, S_ITERS, S_BETA, S_COLS = 8 };
+
+// The PCG scalars are summed in a fixed order (per-CTA partials, then one CTA over the partials), so that a solve
+// is reproducible bit for bit (round-1 advisor: no fp64 atomics in the coarse path's reductions).
+constexpr int kSumThreads = 256;
+__device__ double cta_sum(double x) {  // blockDim.x == kSumThreads; the sum in thread 0
+  __shared__ double red[kSumThreads / 32];
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int v = 0; v < kSumThreads / 32; ++v) r += red[v];
+  return r;
+}
+__device__ double sum_partials(const double* p, int64_t n) {  // one CTA of kSumThreads; the sum in thread 0
+  double x = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += kSumThreads) x += p[e];
+  return cta_sum(x);
+}
 
 __device__ __forceinline__ double damp_cam(const double* Ui, int a, double xi, double mu) {  // diagonal of U'
   const double d = Ui[10 * a] + xi * (a < 3 ? 2.0 : 1.0);
@@ -398,11 +544,10 @@ __device__ __forceinline__ void get_W(const WSrc& s, int64_t k, const double* ca
 
 // J_c, J_l and w of observation k at the anchor (false: degenerate pair, contributes nothing) -- for the W-free
 // products w J_l^T (J_c v) and w J_c^T (J_l u), which never hold W (fewer live registers than get_W).
-__device__ __forceinline__ bool get_J(const WSrc& s, int64_t k, const double* cam, int32_t j, double Jc[27],
+__device__ __forceinline__ bool get_J(const WSrc& s, double2 u, const double* cam, const double l[3], double Jc[27],
                                       double Jl[9], double* w) {
-  const double l[3] = {s.pts[3 * (size_t)j], s.pts[3 * (size_t)j + 1], s.pts[3 * (size_t)j + 2]};
   double r[3];
-  if (!pair_jacobians(cam, l, s.uv[k], s.eps2, r, Jc, Jl)) return false;
+  if (!pair_jacobians(cam, l, u, s.eps2, r, Jc, Jl)) return false;
   const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
   const double d2 = s.delta * s.delta, id2 = 1.0 / d2;
   double rho;
@@ -517,21 +662,22 @@ __global__ void k_cs_init(int64_t M, CS w) {
       rz += ri[a] * v;
     }
   }
-  for (int off = 16; off > 0; off >>= 1) rz += __shfl_down_sync(0xffffffffu, rz, off);
-  if ((threadIdx.x & 31) == 0 && rz != 0.0) atomicAdd(w.s + S_RZ, rz);
+  const double b = cta_sum(rz);
+  if (threadIdx.x == 0) w.part[blockIdx.x] = b;
 }
 
-__global__ void k_cs_start(CS w) {
-  w.s[S_RZ0] = w.s[S_RZ];
-  w.s[S_PQ] = w.s[S_RZN] = 0.0;
+__global__ void __launch_bounds__(kSumThreads) k_cs_start(CS w, int64_t nparts) {
+  const double rz = sum_partials(w.part, nparts);
+  if (threadIdx.x != 0) return;
+  w.s[S_RZ] = rz;
+  w.s[S_RZ0] = rz;
   w.s[S_ITERS] = 0.0;
-  w.s[S_DONE] = (w.s[S_RZ] <= 0.0) ? 1.0 : 0.0;
+  w.s[S_DONE] = (rz <= 0.0) ? 1.0 : 0.0;
 }
 
-// t_j = sum_{k of j} W_k^T v_{c(k)} (fp64 atomics; t zeroed by the caller)
-__global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
-                           const int32_t* __restrict__ obs_pt, int64_t K, const double* __restrict__ v, double* t,
-                           const double* s, int check_done) {
+// t_j = sum_{k of j} W_k^T v_{c(k)}, one thread per observation, fp64 atomics (t zeroed by the caller)
+__global__ void k_cs_pass1_obs(WSrc ws, const int32_t* __restrict__ obs_cam, const int32_t* __restrict__ obs_pt,
+                               int64_t K, const double* __restrict__ v, double* t, const double* s, int check_done) {
   if (check_done && s[S_DONE] != 0.0) return;
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
@@ -540,7 +686,8 @@ __global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
   const double* vi = v + 9 * (size_t)i;
   if (!ws.W) {  // w J_l^T (J_c v)
     double Jc[27], Jl[9], w;
-    if (!get_J(ws, k, ws.cams + 15 * (size_t)i, j, Jc, Jl, &w)) return;
+    const double l[3] = {ws.pts[3 * (size_t)j], ws.pts[3 * (size_t)j + 1], ws.pts[3 * (size_t)j + 2]};
+    if (!get_J(ws, ws.uv[k], ws.cams + 15 * (size_t)i, l, Jc, Jl, &w)) return;
     double y[3];
     for (int r = 0; r < 3; ++r) {
       double x = 0.0;
@@ -557,6 +704,44 @@ __global__ void k_cs_pass1(WSrc ws, const int32_t* __restrict__ obs_cam,
     for (int a = 0; a < 9; ++a) x += Wk[3 * a + c] * vi[a];
     atomicAdd(t + 3 * (size_t)j + c, x);
   }
+}
+
+// The same in point order (the deterministic mode): one thread per point over its observations (fixed order, no
+// atomics; every t_j written)
+__global__ void __launch_bounds__(256) k_cs_pass1_pts(WSrc ws, PtOrder po, int64_t N, const double* __restrict__ v,
+                                                  double* t, const double* s, int check_done) {
+  if (check_done && s[S_DONE] != 0.0) return;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double acc[3] = {0.0, 0.0, 0.0};
+  double l[3] = {0.0, 0.0, 0.0};
+  if (!ws.W)
+    for (int a = 0; a < 3; ++a) l[a] = ws.pts[3 * j + a];
+  const int64_t o1 = po.off[j + 1];
+  for (int64_t o = po.off[j]; o < o1; ++o) {
+    const int32_t i = po.cam[o];
+    if (!intra(ws.part, i, j)) continue;  // W_k = 0
+    const double* vi = v + 9 * (size_t)i;
+    if (!ws.W) {  // w J_l^T (J_c v)
+      double Jc[27], Jl[9], w;
+      if (!get_J(ws, po.uv[o], ws.cams + 15 * (size_t)i, l, Jc, Jl, &w)) continue;
+      double y[3];
+      for (int r = 0; r < 3; ++r) {
+        double x = 0.0;
+        for (int a = 0; a < 9; ++a) x += Jc[9 * r + a] * vi[a];
+        y[r] = w * x;
+      }
+      for (int c = 0; c < 3; ++c) acc[c] += Jl[c] * y[0] + Jl[3 + c] * y[1] + Jl[6 + c] * y[2];
+      continue;
+    }
+    const double* Wk = ws.W + 27 * (size_t)po.k[o];
+    for (int c = 0; c < 3; ++c) {
+      double x = 0.0;
+      for (int a = 0; a < 9; ++a) x += Wk[3 * a + c] * vi[a];
+      acc[c] += x;
+    }
+  }
+  for (int c = 0; c < 3; ++c) t[3 * j + c] = acc[c];
 }
 
 // q_i = U'_i p_i - sum_{k of i} W_k V'^-1 t_j ; s[PQ] += p.q
@@ -581,7 +766,8 @@ __global__ void __launch_bounds__(kCoarseThreads, 4) k_cs_pass2(const double* __
     for (int c = 0; c < 3; ++c) u[c] = Vi[3 * c] * tj[0] + Vi[3 * c + 1] * tj[1] + Vi[3 * c + 2] * tj[2];
     if (!ws.W) {  // w J_c^T (J_l u)
       double Jc[27], Jl[9], w;
-      if (!get_J(ws, k, scam, j, Jc, Jl, &w)) continue;
+      const double l[3] = {ws.pts[3 * (size_t)j], ws.pts[3 * (size_t)j + 1], ws.pts[3 * (size_t)j + 2]};
+      if (!get_J(ws, ws.uv[k], scam, l, Jc, Jl, &w)) continue;
       double y[3];
       for (int r = 0; r < 3; ++r) y[r] = w * (Jl[3 * r] * u[0] + Jl[3 * r + 1] * u[1] + Jl[3 * r + 2] * u[2]);
 #pragma unroll
@@ -619,8 +805,15 @@ __global__ void __launch_bounds__(kCoarseThreads, 4) k_cs_pass2(const double* __
   if (threadIdx.x == 0) {
     double v = 0.0;
     for (int a = 0; a < 9; ++a) v += pq[a];
-    atomicAdd(w.s + S_PQ, v);
+    w.part[i] = v;  // p.q of camera i
   }
+}
+
+// s[PQ] = p.q, summed over the cameras in order
+__global__ void __launch_bounds__(kSumThreads) k_cs_pq(int64_t M, CS w) {
+  if (w.s[S_DONE] != 0.0) return;
+  const double v = sum_partials(w.part, M);
+  if (threadIdx.x == 0) w.s[S_PQ] = v;
 }
 
 // x += alpha p, r -= alpha q, z = P^-1 r, s[RZN] += r.z
@@ -644,8 +837,21 @@ __global__ void k_cs_update1(int64_t M, CS w) {
       rz += ri[a] * v;
     }
   }
-  for (int off = 16; off > 0; off >>= 1) rz += __shfl_down_sync(0xffffffffu, rz, off);
-  if ((threadIdx.x & 31) == 0 && rz != 0.0) atomicAdd(w.s + S_RZN, rz);
+  const double b = cta_sum(rz);
+  if (threadIdx.x == 0) w.part[blockIdx.x] = b;
+}
+
+// r.z of the new residual summed in order; beta = r.z_new / r.z; convergence test (the direction update after it
+// is skipped once converged: x is final after k_cs_update1)
+__global__ void __launch_bounds__(kSumThreads) k_cs_scalars(CS w, int64_t nparts, double tol2) {
+  if (w.s[S_DONE] != 0.0) return;
+  const double rzn = sum_partials(w.part, nparts);
+  if (threadIdx.x != 0) return;
+  w.s[S_BETA] = rzn / w.s[S_RZ];
+  w.s[S_RZN] = rzn;
+  w.s[S_RZ] = rzn;
+  w.s[S_ITERS] += 1.0;
+  if (!(rzn > tol2 * w.s[S_RZ0])) w.s[S_DONE] = 1.0;
 }
 
 // p = z + beta p
@@ -653,16 +859,7 @@ __global__ void k_cs_update2(int64_t M, CS w) {
   if (w.s[S_DONE] != 0.0) return;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= 9 * M) return;
-  const double beta = w.s[S_RZN] / w.s[S_RZ];
-  w.p[e] = w.z[e] + beta * w.p[e];
-}
-
-__global__ void k_cs_scalars(CS w, double tol2) {
-  if (w.s[S_DONE] != 0.0) return;
-  w.s[S_RZ] = w.s[S_RZN];
-  w.s[S_PQ] = w.s[S_RZN] = 0.0;
-  w.s[S_ITERS] += 1.0;
-  if (!(w.s[S_RZ] > tol2 * w.s[S_RZ0])) w.s[S_DONE] = 1.0;
+  w.p[e] = w.z[e] + w.s[S_BETA] * w.p[e];
 }
 
 // dl_j = -V'^-1 (g_l,j + t_j) with t = W^T dc; dc = x
@@ -680,7 +877,7 @@ __global__ void k_cs_backsub(const double* __restrict__ gl, int64_t N, CS w, dou
 
 extern "C" int64_t daba_coarse_solve_workspace(int64_t M, int64_t N) {
   if (M < 0 || N < 0) return -1;
-  return M * 81 + N * 9 + N * 3 + N * 3 + 5 * M * 9 + daba::S_COLS + 8;
+  return M * 81 + N * 9 + N * 3 + N * 3 + 5 * M * 9 + daba::S_COLS + 8 + M + 1;
 }
 
 namespace daba {
@@ -688,7 +885,7 @@ namespace {
 // bad_dev (host, kMaxDev): per device, how many damped blocks were not positive definite (a failed trial of that
 // device, R-N3c); the system is block diagonal over the devices, so the other devices' directions are unaffected.
 int coarse_solve_impl(const double* U, const double* gc, const double* V, const double* gl, WSrc ws,
-                      const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N,
+                      const PtOrder& po, const int32_t* obs_cam, const int32_t* obs_pt, const int64_t* cam_off, int64_t M, int64_t N,
                       int64_t K, double xi, double mu, int max_iter, double tol, double* dc, double* dl, double* work,
                       double info[2], int bad_dev[kMaxDev], void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -704,6 +901,8 @@ int coarse_solve_impl(const double* U, const double* gc, const double* V, const 
   w.q = o; o += M * 9;
   w.s = o; o += S_COLS;
   int* bad = reinterpret_cast<int*>(o);
+  o += 8;
+  w.part = o;  // M + 1
   w.x = dc;  // the camera direction is PCG's iterate
   const int T = 256;
   const unsigned gM = (unsigned)((M + T - 1) / T), gN = (unsigned)((N + T - 1) / T), gK = (unsigned)((K + T - 1) / T),
@@ -714,21 +913,34 @@ int coarse_solve_impl(const double* U, const double* gc, const double* V, const 
     k_cs_cams<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, gc, ws, obs_pt, cam_off, xi, mu, w, bad);
     k_cs_inv<<<(unsigned)((M + 63) / 64), 64, 0, st>>>(M, w, bad, ws.part);
     k_cs_init<<<gM, T, 0, st>>>(M, w);
+    k_cs_start<<<1, kSumThreads, 0, st>>>(w, gM);
+  } else {
+    k_cs_start<<<1, kSumThreads, 0, st>>>(w, 0);
   }
-  k_cs_start<<<1, 1, 0, st>>>(w);
-  for (int it = 0; it < max_iter && M > 0; ++it) {
-    if (N > 0) {
-      if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
-      if (K > 0) k_cs_pass1<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, w.p, w.t, w.s, 1);
+  const bool det = po.off != nullptr;  // deterministic: t in point order
+  auto pass1 = [&](const double* v, int check_done) -> int {
+    if (det) {
+      k_cs_pass1_pts<<<gN, T, 0, st>>>(ws, po, N, v, w.t, w.s, check_done);
+      return 0;
     }
+    if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
+    if (K > 0) k_cs_pass1_obs<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, v, w.t, w.s, check_done);
+    return 0;
+  };
+  for (int it = 0; it < max_iter && M > 0; ++it) {
+    if (N > 0 && pass1(w.p, 1)) return -3;
     k_cs_pass2<<<(unsigned)M, kCoarseThreads, 0, st>>>(U, ws, obs_pt, cam_off, xi, mu, w);
+    k_cs_pq<<<1, kSumThreads, 0, st>>>(M, w);
     k_cs_update1<<<gM, T, 0, st>>>(M, w);
+    k_cs_scalars<<<1, kSumThreads, 0, st>>>(w, gM, tol * tol);
     k_cs_update2<<<g9M, T, 0, st>>>(M, w);
-    k_cs_scalars<<<1, 1, 0, st>>>(w, tol * tol);
   }
   if (N > 0) {  // back-substitution for the points
-    if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) return -3;
-    if (K > 0 && M > 0) k_cs_pass1<<<gK, T, 0, st>>>(ws, obs_cam, obs_pt, K, dc, w.t, w.s, 0);
+    if (M > 0) {
+      if (pass1(dc, 0)) return -3;
+    } else if (cudaMemsetAsync(w.t, 0, (size_t)N * 3 * sizeof(double), st) != cudaSuccess) {
+      return -3;
+    }
     k_cs_backsub<<<gN, T, 0, st>>>(gl, N, w, dl);
   }
   double s[S_COLS + 4];
@@ -747,19 +959,21 @@ extern "C" int daba_coarse_solve(const double* U, const double* gc, const double
                                  int64_t N, int64_t K, double xi, double mu, int max_iter, double tol, double* dc,
                                  double* dl, double* work, double info[2], void* stream) {
   using namespace daba;
-  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || !(xi >= 0) || !(mu >= 0) || max_iter < 0 || !(tol >= 0) || !info)
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || !(xi >= 0) || !(mu >= 0) ||
+      max_iter < 0 || !(tol >= 0) || !info)
     return -1;
   if ((M > 0 && (!U || !gc || !cam_off || !dc || !work)) || (N > 0 && (!V || !gl || !dl || !work)) ||
-      (K > 0 && (!W || !obs_cam || !obs_pt)))
+      (K > 0 && (!W || !obs_cam || !obs_pt)) || (M == 0 && K > 0))
     return -1;
   WSrc ws{W, nullptr, nullptr, nullptr, 0, 1.0, 0.0, Part{nullptr, nullptr, 1}};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (M > 0) {
-    const int v = validate(obs_cam, obs_pt, cam_off, M, N, K, ws.part, static_cast<cudaStream_t>(stream));
+    const int v = validate(obs_cam, obs_pt, cam_off, M, N, K, ws.part, st);
     if (v) return v;
   }
   int bad[kMaxDev];
-  const int rc = coarse_solve_impl(U, gc, V, gl, ws, obs_cam, obs_pt, cam_off, M, N, K, xi, mu, max_iter, tol, dc, dl,
-                                   work, info, bad, stream);
+  const int rc = coarse_solve_impl(U, gc, V, gl, ws, PtOrder{}, obs_cam, obs_pt, cam_off, M, N, K, xi, mu, max_iter,
+                                   tol, dc, dl, work, info, bad, stream);
   return rc ? rc : (bad[0] ? -6 : 0);  // a damped block not positive definite: a failed LM trial (R-N3c)
 }
 
@@ -1041,6 +1255,7 @@ struct Run {
   int trials, pcg_iter;
   double pcg_tol;
   Part part;
+  PtOrder po{};  // the observations in point order (the point-side passes)
   double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal, *dEc;
   cudaStream_t st;
   unsigned active = ~0u;  // devices whose LM acceptance matters (a rank's own device; the halo device is fixed)
@@ -1092,7 +1307,7 @@ int run_dE(const Run& R, const double* c, const double* l, const double* ch, con
 // dE[a] = E^a(x_new | anchor) - E^a(anchor | anchor) (0 if none accepted).
 int lm_step(const Run& R, const double* ca, const double* la, double* co, double* lo, double* ct, double* lt,
             int trial[kMaxDev], double dE[kMaxDev]) {
-  int rc = coarse_blocks_impl(ca, R.M, la, R.N, R.op, R.uv, R.off, R.loss, R.scale, R.eps2, R.part, R.U, R.gc, R.V,
+  int rc = coarse_blocks_impl(ca, R.M, la, R.N, R.op, R.uv, R.off, R.po, R.loss, R.scale, R.eps2, R.part, R.U, R.gc, R.V,
                               R.gl, nullptr, R.Fc, R.st);  // W recomputed in the PCG passes
   if (rc) return rc;
   if (R.M && cudaMemcpyAsync(co, ca, R.M * 15 * sizeof(double), cudaMemcpyDeviceToDevice, R.st) != cudaSuccess)
@@ -1109,7 +1324,7 @@ int lm_step(const Run& R, const double* ca, const double* la, double* co, double
     double info[2], dEt[kMaxDev];
     int bad[kMaxDev];
     const WSrc ws{nullptr, ca, la, R.uv, R.loss, R.scale, R.eps2, R.part};
-    rc = coarse_solve_impl(R.U, R.gc, R.V, R.gl, ws, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter,
+    rc = coarse_solve_impl(R.U, R.gc, R.V, R.gl, ws, R.po, R.oc, R.op, R.off, R.M, R.N, R.K, R.xi, mu, R.pcg_iter,
                            R.pcg_tol, R.dcv, R.dlv, R.work, info, bad, R.st);
     if (rc) return rc;
     if (g) k_cr_retract<<<g, 256, 0, R.st>>>(ca, la, R.dcv, R.dlv, R.M, R.N, ct, lt);
@@ -1139,7 +1354,8 @@ int coarse_run_impl(double* cams, int64_t M, double* pts, int64_t N, const int32
         o.eps * o.eps, o.eps, o.xi, o.mu0, o.mu_up, o.lm_trials, o.pcg_max_iter, o.pcg_tol, part};
   R.st = st;
   const size_t nc = (size_t)M * 15, nl = (size_t)N * 3;
-  const size_t total = 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)N * (9 + 3 + 3) +
+  const size_t npo = o.deterministic ? pt_order_doubles(K, N, true) : 0;
+  const size_t total = npo + 5 * (nc + nl) + (size_t)M * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)N * (9 + 3 + 3) +
                        (size_t)daba_coarse_solve_workspace(M, N) + 8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev;
   double* base = nullptr;
   // scratch from the retained pool (mapping ~1.6 GB afresh per call at Final-13682 cost ~300 ms); unless
@@ -1154,6 +1370,7 @@ int coarse_run_impl(double* cams, int64_t M, double* pts, int64_t N, const int32
     return -5;
   double* op = base;
   auto take = [&](size_t n) { double* p = op; op += n; return p; };
+  double* pos = take(npo);  // first: 16-byte aligned for the pixels
   double *cp = take(nc), *lp = take(nl), *cb = take(nc), *lb = take(nl), *ca = take(nc), *la = take(nl),
          *cm = take(nc), *lm = take(nl), *ct = take(nc), *lt = take(nl);
   R.U = take((size_t)M * 81);
@@ -1167,10 +1384,10 @@ int coarse_run_impl(double* cams, int64_t M, double* pts, int64_t N, const int32
   R.W = nullptr;
   R.work = take((size_t)daba_coarse_solve_workspace(M, N));
   R.scal = take(8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev);
-  int rc = 0;
+  int rc = o.deterministic ? build_pt_order(obs_cam, obs_pt, R.uv, K, N, pos, st, &R.po) : 0;
   // x^{-1} = x^0 (eq. Fainit); F-bar^{-1} = F(x^0) (A18, global form); s^0 = 1
-  if (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-      cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+  if (!rc && (cudaMemcpyAsync(cp, cams, nc * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+               cudaMemcpyAsync(lp, pts, nl * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess))
     rc = -3;
   double Fbar = 0.0, s = 1.0;
   if (!rc) rc = run_F(R, cams, pts, &Fbar);
@@ -1245,6 +1462,7 @@ extern "C" void daba_coarse_default_options(daba_coarse_options* o) {
   o->pcg_tol = 1e-2;
   o->mm_always = 0;
   o->keep_scratch = 0;
+  o->deterministic = 0;
 }
 
 // The device the caller's arrays live on becomes current for the call (round-1 advisor): pools, scratch and launches
@@ -1470,8 +1688,10 @@ extern "C" int daba_coarse_run_dist(const double* cameras, int64_t M, const doub
     R.M_F = noc;    // F counts each pair once, on its camera's owner
     const size_t ncl = (size_t)nc * 15, nl = (size_t)npt * 3;
     double* base = nullptr;
+    const size_t npo = o.deterministic ? pt_order_doubles(KL, npt, true) : 0;
     if (!rc) {
-      const size_t total = 5 * (ncl + nl) + (size_t)nc * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)npt * (9 + 3 + 3) +
+      const size_t total = npo + 5 * (ncl + nl) +
+                           (size_t)nc * (81 + 9 + 1 + 9 + kMaxDev) + (size_t)npt * (9 + 3 + 3) +
                            (size_t)daba_coarse_solve_workspace(nc, npt) + 8 + 2 * kEvalBlocks + kDEBlocks * kMaxDev;
       if (!(base = B.get<double>(total))) rc = -5;
     }
@@ -1479,6 +1699,8 @@ extern "C" int daba_coarse_run_dist(const double* cameras, int64_t M, const doub
     if (!rc) {
       double* op = base;
       auto take = [&](size_t n) { double* p = op; op += n; return p; };
+      double* pos = take(npo);  // first: 16-byte aligned for the pixels
+      if (o.deterministic) rc = build_pt_order(doc, dop, R.uv, KL, npt, pos, st, &R.po);
       double *cp = take(ncl), *lp = take(nl), *cb = take(ncl), *lb = take(nl), *ca = take(ncl), *la = take(nl),
              *cm = take(ncl), *lm = take(nl), *ct = take(ncl), *lt = take(nl);
       R.U = take((size_t)nc * 81);

@@ -53,7 +53,8 @@ class CoarseOptions(ctypes.Structure):
     _fields_ = [("loss", ctypes.c_int), ("scale", ctypes.c_double), ("eps", ctypes.c_double), ("xi", ctypes.c_double),
                 ("eta", ctypes.c_double), ("mu0", ctypes.c_double), ("mu_up", ctypes.c_double),
                 ("lm_trials", ctypes.c_int), ("accelerate", ctypes.c_int), ("pcg_max_iter", ctypes.c_int),
-                ("pcg_tol", ctypes.c_double), ("mm_always", ctypes.c_int), ("keep_scratch", ctypes.c_int)]
+                ("pcg_tol", ctypes.c_double), ("mm_always", ctypes.c_int), ("keep_scratch", ctypes.c_int),
+                ("deterministic", ctypes.c_int)]
 
 
 def lib():

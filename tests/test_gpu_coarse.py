@@ -242,10 +242,11 @@ def _partition(p, ndev, kind, seed=0):
     return cam_dev, cnt.argmax(axis=1)
 
 
-@pytest.mark.parametrize("ndev,kind,loss,eta", [(2, "contiguous", oracle.LOSS_HUBER, 0.1),
-                                                (3, "random", oracle.LOSS_CAUCHY, 1.0),
-                                                (2, "random", oracle.LOSS_TRIVIAL, 1.0)])
-def test_coarse_run_partitioned_matches_the_oracle(ndev, kind, loss, eta):
+@pytest.mark.parametrize("ndev,kind,loss,eta,det", [(2, "contiguous", oracle.LOSS_HUBER, 0.1, 0),
+                                                    (3, "random", oracle.LOSS_CAUCHY, 1.0, 1),
+                                                    (2, "random", oracle.LOSS_TRIVIAL, 1.0, 0),
+                                                    (2, "contiguous", oracle.LOSS_HUBER, 0.1, 1)])
+def test_coarse_run_partitioned_matches_the_oracle(ndev, kind, loss, eta, det):
     """daba_coarse_run_part (eq. Ealpha: E' pairs exact in their device's LM step, E'' pairs majorized by P on the
     camera's device and Q on the point's; each device accepts its own first decreasing trial) against
     oracle/coarse.run with the same device assignment: restart flags identical, F / F-bar / E traces within 1e-9,
@@ -255,7 +256,7 @@ def test_coarse_run_partitioned_matches_the_oracle(ndev, kind, loss, eta):
     cp = coarse.Problem(p, cam_dev, pt_dev, eta=eta)
     assert 0 < cp.intra.sum() < cp.K  # both kinds of pairs occur
     tr_ref, c_ref, l_ref = coarse.run(cp, 8)
-    tr, trials, c, l = _run_part_gpu(cp, 8, cam_dev, pt_dev)
+    tr, trials, c, l = _run_part_gpu(cp, 8, cam_dev, pt_dev, deterministic=det)
     np.testing.assert_array_equal(tr[:, 3], tr_ref[:, 3])
     for col in (0, 1, 2, 4):
         np.testing.assert_allclose(tr[:, col], tr_ref[:, col], rtol=1e-9)
@@ -279,7 +280,7 @@ def test_coarse_run_one_device_entries_agree():
     tr0 = daba.coarse_run(cams, pts, t(cp.oc[order], torch.int32), t(cp.op[order], torch.int32),
                           t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 6, loss=cp.opt.kind,
                           scale=cp.opt.scale, pcg_max_iter=2000, pcg_tol=1e-15)
-    # (the PCG sums with fp64 atomics: two runs agree to rounding, not bitwise — include/daba.h)
+    # (the point sums with fp64 atomics: two runs agree to rounding, not bitwise — include/daba.h)
     np.testing.assert_array_equal(tr1[:, 3], tr0[:, 3])
     np.testing.assert_allclose(tr1, tr0, rtol=1e-10)
     np.testing.assert_allclose(c1, cams.cpu().numpy(), rtol=0, atol=1e-10 * np.abs(c1).max())
@@ -293,16 +294,37 @@ def test_coarse_run_mm_only_on_restart(ndev):
     cam_dev, pt_dev = _partition(p, ndev, "contiguous")
     cp = coarse.Problem(p, cam_dev, pt_dev, eta=1.0)
     kw = dict(cam_dev=cam_dev, pt_dev=pt_dev) if ndev > 1 else {}
-    tra, _, ca, la = _run_part_gpu(cp, 10, mm_always=1, **kw)
-    trb, trials_b, cb, lb = _run_part_gpu(cp, 10, mm_always=0, **kw)
+    tra, _, ca, la = _run_part_gpu(cp, 10, mm_always=1, deterministic=1, **kw)
+    trb, trials_b, cb, lb = _run_part_gpu(cp, 10, mm_always=0, deterministic=1, **kw)
     rs = tra[:, 3] == 1
     assert rs.any() and (~rs).any()
-    np.testing.assert_array_equal(trb[:, 3], tra[:, 3])
-    np.testing.assert_allclose(trb[:, :3], tra[:, :3], rtol=1e-10)  # (rounding: fp64 atomics in the PCG)
-    np.testing.assert_allclose(trb[rs, 4], tra[rs, 4], rtol=1e-10)
+    np.testing.assert_array_equal(trb[:, :4], tra[:, :4])  # (deterministic mode: bit for bit)
+    np.testing.assert_array_equal(trb[rs, 4], tra[rs, 4])
     assert np.all(np.isnan(trb[~rs, 4])) and np.all(trials_b[~rs, 1] == -1)
-    np.testing.assert_allclose(cb, ca, rtol=0, atol=1e-10 * np.abs(ca).max())
-    np.testing.assert_allclose(lb, la, rtol=0, atol=1e-10 * np.abs(la).max())
+    np.testing.assert_array_equal(cb, ca)
+    np.testing.assert_array_equal(lb, la)
+
+
+@pytest.mark.parametrize("ndev", [1, 3])
+def test_coarse_run_deterministic_mode(ndev):
+    """deterministic = 1 takes every sum in a fixed order (the point sides over a stable sort by point, the PCG
+    scalars by per-CTA partials; no fp64 atomics): two runs of the inexact configuration the timing tools use (PCG
+    <= 3 iterations, tol 1e-1) give identical traces, accepted trials and states; and they equal the atomic mode's
+    run to rounding (the same iteration, another summation order)."""
+    p = gen.generate("ladybug49", loss=oracle.LOSS_HUBER, outlier_frac=0.05)
+    cam_dev, pt_dev = _partition(p, ndev, "contiguous")
+    cp = coarse.Problem(p, cam_dev, pt_dev, eta=0.1)
+    kw = dict(cam_dev=cam_dev, pt_dev=pt_dev) if ndev > 1 else {}
+    runs = [_run_part_gpu(cp, 6, pcg_max_iter=3, pcg_tol=1e-1, mm_always=0, deterministic=1, **kw) for _ in range(2)]
+    for a, b in zip(runs[0], runs[1]):
+        np.testing.assert_array_equal(a, b)
+    assert runs[0][0][-1, 0] < runs[0][0][0, 0]
+    tr, trials, c, l = _run_part_gpu(cp, 6, pcg_max_iter=3, pcg_tol=1e-1, mm_always=0, **kw)
+    np.testing.assert_array_equal(tr[:, 3], runs[0][0][:, 3])
+    np.testing.assert_array_equal(trials, runs[0][1])
+    np.testing.assert_allclose(tr[:, :3], runs[0][0][:, :3], rtol=1e-9)
+    assert np.abs(c - runs[0][2]).max() <= 1e-7 * np.abs(c).max()
+    assert np.abs(l - runs[0][3]).max() <= 1e-7 * np.abs(l).max()
 
 
 def test_coarse_entries_reject_bad_indices_before_writing():
@@ -341,8 +363,8 @@ def test_coarse_entries_reject_bad_indices_before_writing():
                              t(cp.op[order], torch.int32), t(cp.uv[order], torch.float64), t(cam_off, torch.int64), 1)
 
 
-@pytest.mark.parametrize("nranks,loss,eta", [(2, oracle.LOSS_HUBER, 0.1), (3, oracle.LOSS_CAUCHY, 1.0)])
-def test_coarse_run_dist_matches_the_oracle(nranks, loss, eta):
+@pytest.mark.parametrize("nranks,loss,eta,det", [(2, oracle.LOSS_HUBER, 0.1, 0), (3, oracle.LOSS_CAUCHY, 1.0, 1)])
+def test_coarse_run_dist_matches_the_oracle(nranks, loss, eta, det):
     """NEXT-3 with one device per rank (daba_coarse_run_dist; ranks = threads through the LOCAL transport, each
     solving its own device's subproblem, allreducing F / E and exchanging the boundary variables): equal to
     oracle/coarse.run with the daba_create partition as the device assignment — restart flags identical, traces
@@ -362,7 +384,7 @@ def test_coarse_run_dist_matches_the_oracle(nranks, loss, eta):
         try:
             out[r] = daba.coarse_run_dist(p.cams, p.pts, p.obs_cam, p.obs_pt, p.obs_uv, 8, rank=r, nranks=nranks,
                                           comm_key=key, comm=daba.COMM_LOCAL, loss=loss, scale=p.loss_scale, eta=eta,
-                                          pcg_max_iter=2000, pcg_tol=1e-15, mm_always=1)
+                                          pcg_max_iter=2000, pcg_tol=1e-15, mm_always=1, deterministic=det)
         except Exception as e:  # pragma: no cover
             err.append(e)
     th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]

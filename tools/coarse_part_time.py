@@ -2,7 +2,7 @@
 iterations for ndev devices (contiguous camera ranges, plurality points), the MM subproblem only on restarts
 (mm_always = 0), against the finest partition (daba_iterate) to the same F.
 
-    python tools/coarse_part_time.py CONFIG N_ITERS PCG_ITERS PCG_TOL NDEV[,NDEV...]
+    python tools/coarse_part_time.py CONFIG N_ITERS PCG_ITERS PCG_TOL NDEV[,NDEV...]     (COARSE_DET=1: deterministic)
 """
 import json
 import os
@@ -46,7 +46,8 @@ out = {"config": cfg, "M": p.M, "N": p.N, "K": p.K, "iters": n, "pcg_max_iter": 
        "finest_ms_per_iter": finest_ms, "runs": []}
 for nd in ndevs:
     cd, pd = contiguous_partition(p, nd)
-    kw = dict(loss=p.loss, scale=p.loss_scale, pcg_max_iter=pcg, pcg_tol=tol, mm_always=0, keep_scratch=1)
+    kw = dict(loss=p.loss, scale=p.loss_scale, pcg_max_iter=pcg, pcg_tol=tol, mm_always=0, keep_scratch=1,
+              deterministic=int(os.environ.get("COARSE_DET", "0")))
     part = dict(cam_dev=t(cd, torch.int32), pt_dev=t(pd, torch.int32), ndev=nd) if nd > 1 else {}
     daba.coarse_run_part(c0.clone(), l0.clone(), *args, 1, **part, **kw)  # warm-up
     cams, pts = c0.clone(), l0.clone()

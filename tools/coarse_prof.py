@@ -25,5 +25,5 @@ if ndev > 1:
     cd, pd = contiguous_partition(p, ndev)
     part = dict(cam_dev=t(cd, torch.int32), pt_dev=t(pd, torch.int32), ndev=ndev)
 tr, _ = daba.coarse_run_part(cams, pts, *args, iters, loss=p.loss, scale=p.loss_scale, pcg_max_iter=3, pcg_tol=1e-1,
-                             mm_always=0, **part)
+                             mm_always=0, deterministic=int(os.environ.get("COARSE_DET", "0")), **part)
 print(tr)
