@@ -1330,6 +1330,7 @@ extern "C" void daba_destroy(daba_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);  // (a create that failed with a side-stream upload in flight)
   collect_times(ctx);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
