@@ -656,7 +656,11 @@ __device__ void finish_block(const IterParams& p) {
 // CTAs/SM 0.607 / 0.717, 4 records at 3 CTAs/SM spill: 1.14, a max-L1 carve-out 0.69)
 __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
   double qv[kPtCols] = {0, 0, 0, 0};
-  for (int j = blockIdx.x * kPtPassThreads + threadIdx.x; j < p.n_own_pts; j += gridDim.x * kPtPassThreads) {
+  for (int jj = blockIdx.x * kPtPassThreads + threadIdx.x; jj < p.n_own_pts; jj += gridDim.x * kPtPassThreads) {
+    // highest point first: the camera pass writes the last cameras' records last, so theirs are the ones still in
+    // L2, and (points numbered along the cameras) the highest points read them (8-rank shard of Final-13682:
+    // 0.1078 -> 0.1060 ms; one rank unchanged)
+    const int j = p.n_own_pts - 1 - jj;
     const double4 k4 = p.pts[p.roles[1]][j], b4 = p.lbar[p.roles[4]][j];
     const double lk[3] = {k4.x, k4.y, k4.z};
     const double lb[3] = {b4.x, b4.y, b4.z};
