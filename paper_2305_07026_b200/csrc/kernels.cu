@@ -125,32 +125,12 @@ struct CamRegs {
 #define DABA_MINB (384 / DABA_CPT)  // 12 warps per SM: the 170-register budget of the moment accumulators
 #endif
 
-// One observation's contribution to the camera moments at one anchor.
-template <int LOSS, bool ACC>
-__device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, double2 u, double lx, double ly,
-                                        double lz, double* acc, int64_t rec) {
-  const double s = fma(u.x, u.x, u.y * u.y);
-  const double s2 = s * s;
-  const double pz = fma(s, fma(s, c[14], c[13]), c[12]);  // eq. ray
-  const double vx = lx - c[9], vy = ly - c[10], vz = lz - c[11];
-  const double nv = fma(vx, vx, fma(vy, vy, vz * vz));
-  if (!(nv > p.eps2)) {  // Assumption 2 violated at this anchor: the pair contributes nothing
-    acc[40] += 1.0;
-    if (rec >= 0)
-      st256(rec_ptr(p, rec, ACC ? 0 : 1), make_double4(0.0, 0.0, 0.0, 0.0));
-    return;
-  }
-  // world-frame ray R p, lambda = (l - t).R p / |l - t|^2 (eq. gamma), world-frame error R e = R p - lambda (l - t)
-  // (eq. error): the moments of e are accumulated in the world frame and rotated by R_hat^T once per camera in
-  // k_cam_solve (they are linear in e), and R e is also the point-side record's vector
-  const double rx = fma(c[0], u.x, fma(c[1], u.y, c[2] * pz));
-  const double ry = fma(c[3], u.x, fma(c[4], u.y, c[5] * pz));
-  const double rz = fma(c[6], u.x, fma(c[7], u.y, c[8] * pz));
-  const double lam = fma(vx, rx, fma(vy, ry, vz * rz)) * rcp_d(nv);  // eq. gamma
-  const double ex = fma(-lam, vx, rx), ey = fma(-lam, vy, ry), ez = fma(-lam, vz, rz);  // R e (eq. error)
-  const double sh = fma(ex, ex, fma(ey, ey, ez * ez));
-  double rho = 0;
-  const double w = loss_eval<LOSS, !ACC>(sh, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
+// One observation's moments and point-side record at one anchor, from its geometry (s = |u|^2, lambda, the
+// world-frame error R e, |R e|^2, w = rho', rho).
+template <bool ACC>
+__device__ __forceinline__ void obs_moments(const IterParams& p, double2 u, double s, double s2, double lam, double ex,
+                                            double ey, double ez, double sh, double w, double rho, double* acc,
+                                            int64_t rec) {
   const double wx = w * u.x, wy = w * u.y, ws = w * s, ws2 = w * s2;
   acc[0] = fma(wx, u.x, acc[0]);
   acc[1] = fma(wx, u.y, acc[1]);
@@ -200,6 +180,68 @@ __device__ __forceinline__ void cam_obs(const IterParams& p, const CamRegs& c, d
   // coalesced at the camera-side index (one 32-byte record per anchor)
   if (rec >= 0)
     st256(rec_ptr(p, rec, ACC ? 0 : 1), make_double4(wl * lam, wl * ex, wl * ey, wl * ez));
+}
+
+// Two observations of one camera at one anchor: each camera value is read from shared memory once for both
+// (15 shared loads per pair instead of per observation), the two dependency chains interleaved.  Per observation:
+// s = |u|^2, p = (u, d1 + d2 s + d3 s^2) (eq. ray), v = l - t, the world-frame ray R p, lambda = v.R p / |v|^2
+// (eq. gamma), the world-frame error R e = R p - lambda v (eq. error; its moments are rotated into the anchor
+// camera frame once per camera by k_cam_solve), w = rho'(|R e|^2) (eq. w); a pair violating Assumption 2 at this
+// anchor contributes nothing (counted in slot 40, zero record).
+template <int LOSS, bool ACC>
+__device__ __forceinline__ void cam_obs2(const IterParams& p, const CamRegs& c, double2 u0, double4 l0, double2 u1,
+                                         double4 l1, bool has1, double* acc, int64_t rec0, int64_t rec1) {
+  const double s0 = fma(u0.x, u0.x, u0.y * u0.y), s1 = fma(u1.x, u1.x, u1.y * u1.y);
+  double pz0, pz1, vx0, vy0, vz0, vx1, vy1, vz1, rx0, ry0, rz0, rx1, ry1, rz1;
+  {
+    const double d0 = c[12], d1 = c[13], d2 = c[14];
+    pz0 = fma(s0, fma(s0, d2, d1), d0);  // eq. ray
+    pz1 = fma(s1, fma(s1, d2, d1), d0);
+  }
+  {
+    const double tx = c[9], ty = c[10], tz = c[11];
+    vx0 = l0.x - tx; vy0 = l0.y - ty; vz0 = l0.z - tz;
+    vx1 = l1.x - tx; vy1 = l1.y - ty; vz1 = l1.z - tz;
+  }
+  {
+    const double a = c[0], b = c[1], d = c[2];
+    rx0 = fma(a, u0.x, fma(b, u0.y, d * pz0));
+    rx1 = fma(a, u1.x, fma(b, u1.y, d * pz1));
+  }
+  {
+    const double a = c[3], b = c[4], d = c[5];
+    ry0 = fma(a, u0.x, fma(b, u0.y, d * pz0));
+    ry1 = fma(a, u1.x, fma(b, u1.y, d * pz1));
+  }
+  {
+    const double a = c[6], b = c[7], d = c[8];
+    rz0 = fma(a, u0.x, fma(b, u0.y, d * pz0));
+    rz1 = fma(a, u1.x, fma(b, u1.y, d * pz1));
+  }
+  const double nv0 = fma(vx0, vx0, fma(vy0, vy0, vz0 * vz0)), nv1 = fma(vx1, vx1, fma(vy1, vy1, vz1 * vz1));
+  const bool ok0 = nv0 > p.eps2, ok1 = nv1 > p.eps2;  // Assumption 2 at this anchor
+  const double lam0 = fma(vx0, rx0, fma(vy0, ry0, vz0 * rz0)) * rcp_d(nv0);  // eq. gamma
+  const double lam1 = fma(vx1, rx1, fma(vy1, ry1, vz1 * rz1)) * rcp_d(nv1);
+  const double ex0 = fma(-lam0, vx0, rx0), ey0 = fma(-lam0, vy0, ry0), ez0 = fma(-lam0, vz0, rz0);  // eq. error
+  const double ex1 = fma(-lam1, vx1, rx1), ey1 = fma(-lam1, vy1, ry1), ez1 = fma(-lam1, vz1, rz1);
+  const double sh0 = fma(ex0, ex0, fma(ey0, ey0, ez0 * ez0)), sh1 = fma(ex1, ex1, fma(ey1, ey1, ez1 * ez1));
+  if (ok0) {
+    double rho = 0;
+    const double w = loss_eval<LOSS, !ACC>(sh0, p.delta, p.delta2, p.idelta2, &rho);  // eq. w
+    obs_moments<ACC>(p, u0, s0, s0 * s0, lam0, ex0, ey0, ez0, sh0, w, rho, acc, rec0);
+  } else {  // the pair contributes nothing
+    acc[40] += 1.0;
+    if (rec0 >= 0) st256(rec_ptr(p, rec0, ACC ? 0 : 1), make_double4(0.0, 0.0, 0.0, 0.0));
+  }
+  if (!has1) return;
+  if (ok1) {
+    double rho = 0;
+    const double w = loss_eval<LOSS, !ACC>(sh1, p.delta, p.delta2, p.idelta2, &rho);
+    obs_moments<ACC>(p, u1, s1, s1 * s1, lam1, ex1, ey1, ez1, sh1, w, rho, acc, rec1);
+  } else {
+    acc[40] += 1.0;
+    if (rec1 >= 0) st256(rec_ptr(p, rec1, ACC ? 0 : 1), make_double4(0.0, 0.0, 0.0, 0.0));
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -259,8 +301,8 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
     const double2 u1 = *uslot(k + 1);
     issue(k + kRing);  // refills the two slots just read
     issue(k + kRing + 1);
-    cam_obs<LOSS, ACC>(p, c, u0, l0.x, l0.y, l0.z, acc, REC(k));
-    if (k + 1 < n) cam_obs<LOSS, ACC>(p, c, u1, l1.x, l1.y, l1.z, acc, REC(k + 1));
+    // (one camera read per pair: 0.7093 -> 0.7034 ms against one observation at a time, Final-13682)
+    cam_obs2<LOSS, ACC>(p, c, u0, l0, u1, l1, k + 1 < n, acc, REC(k), REC(k + 1));
   }
   cp_async_wait<0>();
 #undef REC
