@@ -1256,8 +1256,9 @@ struct Run {
   double pcg_tol;
   Part part;
   PtOrder po{};  // the observations in point order (the point-side passes)
-  double *U, *gc, *V, *gl, *W, *Fc, *dcv, *dlv, *work, *scal, *dEc;
-  cudaStream_t st;
+  double *U = nullptr, *gc = nullptr, *V = nullptr, *gl = nullptr, *W = nullptr, *Fc = nullptr, *dcv = nullptr,
+         *dlv = nullptr, *work = nullptr, *scal = nullptr, *dEc = nullptr;
+  cudaStream_t st = nullptr;
   unsigned active = ~0u;  // devices whose LM acceptance matters (a rank's own device; the halo device is fixed)
   int64_t M_F = -1;       // F(x) sums the first M_F cameras' pairs (a rank's own cameras); -1: all
 };
