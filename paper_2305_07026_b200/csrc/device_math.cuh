@@ -28,6 +28,43 @@ __device__ __forceinline__ double rsqrt_d(double x) {
   return y * fma(-h * y, y, 1.5);
 }
 
+// log(1 + q) for q >= 0 (the Cauchy loss's rho at every observation of the x^k anchor): q < sqrt(2) - 1 takes
+// f = q / (2 + q) directly (no rounding of 1 + q), larger q reduces 1 + q = m 2^e with m in [sqrt(1/2), sqrt(2))
+// and f = (m - 1) / (m + 1); then log1p = e ln 2 + 2 atanh(f), the atanh series to f^21 (|f| <= 0.1716, so the
+// first omitted term is below 2^-53 of the sum).  Within a few ulp of the correctly rounded value; about a third of
+// the FP64 instructions of the library log1p (camera pass on the Cauchy slab: see DESIGN.md §6).  NaN / inf (and
+// negative q, which the loss never passes) go to the library routine.
+__device__ __forceinline__ double log1p_pos(double q) {
+  if (!(q >= 0.0 && q <= 1.7976931348623157e308)) return log1p(q);
+  const double u = 1.0 + q;
+  const int hi = __double2hiint(u);
+  int e = (hi >> 20) - 1023;
+  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(u));  // [1, 2)
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const bool small = q < 0.41421356237309503;
+  const double num = small ? q : m - 1.0;
+  const double den = small ? 2.0 + q : m + 1.0;
+  const double f = num * rcp_d(den);
+  const double z = f * f;
+  double P = 1.0 / 21;
+  P = fma(P, z, 1.0 / 19);
+  P = fma(P, z, 1.0 / 17);
+  P = fma(P, z, 1.0 / 15);
+  P = fma(P, z, 1.0 / 13);
+  P = fma(P, z, 1.0 / 11);
+  P = fma(P, z, 1.0 / 9);
+  P = fma(P, z, 1.0 / 7);
+  P = fma(P, z, 1.0 / 5);
+  P = fma(P, z, 1.0 / 3);
+  const double f2 = f + f;
+  const double lm = fma(f2 * z, P, f2);  // 2 atanh(f) = log m
+  const double de = small ? 0.0 : (double)e;
+  return fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, lm));  // ln 2 = hi + lo
+}
+
 // Robust loss of eq. Fij, Assumption 1; delta2 = delta^2, idelta2 = 1/delta^2.
 // Returns w = rho'(s) and, when WANT_RHO, rho(s).
 template <int LOSS, bool WANT_RHO>
@@ -42,7 +79,11 @@ __device__ __forceinline__ double loss_eval(double s, double delta, double delta
     return delta * ri;
   } else if (LOSS == kCauchy) {
     const double q = s * idelta2;
+#ifndef DABA_LIB_LOG1P
+    if (WANT_RHO) *rho = delta2 * log1p_pos(q);
+#else
     if (WANT_RHO) *rho = delta2 * log1p(q);
+#endif
     return rcp_d(1.0 + q);  // = 1 / (1 + q) without the division's slow-path call
   } else {
     if (WANT_RHO) *rho = s;
