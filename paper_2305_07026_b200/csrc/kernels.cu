@@ -62,6 +62,17 @@ __device__ __forceinline__ double4 ld256(const double4* q) {
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(q));
   return v;
 }
+// The same for gathers with no reuse in L1 (points by the camera pass, records by the point sums): no L1 line
+// allocated, so the L1 / shared-memory array keeps what is reused (Final-13682: camera pass 0.704 -> 0.678 ms,
+// point sums 0.590 -> 0.581 ms, iteration 1.309 -> 1.268 ms).
+__device__ __forceinline__ double4 ld256_na(const double4* q) {
+  double4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(q));
+  return v;
+}
+
 __device__ __forceinline__ void st256(double4* q, double4 v) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(q), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w));
 }
@@ -288,14 +299,14 @@ __device__ __forceinline__ void cam_pass_body(const IterParams& p, const CamChun
   // two observations per step: two independent dependency chains feed the same accumulators; the next step's
   // point records are in flight (registers).  (Measured: one observation per step 0.90 ms vs 0.76 ms; a deeper
   // record prefetch was slower.)
-  double4 lq0 = 0 < n ? ld256(L + sidx[lane]) : make_double4(0, 0, 0, 0);
-  double4 lq1 = 1 < n ? ld256(L + sidx[lane + G]) : make_double4(0, 0, 0, 0);
+  double4 lq0 = 0 < n ? ld256_na(L + sidx[lane]) : make_double4(0, 0, 0, 0);
+  double4 lq1 = 1 < n ? ld256_na(L + sidx[lane + G]) : make_double4(0, 0, 0, 0);
   issue(kRing - 1);
 #pragma unroll 1
   for (int k = 0; k < n; k += 2) {
     const double4 l0 = lq0, l1 = lq1;
-    if (k + 2 < n) lq0 = ld256(L + sidx[lane + (k + 2) * G]);
-    if (k + 3 < n) lq1 = ld256(L + sidx[lane + (k + 3) * G]);
+    if (k + 2 < n) lq0 = ld256_na(L + sidx[lane + (k + 2) * G]);
+    if (k + 3 < n) lq1 = ld256_na(L + sidx[lane + (k + 3) * G]);
     cp_async_wait<kRing - 2>();  // groups k and k + 1 have landed
     const double2 u0 = *uslot(k);
     const double2 u1 = *uslot(k + 1);
@@ -718,8 +729,8 @@ __global__ void __launch_bounds__(kPtPassThreads, 2) k_pt_sum(IterParams p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (r[i] >= 0) {
-          A[i] = ld256(rec_ptr(p, r[i], 0));
-          B[i] = ld256(rec_ptr(p, r[i], 1));
+          A[i] = ld256_na(rec_ptr(p, r[i], 0));
+          B[i] = ld256_na(rec_ptr(p, r[i], 1));
         }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
