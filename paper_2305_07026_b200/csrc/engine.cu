@@ -851,6 +851,26 @@ extern "C" int daba_create(const double* cameras, int64_t M, const double* point
       bpt.push_back(S.p_pt[q]);
       buv.push_back(make_double2(obs_uv[2 * S.p_obs[q]], obs_uv[2 * S.p_obs[q] + 1]));
     }
+    if (bcam.size() > 1 && env_int("DABA_BSORT", 1) != 0) {
+      // boundary observations in camera order (stable): neighbouring threads of k_pt_boundary then share the halo
+      // camera's record in L1; the point side's record indices follow the permutation
+      std::vector<int32_t> perm(bcam.size()), rank_of(bcam.size());
+      for (size_t b = 0; b < perm.size(); ++b) perm[b] = (int32_t)b;
+      std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) { return bcam[(size_t)x] < bcam[(size_t)y]; });
+      std::vector<int32_t> c2(bcam.size()), p2(bcam.size());
+      std::vector<double2> u2(bcam.size());
+      for (size_t r = 0; r < perm.size(); ++r) {
+        rank_of[(size_t)perm[r]] = (int32_t)r;
+        c2[r] = bcam[(size_t)perm[r]];
+        p2[r] = bpt[(size_t)perm[r]];
+        u2[r] = buv[(size_t)perm[r]];
+      }
+      bcam.swap(c2);
+      bpt.swap(p2);
+      buv.swap(u2);
+      for (size_t q = 0; q < src.size(); ++q)
+        if (src[q] >= (int32_t)kc) src[q] = (int32_t)kc + rank_of[(size_t)(src[q] - (int32_t)kc)];
+    }
     P.n_cam_side = (int64_t)kc;
     P.n_boundary = (int64_t)bcam.size();
     P.n_records = std::max<int64_t>(P.n_cam_side + P.n_boundary, 1);
