@@ -542,19 +542,75 @@ __device__ __forceinline__ void get_W(const WSrc& s, int64_t k, const double* ca
     for (int c = 0; c < 3; ++c) Wk[3 * a + c] = w * (Jc[a] * Jl[c] + Jc[9 + a] * Jl[3 + c] + Jc[18 + a] * Jl[6 + c]);
 }
 
-// J_c, J_l and w of observation k at the anchor (false: degenerate pair, contributes nothing) -- for the W-free
-// products w J_l^T (J_c v) and w J_c^T (J_l u), which never hold W (fewer live registers than get_W).
-__device__ __forceinline__ bool get_J(const WSrc& s, double2 u, const double* cam, const double l[3], double Jc[27],
-                                      double Jl[9], double* w) {
+// The PCG products without forming J_c: with q = R p, v = l - t, inv = 1/|v|^2, Pi = I - v v^T inv,
+// J_c = [Pi (-[q]x), -J_l, (Pi R e3) b^T] and J_l = -v q^T inv + 2 lam v v^T inv - lam I (pair_jacobians), so
+//   J_c x = Pi (x_theta x q + R e3 (b . x_d)) - J_l x_t,
+//   J_c^T y = (q x Pi y, -J_l^T y, b (R e3 . Pi y)),
+// about 40 FLOP per product instead of forming the 27 entries of J_c and multiplying (same values up to rounding).
+struct PairGeo {
+  double q[3], v[3], inv, lam, s, w;
+};
+__device__ __forceinline__ bool get_geo(const WSrc& ws, double2 u, const double* cam, const double l[3],
+                                        PairGeo* g) {
+  const double s = u.x * u.x + u.y * u.y;
+  const double pz = cam[12] + cam[13] * s + cam[14] * s * s;  // eq. ray
+  for (int a = 0; a < 3; ++a) {
+    g->q[a] = cam[3 * a] * u.x + cam[3 * a + 1] * u.y + cam[3 * a + 2] * pz;  // R p
+    g->v[a] = l[a] - cam[9 + a];
+  }
+  const double nv = g->v[0] * g->v[0] + g->v[1] * g->v[1] + g->v[2] * g->v[2];
+  if (!(nv > ws.eps2)) return false;  // R-N3d
+  g->inv = 1.0 / nv;
+  g->lam = (g->v[0] * g->q[0] + g->v[1] * g->q[1] + g->v[2] * g->q[2]) * g->inv;  // eq. lambdaij
   double r[3];
-  if (!pair_jacobians(cam, l, u, s.eps2, r, Jc, Jl)) return false;
+  for (int a = 0; a < 3; ++a) r[a] = g->q[a] - g->lam * g->v[a];  // R e
   const double sh = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
-  const double d2 = s.delta * s.delta, id2 = 1.0 / d2;
+  const double d2 = ws.delta * ws.delta, id2 = 1.0 / d2;
   double rho;
-  *w = s.loss == kHuber    ? loss_eval<kHuber, false>(sh, s.delta, d2, id2, &rho)
-       : s.loss == kCauchy ? loss_eval<kCauchy, false>(sh, s.delta, d2, id2, &rho)
-                           : 1.0;
+  g->w = ws.loss == kHuber    ? loss_eval<kHuber, false>(sh, ws.delta, d2, id2, &rho)
+         : ws.loss == kCauchy ? loss_eval<kCauchy, false>(sh, ws.delta, d2, id2, &rho)
+                              : 1.0;
+  g->s = s;
   return true;
+}
+// J_l x (3-vector)
+__device__ __forceinline__ void jl_times(const PairGeo& g, const double x[3], double out[3]) {
+  const double qx = (g.q[0] * x[0] + g.q[1] * x[1] + g.q[2] * x[2]) * g.inv;
+  const double vx = 2.0 * g.lam * (g.v[0] * x[0] + g.v[1] * x[1] + g.v[2] * x[2]) * g.inv;
+  for (int a = 0; a < 3; ++a) out[a] = g.v[a] * (vx - qx) - g.lam * x[a];
+}
+// J_l^T y
+__device__ __forceinline__ void jlt_times(const PairGeo& g, const double y[3], double out[3]) {
+  const double vy = (g.v[0] * y[0] + g.v[1] * y[1] + g.v[2] * y[2]) * g.inv;
+  for (int a = 0; a < 3; ++a) out[a] = -g.q[a] * vy + 2.0 * g.lam * g.v[a] * vy - g.lam * y[a];
+}
+// J_c x for the camera direction x (9)
+__device__ __forceinline__ void jc_times(const PairGeo& g, const double* cam, const double* x, double out[3]) {
+  const double bd = x[6] + g.s * x[7] + g.s * g.s * x[8];
+  double z[3] = {x[1] * g.q[2] - x[2] * g.q[1] + cam[2] * bd,  // x_theta x q + R e3 (b . x_d)
+                 x[2] * g.q[0] - x[0] * g.q[2] + cam[5] * bd,
+                 x[0] * g.q[1] - x[1] * g.q[0] + cam[8] * bd};
+  const double vz = (g.v[0] * z[0] + g.v[1] * z[1] + g.v[2] * z[2]) * g.inv;
+  double jt[3];
+  jl_times(g, x + 3, jt);
+  for (int a = 0; a < 3; ++a) out[a] = z[a] - g.v[a] * vz - jt[a];
+}
+// J_c^T y (9), accumulated into acc
+__device__ __forceinline__ void jct_times_add(const PairGeo& g, const double* cam, const double y[3], double* acc) {
+  const double vy = (g.v[0] * y[0] + g.v[1] * y[1] + g.v[2] * y[2]) * g.inv;
+  const double py[3] = {y[0] - g.v[0] * vy, y[1] - g.v[1] * vy, y[2] - g.v[2] * vy};  // Pi y
+  acc[0] += g.q[1] * py[2] - g.q[2] * py[1];  // q x Pi y
+  acc[1] += g.q[2] * py[0] - g.q[0] * py[2];
+  acc[2] += g.q[0] * py[1] - g.q[1] * py[0];
+  double jt[3];
+  jlt_times(g, y, jt);
+  acc[3] -= jt[0];
+  acc[4] -= jt[1];
+  acc[5] -= jt[2];
+  const double rp = cam[2] * py[0] + cam[5] * py[1] + cam[8] * py[2];  // R e3 . Pi y
+  acc[6] += rp;
+  acc[7] += g.s * rp;
+  acc[8] += g.s * g.s * rp;
 }
 
 __global__ void k_cs_points(const double* __restrict__ V, const double* __restrict__ gl, int64_t N, double xi,
@@ -685,16 +741,15 @@ __global__ void k_cs_pass1_obs(WSrc ws, const int32_t* __restrict__ obs_cam, con
   if (!intra(ws.part, i, j)) return;  // W_k = 0
   const double* vi = v + 9 * (size_t)i;
   if (!ws.W) {  // w J_l^T (J_c v)
-    double Jc[27], Jl[9], w;
     const double l[3] = {ws.pts[3 * (size_t)j], ws.pts[3 * (size_t)j + 1], ws.pts[3 * (size_t)j + 2]};
-    if (!get_J(ws, ws.uv[k], ws.cams + 15 * (size_t)i, l, Jc, Jl, &w)) return;
-    double y[3];
-    for (int r = 0; r < 3; ++r) {
-      double x = 0.0;
-      for (int a = 0; a < 9; ++a) x += Jc[9 * r + a] * vi[a];
-      y[r] = w * x;
-    }
-    for (int c = 0; c < 3; ++c) atomicAdd(t + 3 * (size_t)j + c, Jl[c] * y[0] + Jl[3 + c] * y[1] + Jl[6 + c] * y[2]);
+    const double* cam = ws.cams + 15 * (size_t)i;
+    PairGeo g;
+    if (!get_geo(ws, ws.uv[k], cam, l, &g)) return;
+    double y[3], o[3];
+    jc_times(g, cam, vi, y);
+    for (int r = 0; r < 3; ++r) y[r] *= g.w;
+    jlt_times(g, y, o);
+    for (int c = 0; c < 3; ++c) atomicAdd(t + 3 * (size_t)j + c, o[c]);
     return;
   }
   double Wk[27];
@@ -723,15 +778,14 @@ __global__ void __launch_bounds__(256) k_cs_pass1_pts(WSrc ws, PtOrder po, int64
     if (!intra(ws.part, i, j)) continue;  // W_k = 0
     const double* vi = v + 9 * (size_t)i;
     if (!ws.W) {  // w J_l^T (J_c v)
-      double Jc[27], Jl[9], w;
-      if (!get_J(ws, po.uv[o], ws.cams + 15 * (size_t)i, l, Jc, Jl, &w)) continue;
-      double y[3];
-      for (int r = 0; r < 3; ++r) {
-        double x = 0.0;
-        for (int a = 0; a < 9; ++a) x += Jc[9 * r + a] * vi[a];
-        y[r] = w * x;
-      }
-      for (int c = 0; c < 3; ++c) acc[c] += Jl[c] * y[0] + Jl[3 + c] * y[1] + Jl[6 + c] * y[2];
+      const double* cam = ws.cams + 15 * (size_t)i;
+      PairGeo g;
+      if (!get_geo(ws, po.uv[o], cam, l, &g)) continue;
+      double y[3], q[3];
+      jc_times(g, cam, vi, y);
+      for (int r = 0; r < 3; ++r) y[r] *= g.w;
+      jlt_times(g, y, q);
+      for (int c = 0; c < 3; ++c) acc[c] += q[c];
       continue;
     }
     const double* Wk = ws.W + 27 * (size_t)po.k[o];
@@ -765,13 +819,13 @@ __global__ void __launch_bounds__(kCoarseThreads, 4) k_cs_pass2(const double* __
     double u[3];
     for (int c = 0; c < 3; ++c) u[c] = Vi[3 * c] * tj[0] + Vi[3 * c + 1] * tj[1] + Vi[3 * c + 2] * tj[2];
     if (!ws.W) {  // w J_c^T (J_l u)
-      double Jc[27], Jl[9], w;
       const double l[3] = {ws.pts[3 * (size_t)j], ws.pts[3 * (size_t)j + 1], ws.pts[3 * (size_t)j + 2]};
-      if (!get_J(ws, ws.uv[k], scam, l, Jc, Jl, &w)) continue;
+      PairGeo g;
+      if (!get_geo(ws, ws.uv[k], scam, l, &g)) continue;
       double y[3];
-      for (int r = 0; r < 3; ++r) y[r] = w * (Jl[3 * r] * u[0] + Jl[3 * r + 1] * u[1] + Jl[3 * r + 2] * u[2]);
-#pragma unroll
-      for (int a = 0; a < 9; ++a) acc[a] += Jc[a] * y[0] + Jc[9 + a] * y[1] + Jc[18 + a] * y[2];
+      jl_times(g, u, y);
+      for (int r = 0; r < 3; ++r) y[r] *= g.w;
+      jct_times_add(g, scam, y, acc);
       continue;
     }
     double Wk[27];
