@@ -50,12 +50,14 @@ for nd in ndevs:
               deterministic=int(os.environ.get("COARSE_DET", "0")))
     part = dict(cam_dev=t(cd, torch.int32), pt_dev=t(pd, torch.int32), ndev=nd) if nd > 1 else {}
     daba.coarse_run_part(c0.clone(), l0.clone(), *args, 1, **part, **kw)  # warm-up
-    cams, pts = c0.clone(), l0.clone()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    tr, trials = daba.coarse_run_part(cams, pts, *args, n, **part, **kw)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = float("inf")
+    for rep in range(2):  # the faster of two runs (clocks vary under the power cap after the finest runs)
+        cams, pts = c0.clone(), l0.clone()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr, trials = daba.coarse_run_part(cams, pts, *args, n, **part, **kw)
+        torch.cuda.synchronize()
+        dt = min(dt, time.perf_counter() - t0)
     F_end = float(daba.coarse_blocks(cams, pts, args[1], args[2], args[3], loss=p.loss, scale=p.loss_scale)[5].sum())
     hit = np.flatnonzero(np.asarray(Ftr) <= F_end)
     k = int(hit[0]) if hit.size else None
