@@ -330,9 +330,10 @@ def main():
     dms, dl = kt[dname]
     per_launch_ms = dms / max(dl, 1)
     traffic, fp64_pipe = None, None
-    try:
-        tj = json.load(open(TRAFFIC)).get(dname, {})
-        traffic, fp64_pipe = tj.get("dram_bytes_per_launch"), tj.get("fp64_pipe_pct")
+    try:  # (captured on the single-GPU Final-13682 workload: it applies only to that launch)
+        if world == 1 and a.config == "final13682":
+            tj = json.load(open(TRAFFIC)).get(dname, {})
+            traffic, fp64_pipe = tj.get("dram_bytes_per_launch"), tj.get("fp64_pipe_pct")
     except Exception:
         pass
     roof = None
