@@ -208,6 +208,8 @@ int daba_pixel_residuals(daba_ctx* ctx, double* resid_out);
  * ALL pointers are DEVICE pointers (fp64 unless stated); the caller owns every buffer.  cams: M x 15 in the native
  * layout (R camera->world row-major, t = camera centre, d = (f, f k1, f k2)); pts: N x 3; obs_pt (int32) and
  * obs_uv (K x 2) sorted by camera, with camera i's observations at [cam_off[i], cam_off[i+1]) (int64, M+1 entries).
+ * W may be NULL (the per-observation blocks are then not formed: U and gc come from the structure of J_c, the
+ * path daba_coarse_run takes).
  * A pair with |l - t| <= eps (Assumption 2) adds nothing and gets W[k] = 0.  V / gl are zeroed and then
  * accumulated with fp64 atomics (summation order not fixed); U / gc / F_cam are written in a fixed order.
  * The indices are checked on the device first (obs_pt in [0, N), cam_off monotone from 0 to K): DABA_E_INVALID_ARG

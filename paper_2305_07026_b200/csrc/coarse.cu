@@ -124,7 +124,7 @@ __device__ __forceinline__ bool pair_jacobians(const double* __restrict__ cam, c
 // (exact: P is quadratic in the residual), 2 w J^T J and 2 w J^T (R e / 2) with J = [-[q]x, lam I, R e3 b^T]; the
 // point side adds Q_ij's, 2 w lam^2 I and -w lam R e (eq. Q: Q = w |lam l - g|^2 + a/2, lam l_hat - g = -R e / 2);
 // W_k = 0 (the pair couples no two variables of one device).
-template <int LOSS>
+template <int LOSS, bool SW>
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
     const double* __restrict__ cams, const double* __restrict__ pts, const int32_t* __restrict__ obs_pt,
     const double2* __restrict__ uv, const int64_t* __restrict__ cam_off, double delta, double eps2, Part part,
@@ -151,25 +151,113 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_blocks(
       Fsum += 0.5 * rho;  // P + Q = F at the anchor (Prop. 1)
       const double s = uv[k].x * uv[k].x + uv[k].y * uv[k].y;
       const double b[3] = {1.0, s, s * s};
-      // J = [-[q]x, lam I, R e3 b^T] (3 x 9, row-major)
-      double J[27];
-      const double mq[9] = {0, q[2], -q[1], -q[2], 0, q[0], q[1], -q[0], 0};
-      for (int a = 0; a < 3; ++a)
-        for (int c = 0; c < 3; ++c) {
-          J[9 * a + c] = mq[3 * a + c];
-          J[9 * a + 3 + c] = a == c ? lam : 0.0;
-          J[9 * a + 6 + c] = scam[3 * a + 2] * b[c];
+      // 2 w J^T J and w J^T R e for J = [M, lam I, R e3 b^T], M = -[q]x, from its structure:
+      //   M^T M = |q|^2 I - q q^T,  M^T (lam I) = lam [q]x,  M^T R e3 = q x R e3,  lam^2 I,  lam R e3 b^T,
+      //   |R e3|^2 b b^T;  J^T R e = (q x R e, lam R e, (R e3 . R e) b)
+      const double r3[3] = {scam[2], scam[5], scam[8]};
+      const double q3[3] = {q[1] * r3[2] - q[2] * r3[1], q[2] * r3[0] - q[0] * r3[2], q[0] * r3[1] - q[1] * r3[0]};
+      const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+      const double n3 = r3[0] * r3[0] + r3[1] * r3[1] + r3[2] * r3[2];
+      const double w2 = 2.0 * w, w2l = w2 * lam;
+      const double qx[9] = {0.0, -q[2], q[1], q[2], 0.0, -q[0], -q[1], q[0], 0.0};  // [q]x (row a, column c)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int c = 0; c <= a; ++c) {
+          acc[tri9(a, c)] += w2 * ((a == c ? qq : 0.0) - q[a] * q[c]);
+          acc[tri9(6 + a, 6 + c)] += w2 * n3 * b[a] * b[c];
         }
+        acc[tri9(3 + a, 3 + a)] += w2l * lam;
 #pragma unroll
-      for (int a = 0; a < 9; ++a) {
+        for (int c = 0; c < 3; ++c) {
+          acc[tri9(3 + a, c)] += w2l * qx[3 * c + a];  // (lam [q]x)^T: row t_a, column theta_c
+          acc[tri9(6 + a, c)] += w2 * q3[c] * b[a];
+          acc[tri9(6 + a, 3 + c)] += w2l * r3[c] * b[a];
+        }
+      }
+      acc[45 + 0] += w * (q[1] * Re[2] - q[2] * Re[1]);
+      acc[45 + 1] += w * (q[2] * Re[0] - q[0] * Re[2]);
+      acc[45 + 2] += w * (q[0] * Re[1] - q[1] * Re[0]);
+      const double r3e = r3[0] * Re[0] + r3[1] * Re[1] + r3[2] * Re[2];
 #pragma unroll
-        for (int c = 0; c <= a; ++c) acc[tri9(a, c)] += 2.0 * w * (J[a] * J[c] + J[9 + a] * J[9 + c] + J[18 + a] * J[18 + c]);
-        acc[45 + a] += w * (J[a] * Re[0] + J[9 + a] * Re[1] + J[18 + a] * Re[2]);
+      for (int a = 0; a < 3; ++a) {
+        acc[48 + a] += w * lam * Re[a];
+        acc[51 + a] += w * r3e * b[a];
       }
       if (V)  // the point side, Q_ij (else k_coarse_pts)
         for (int a = 0; a < 3; ++a) {
           atomicAdd(V + 9 * (size_t)j + 4 * a, 2.0 * w * lam * lam);
           atomicAdd(gl + 3 * (size_t)j + a, -w * lam * Re[a]);
+        }
+      continue;
+    }
+    if (!SW) {
+      // Without the per-observation W blocks, U and g_c come from the structure of J_c = [Pi M, -J_l, Pi R e3 b^T]
+      // (M = -[q]x, Pi = I - v v^T inv, J_l = -lam Pi - v r^T inv, Pi v = 0, Pi r = r):
+      //   M^T Pi M = |q|^2 I - q q^T - (q x v)(q x v)^T inv,  (Pi M)^T (-J_l) = lam ([q]x - (q x v) v^T inv),
+      //   (Pi M)^T Pi R e3 = q x Pi R e3,  J_l^T J_l = lam^2 Pi + r r^T inv,  (-J_l)^T Pi R e3 = lam Pi R e3,
+      //   (Pi R e3)^T Pi R e3 = R e3 . Pi R e3;  J_c^T r = (q x r, lam r, (R e3 . r) b)
+      // -- the same blocks as the explicit products below, with about 40% fewer FLOP and no J_c array.
+      const double2 uk = uv[k];
+      const double s = uk.x * uk.x + uk.y * uk.y;
+      const double pz = scam[12] + scam[13] * s + scam[14] * s * s;  // eq. ray
+      double q[3], v[3];
+      for (int a = 0; a < 3; ++a) {
+        q[a] = scam[3 * a] * uk.x + scam[3 * a + 1] * uk.y + scam[3 * a + 2] * pz;
+        v[a] = l[a] - scam[9 + a];
+      }
+      const double nv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+      if (!(nv > eps2)) continue;  // R-N3d: the pair contributes nothing
+      const double inv = 1.0 / nv;
+      const double lam = (v[0] * q[0] + v[1] * q[1] + v[2] * q[2]) * inv;  // eq. lambdaij
+      double rr[3];
+      for (int a = 0; a < 3; ++a) rr[a] = q[a] - lam * v[a];  // R e (eq. error)
+      const double sh = rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+      double rho = 0.0;
+      const double w = loss_eval<LOSS, true>(sh, delta, delta2, idelta2, &rho);  // R-N3a
+      Fsum += 0.5 * rho;                                                        // eq. Fij
+      const double b[3] = {1.0, s, s * s};
+      const double r3[3] = {scam[2], scam[5], scam[8]};
+      const double qv[3] = {q[1] * v[2] - q[2] * v[1], q[2] * v[0] - q[0] * v[2], q[0] * v[1] - q[1] * v[0]};
+      const double vr3 = (v[0] * r3[0] + v[1] * r3[1] + v[2] * r3[2]) * inv;
+      const double pr3[3] = {r3[0] - v[0] * vr3, r3[1] - v[1] * vr3, r3[2] - v[2] * vr3};  // Pi R e3
+      const double qp[3] = {q[1] * pr3[2] - q[2] * pr3[1], q[2] * pr3[0] - q[0] * pr3[2], q[0] * pr3[1] - q[1] * pr3[0]};
+      const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+      const double rp = r3[0] * pr3[0] + r3[1] * pr3[1] + r3[2] * pr3[2];
+      const double wi = w * inv, wl = w * lam, wll = wl * lam;
+      // [q]x (row a, column c)
+      const double qx[9] = {0.0, -q[2], q[1], q[2], 0.0, -q[0], -q[1], q[0], 0.0};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int c = 0; c <= a; ++c) {
+          acc[tri9(a, c)] += w * ((a == c ? qq : 0.0) - q[a] * q[c]) - wi * qv[a] * qv[c];  // theta theta
+          acc[tri9(3 + a, 3 + c)] += wll * ((a == c ? 1.0 : 0.0) - v[a] * v[c] * inv) + wi * rr[a] * rr[c];  // t t
+          acc[tri9(6 + a, 6 + c)] += w * rp * b[a] * b[c];  // d d
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[tri9(3 + a, c)] += wl * (qx[3 * c + a] - qv[c] * v[a] * inv);  // t theta
+          acc[tri9(6 + a, c)] += w * qp[c] * b[a];                           // d theta
+          acc[tri9(6 + a, 3 + c)] += wl * pr3[c] * b[a];                      // d t
+        }
+      }
+      acc[45 + 0] += w * (q[1] * rr[2] - q[2] * rr[1]);  // g_c = w J_c^T r
+      acc[45 + 1] += w * (q[2] * rr[0] - q[0] * rr[2]);
+      acc[45 + 2] += w * (q[0] * rr[1] - q[1] * rr[0]);
+      const double r3r = r3[0] * rr[0] + r3[1] * rr[1] + r3[2] * rr[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[48 + a] += wl * rr[a];
+        acc[51 + a] += w * r3r * b[a];
+      }
+      if (V)  // the point side: V += w J_l^T J_l = w (lam^2 Pi + r r^T inv), g_l += w J_l^T r = -w lam r
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+#pragma unroll
+          for (int c = 0; c <= a; ++c)
+            atomicAdd(V + 9 * (size_t)j + 3 * a + c, wll * ((a == c ? 1.0 : 0.0) - v[a] * v[c] * inv) + wi * rr[a] * rr[c]);
+          atomicAdd(gl + 3 * (size_t)j + a, -wl * rr[a]);
         }
       continue;
     }
@@ -361,12 +449,18 @@ int coarse_blocks_impl(const double* cams, int64_t M, const double* pts, int64_t
   double *Va = det ? nullptr : V, *gla = det ? nullptr : gl;
   if (M > 0) {
     const dim3 g((unsigned)M), b(kCoarseThreads);
-    if (loss == kHuber)
-      k_coarse_blocks<kHuber><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
-    else if (loss == kCauchy)
-      k_coarse_blocks<kCauchy><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
-    else
-      k_coarse_blocks<kTrivial><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam);
+#define DABA_BLOCKS(L, SW_) \
+  k_coarse_blocks<L, SW_><<<g, b, 0, st>>>(cams, pts, obs_pt, uv, cam_off, scale, eps2, part, U, gc, Va, gla, W, F_cam)
+    if (W) {
+      if (loss == kHuber) DABA_BLOCKS(kHuber, true);
+      else if (loss == kCauchy) DABA_BLOCKS(kCauchy, true);
+      else DABA_BLOCKS(kTrivial, true);
+    } else {
+      if (loss == kHuber) DABA_BLOCKS(kHuber, false);
+      else if (loss == kCauchy) DABA_BLOCKS(kCauchy, false);
+      else DABA_BLOCKS(kTrivial, false);
+    }
+#undef DABA_BLOCKS
   }
   if (N > 0 && !det) k_coarse_mirror<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(V, N);
   if (N > 0 && det) {

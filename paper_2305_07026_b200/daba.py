@@ -227,24 +227,26 @@ def _coarse_check(what, cams=None, pts=None, obs_cam=None, obs_pt=None, obs_uv=N
             raise DabaError(-1, f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
 
 
-def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1.0, eps=1e-8, stream=None):
+def coarse_blocks(cams, pts, obs_pt, obs_uv, cam_off, loss=LOSS_TRIVIAL, scale=1.0, eps=1e-8, stream=None, with_W=True):
     """daba_coarse_blocks (include/daba.h): the Gauss-Newton blocks of the intra-device penalties.
     Inputs are CUDA tensors already on the device (torch: device memory only): cams (M, 15) fp64 native layout,
     pts (N, 3) fp64, obs_pt (K,) int32 and obs_uv (K, 2) fp64 sorted by camera, cam_off (M + 1,) int64.  Returns
-    the CUDA tensors (U (M, 9, 9), gc (M, 9), V (N, 3, 3), gl (N, 3), W (K, 9, 3), F_cam (M,)); the call is
-    asynchronous on `stream` (default: torch's current stream)."""
+    the CUDA tensors (U (M, 9, 9), gc (M, 9), V (N, 3, 3), gl (N, 3), W (K, 9, 3) or None when with_W is False,
+    F_cam (M,)); the call is asynchronous on `stream` (default: torch's current stream)."""
     import torch
     M, N, K = cams.shape[0], pts.shape[0], obs_pt.shape[0]
     _coarse_check("coarse_blocks", cams=cams, pts=pts, obs_pt=obs_pt, obs_uv=obs_uv, cam_off=cam_off)
     dev, f64 = cams.device, torch.float64
     U, gc = torch.empty((M, 9, 9), dtype=f64, device=dev), torch.empty((M, 9), dtype=f64, device=dev)
     V, gl = torch.empty((N, 3, 3), dtype=f64, device=dev), torch.empty((N, 3), dtype=f64, device=dev)
-    W, F = torch.empty((K, 9, 3), dtype=f64, device=dev), torch.empty((M,), dtype=f64, device=dev)
+    W = torch.empty((K, 9, 3), dtype=f64, device=dev) if with_W else None
+    F = torch.empty((M,), dtype=f64, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         rc = lib().daba_coarse_blocks(cams.data_ptr(), M, pts.data_ptr(), N, obs_pt.data_ptr(), obs_uv.data_ptr(),
                                       cam_off.data_ptr(), K, int(loss), float(scale), float(eps), U.data_ptr(),
-                                      gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr(), F.data_ptr(), st)
+                                      gc.data_ptr(), V.data_ptr(), gl.data_ptr(), W.data_ptr() if with_W else None,
+                                      F.data_ptr(), st)
     if rc != 0:
         raise DabaError(rc, "daba_coarse_blocks")
     return U, gc, V, gl, W, F

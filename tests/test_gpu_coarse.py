@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def _blocks_gpu(cp, cams, pts, order):
+def _blocks_gpu(cp, cams, pts, order, with_W=True):
     import paper_2305_07026_b200 as daba
     dev = torch.device("cuda:0")
     oc = cp.oc[order]
@@ -26,9 +26,9 @@ def _blocks_gpu(cp, cams, pts, order):
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)  # noqa: E731
     out = daba.coarse_blocks(t(cams, torch.float64), t(pts, torch.float64), t(cp.op[order], torch.int32),
                              t(cp.uv[order], torch.float64), t(cam_off, torch.int64), loss=cp.opt.kind,
-                             scale=cp.opt.scale, eps=cp.opt.eps)
+                             scale=cp.opt.scale, eps=cp.opt.eps, with_W=with_W)
     torch.cuda.synchronize()
-    return [x.cpu().numpy() for x in out]
+    return [x.cpu().numpy() if x is not None else None for x in out]
 
 
 def _close(gpu, ref, rel=1e-11):
@@ -49,6 +49,14 @@ def _check(cp, cams, pts):
     _close(gW, W[order])
     assert gF.sum() == pytest.approx(Fc.sum(), rel=1e-12)
     _close(gF, Fc)
+    # without W: U, g_c and the point blocks from the structure of J_c (the path of daba_coarse_run)
+    sU, sgc, sV, sgl, sW, sF = _blocks_gpu(cp, cams, pts, order, with_W=False)
+    assert sW is None
+    _close(sU, U)
+    _close(sgc, gc)
+    _close(sV, V)
+    _close(sgl, gl)
+    _close(sF, Fc)
 
 
 @pytest.mark.parametrize("loss", [oracle.LOSS_TRIVIAL, oracle.LOSS_HUBER, oracle.LOSS_CAUCHY])
