@@ -1,3 +1,5 @@
+"""NEXT-3 phase timing on Final-13682 (round-1 helper): daba_coarse_blocks, daba_coarse_solve with the stored W,
+and daba_coarse_run over 1 / 2 iterations (host clock)."""
 import os, sys, time, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import gen, paper_2305_07026_b200 as daba
