@@ -117,7 +117,7 @@ __device__ __forceinline__ void extrapolate_camera(const double* ck, const doubl
 //  14 w lam ux  15 w lam uy  16-18 w lam s^m  19 w lam^2
 //  20-22 w e ux  23-25 w e uy  26-28 w e  29-31 w e s  32-34 w e s^2  35-37 w lam e   (e = R e, world frame;
 //        k_cam_solve rotates them into the anchor camera frame: the camera pass never applies R^T)
-//  38 w |e|^2   39 a   [40 degenerate pairs]
+//  38 (unused: 0)   39 rho / 2 = a + w |e|^2 / 2   [40 degenerate pairs]
 // Camera record kept in shared memory and re-read at every use (volatile shared loads are not hoisted into
 // registers): frees ~30 registers per thread in the camera pass, i.e. more resident CTAs per SM (a copy in
 // registers measured 0.80 ms with spills at 6 CTAs/SM, 0.86 ms at 4).
@@ -183,10 +183,8 @@ __device__ __forceinline__ void obs_moments(const IterParams& p, double2 u, doub
   acc[35] = fma(wl, ex, acc[35]);
   acc[36] = fma(wl, ey, acc[36]);
   acc[37] = fma(wl, ez, acc[37]);
-  if (!ACC) {
-    acc[38] = fma(w, sh, acc[38]);
-    acc[39] += 0.5 * fma(-w, sh, rho);  // eq. a
-  }
+  if (!ACC)  // F_i = sum (a + w |e|^2 / 2) = sum rho / 2 (eqs. a, Fij): one accumulator (slot 38 stays 0)
+    acc[39] = fma(0.5, rho, acc[39]);
   // point side of the same pair: (w lam^2, w lam R e) with the world-frame error R e (eq. Q's sums), written
   // coalesced at the camera-side index (one 32-byte record per anchor)
   if (rec >= 0)
@@ -1029,7 +1027,7 @@ __global__ void __launch_bounds__(128) k_cam_solve(IterParams p) {
       dt[k] = ca[9 + k] - th[k];
       dd[k] = ca[12 + k] - dh[k];
     }
-    q[0] = m[39] + 0.5 * m[38];  // F_i = sum (a + w |e|^2 / 2) = sum rho / 2
+    q[0] = m[39];  // F_i = sum rho / 2 (slot 38 unused)
     q[1] = delta_P(Rh, S, dR, dt, dd, p.xi);
     q[2] = dP_acc;
     double sa = 0, sm = 0;
