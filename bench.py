@@ -36,12 +36,12 @@ FP64_FLOPS_PEAK = 2 * 17.71e12
 #   bytes: K * 20 (u 16 B + point index 4 B) + N * 96 (read l^k and l^{k-1}, write l_acc and l_mm; 24 B each)
 #          + M * 500 (camera copies and moments)
 #   k_cam_pass's own share: K * 20 + N * 48 (reads the two anchors' points once) + M * 256 (the two anchor cameras)
-#   FP64: 152.5 FLOP per observation and anchor in k_cam_pass — ncu SASS opcode counts of one launch on
-#   Final-13682 (DFMA 58.59 x 2 + DMUL 24.74 + DADD 10.59 thread instructions per observation and anchor;
-#   profiles/r02_cam_pass_sass_counts.txt), i.e. 305.0 FLOP per observation and iteration.
+#   FP64: 150.5 FLOP per observation and anchor in k_cam_pass — ncu SASS opcode counts of one launch on
+#   Final-13682 (DFMA 57.58 x 2 + DMUL 24.74 + DADD 10.59 thread instructions per observation and anchor;
+#   profiles/r02_cam_pass_sass_counts.txt), i.e. 301.0 FLOP per observation and iteration.
 ALG_BYTES_ITER = lambda K, N, M: 20 * K + 96 * N + 500 * M
 ALG_BYTES = {"k_cam_pass": lambda K, N, M: 20 * K + 48 * N + 256 * M}
-FLOP_PER_ANCHOR_OBS = 152.5
+FLOP_PER_ANCHOR_OBS = 150.5
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
